@@ -1,0 +1,136 @@
+/*
+ * divas_b200.h -- C ABI of the B200-native DivAS fusion hot path.
+ *
+ * One shared library, libdivas_b200.so (sm_100a), built from
+ * paper_2601_04860_b200/csrc/.  Plain pointers and sizes only: every array
+ * argument is a DEVICE pointer (CUDA global memory, C-contiguous, 16-byte
+ * aligned unless stated), `stream` is a cudaStream_t passed as void*, and the
+ * caller owns every buffer ("Ownership").  The library
+ * keeps no mutable global state: all scratch lives in a caller-provided
+ * workspace, so calls are re-entrant across threads and streams.
+ *
+ * Every entry point returns 0 on success or a nonzero DIVAS_E* code; the
+ * message of the calling thread's last failure is divas_last_error().
+ * Kernels are enqueued asynchronously on `stream`; nothing synchronises.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/divas/):
+ *   divas_refine         <- segmenter.refine_mask            segmenter.py:129-152
+ *   divas_fuse           <- fusion._gradient_maps + fusion._fuse_kernel
+ *                           (the numba operator that fusion.fuse calls)
+ *                                                           fusion.py:684-689, :493-509, :720-723
+ *   divas_gradient_maps  <- fusion._gradient_maps            fusion.py:684-689
+ *   divas_threshold      <- `ogrid.probs >= threshold` + np.argwhere
+ *                                                           ablation.py:109
+ *   divas_overlay        <- fusion._overlay_kernel           fusion.py:771-843
+ */
+#ifndef DIVAS_B200_H
+#define DIVAS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DIVAS_ABI_VERSION 1
+
+/* error codes */
+#define DIVAS_OK          0
+#define DIVAS_EINVAL      1   /* bad argument (shape, size, null pointer)   */
+#define DIVAS_ECUDA       2   /* CUDA launch / runtime failure              */
+#define DIVAS_EWORKSPACE  3   /* workspace too small                        */
+
+/* Per-view camera record, DIVAS_CAM_STRIDE doubles per view, in device
+ * memory:  r[9] (world_from_camera[:3,:3] row-major; columns are the camera
+ * axes in world, geometry.py:61-64), pos[3] (world_from_camera[:3,3]),
+ * fx, fy, cx, cy, width, height  (fusion.py:671-673, :444-451). */
+#define DIVAS_CAM_STRIDE 18
+
+/* FusionParams.as_vector() layout (fusion.py:80-87). */
+#define DIVAS_NPARAM 14
+
+/* Views are stored as padded SoA planes [nv][hm][wm] exactly as
+ * fusion._pack_views builds them (fusion.py:653-681): (hm, wm) is the largest
+ * view, smaller views sit in the top-left corner, padding is zero.  The valid
+ * flag is derived as n_samples > 0 (render.py:67-69). */
+
+/* ---------------------------------------------------------------------- */
+/* Refinement: out = clip(mask * (1 - zhat), 0, 1) on valid pixels, 0 else, */
+/* zhat min-max normalised over each view's valid pixels (Eq. 2).           */
+/* ---------------------------------------------------------------------- */
+size_t divas_refine_workspace_size(int32_t nv);
+int divas_refine(int32_t nv, int64_t hm, int64_t wm,
+                 const float *mask, const float *z_surface, const int32_t *n_samples,
+                 float *out, void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Fusion                                                                   */
+/* ---------------------------------------------------------------------- */
+typedef struct divas_fuse_args {
+    int64_t g;                   /* grid resolution G (voxels per axis)       */
+    double origin[3];            /* grid min corner (VoxelGrid.origin)        */
+    double dx_vox;               /* VoxelGrid.voxel_size()                    */
+    const float *density;        /* [G^3] rho, [ix,iy,iz] C-order             */
+    int32_t nv;                  /* number of views (>= 1)                    */
+    int32_t hm, wm;              /* padded plane height / width               */
+    const double *cams;          /* [nv][DIVAS_CAM_STRIDE]                    */
+    const float *masks;          /* [nv][hm][wm] refined confidences          */
+    const float *dmins, *dmaxs, *dexps;   /* [nv][hm][wm]                     */
+    const int32_t *nsamps;       /* [nv][hm][wm]                              */
+    double pv[DIVAS_NPARAM];     /* FusionParams.as_vector()                  */
+    double bc[3], bh[3];         /* SceneBounds centre / half (fusion.py:542) */
+    int32_t unbounded;           /* spherical contraction on/off              */
+    int64_t vox_lo, vox_hi;      /* flat voxel range [lo, hi) to fuse (a slab) */
+    double *probs;               /* [G^3] out, written on [lo, hi)            */
+    int32_t *n_thick, *n_thin;   /* [G^3] integer votes, or NULL              */
+    double *sw, *smw, *st;       /* [G^3] sorted sums, or NULL                */
+    uint8_t *occ;                /* [G^3] fused threshold p >= occ_thr, or NULL */
+    double occ_thr;
+} divas_fuse_args;
+
+/* Workspace for divas_fuse over `n_vox` voxels (the slab length). */
+size_t divas_fuse_workspace_size(int64_t n_vox, int32_t nv);
+int divas_fuse(const divas_fuse_args *args, void *workspace, size_t workspace_bytes,
+               void *stream);
+
+/* Number of voxels that passed the exact density gate in the last
+ * divas_fuse that used `workspace` (device pointer to one int64). */
+const int64_t *divas_fuse_gated_count(const void *workspace);
+
+/* The f64 depth-gradient maps of fusion._gradient_maps on the padded planes
+ * (divas_fuse computes g on the fly; this export is for parity tests). */
+int divas_gradient_maps(int32_t nv, int32_t hm, int32_t wm, const float *dexps,
+                        const float *dmins, const float *dmaxs, const int32_t *nsamps,
+                        double eps, double kappa, double *out, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Threshold / extract: occ[i] = p[i] >= thr;  idx = C-order indices of the */
+/* set voxels (np.argwhere order), written as (ix,iy,iz) int64 triples when */
+/* g > 0 (needs n == g^3) or as flat int64 indices when g == 0.  *count     */
+/* (device int64) receives the number of set voxels.  occ / idx may be NULL.*/
+/* ---------------------------------------------------------------------- */
+size_t divas_threshold_workspace_size(int64_t n);
+int divas_threshold(const double *p, int64_t n, double thr, int64_t g,
+                    uint8_t *occ, int64_t *idx, int64_t *count,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Overlay: binary mask of pixels whose ray meets a voxel with p >= thr     */
+/* (project_grid_overlay).  cam: one DIVAS_CAM_STRIDE record; dmin/dmax/    */
+/* nsamp: [h][w] planes of the view; probs: [G^3]; out: [h][w] uint8.       */
+/* ---------------------------------------------------------------------- */
+int divas_overlay(const double *cam, int32_t h, int32_t w, const float *dmin,
+                  const float *dmax, const int32_t *nsamp, const double *probs,
+                  int64_t g, const double origin[3], double dx_vox,
+                  const double bc[3], const double bh[3], int32_t unbounded,
+                  double thr, uint8_t *out, void *stream);
+
+/* ---------------------------------------------------------------------- */
+const char *divas_last_error(void);
+int divas_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DIVAS_B200_H */

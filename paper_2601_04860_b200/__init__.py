@@ -1,0 +1,25 @@
+"""B200-native DivAS fusion hot path (arxiv 2601.04860).
+
+Depth-weighted mask refinement, multi-view voxel fusion and threshold /
+extract, as hand-written sm_100a CUDA kernels behind a C ABI
+(include/divas_b200.h, libdivas_b200.so) with the reference package's Python
+entry points on top.  See DESIGN.md.
+"""
+
+from .geometry import Camera, SceneBounds, VoxelGrid, look_at
+from .render import ViewGeometry
+from .scene import DensityGrid
+from .segmenter import ConfidenceMask, refine_mask, refine_masks_device
+from .fusion import (DeviceViews, FusionParams, FusionStats, Fuser, OccupancyGrid,
+                     extract, extract_device, fuse, fuse_with_stats, project_grid_overlay,
+                     threshold, threshold_device)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Camera", "SceneBounds", "VoxelGrid", "look_at", "ViewGeometry", "DensityGrid",
+    "ConfidenceMask", "refine_mask", "refine_masks_device",
+    "DeviceViews", "FusionParams", "FusionStats", "Fuser", "OccupancyGrid",
+    "fuse", "fuse_with_stats", "project_grid_overlay",
+    "threshold", "threshold_device", "extract", "extract_device",
+]

@@ -1,0 +1,107 @@
+"""ctypes binding of libdivas_b200.so (the C ABI declared in include/divas_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+present, every compute entry point raises.  Build it with
+``python -m paper_2601_04860_b200.build`` (``__graft_entry__.build()`` does).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libdivas_b200.so")
+
+CAM_STRIDE = 18
+NPARAM = 14
+
+# every symbol include/divas_b200.h declares
+EXPORTS = (
+    "divas_refine_workspace_size", "divas_refine",
+    "divas_fuse_workspace_size", "divas_fuse", "divas_fuse_gated_count",
+    "divas_gradient_maps",
+    "divas_threshold_workspace_size", "divas_threshold",
+    "divas_overlay",
+    "divas_last_error", "divas_abi_version",
+)
+
+_VP = ctypes.c_void_p
+_D3 = ctypes.c_double * 3
+
+
+class FuseArgs(ctypes.Structure):
+    """Mirror of ``divas_fuse_args`` (include/divas_b200.h)."""
+
+    _fields_ = [
+        ("g", ctypes.c_int64), ("origin", _D3), ("dx_vox", ctypes.c_double),
+        ("density", _VP), ("nv", ctypes.c_int32), ("hm", ctypes.c_int32),
+        ("wm", ctypes.c_int32), ("cams", _VP), ("masks", _VP), ("dmins", _VP),
+        ("dmaxs", _VP), ("dexps", _VP), ("nsamps", _VP),
+        ("pv", ctypes.c_double * NPARAM), ("bc", _D3), ("bh", _D3),
+        ("unbounded", ctypes.c_int32), ("vox_lo", ctypes.c_int64), ("vox_hi", ctypes.c_int64),
+        ("probs", _VP), ("n_thick", _VP), ("n_thin", _VP), ("sw", _VP), ("smw", _VP),
+        ("st", _VP), ("occ", _VP), ("occ_thr", ctypes.c_double),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(lib):
+    S, I64, I32, D = ctypes.c_size_t, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+    sig = {
+        "divas_refine_workspace_size": (S, [I32]),
+        "divas_refine": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP, S, _VP]),
+        "divas_fuse_workspace_size": (S, [I64, I32]),
+        "divas_fuse": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, S, _VP]),
+        "divas_fuse_gated_count": (_VP, [_VP]),
+        "divas_gradient_maps": (ctypes.c_int, [I32, I32, I32, _VP, _VP, _VP, _VP, D, D, _VP, _VP]),
+        "divas_threshold_workspace_size": (S, [I64]),
+        "divas_threshold": (ctypes.c_int, [_VP, I64, D, I64, _VP, _VP, _VP, _VP, S, _VP]),
+        "divas_overlay": (ctypes.c_int, [_VP, I32, I32, _VP, _VP, _VP, _VP, I64,
+                                         ctypes.POINTER(D), D, ctypes.POINTER(D),
+                                         ctypes.POINTER(D), I32, D, _VP, _VP]),
+        "divas_last_error": (ctypes.c_char_p, []),
+        "divas_abi_version": (ctypes.c_int, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def lib():
+    """The loaded library; raises if it has not been built (no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build the sm_100a kernels with "
+                    "`python -m paper_2601_04860_b200.build` (there is no CPU fallback)")
+            handle = ctypes.CDLL(LIB_PATH)
+            _declare(handle)
+            _lib = handle
+    return _lib
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = lib().divas_last_error().decode(errors="replace")
+        if rc == 1:
+            raise ValueError(f"{what}: {msg}")
+        raise RuntimeError(f"{what} failed (code {rc}): {msg}")
+
+
+def ptr(t) -> int:
+    """Device pointer of a torch tensor (0 for None)."""
+    return 0 if t is None else int(t.data_ptr())
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

@@ -1,0 +1,169 @@
+// refine.cu -- kernel (a): depth-weighted confidence refinement (paper Eq. 2).
+//
+// Reference: segmenter.refine_mask (/root/reference/pkg/src/divas/segmenter.py:129-152)
+//   valid = n_samples > 0; lo, hi = min, max of z over valid pixels (f64);
+//   zhat = (z - lo) / (hi - lo)  (0 if hi - lo <= 0);
+//   out = clip(f64(mask) * (1 - zhat), 0, 1) on valid pixels, 0 elsewhere; -> f32 RNE.
+//
+// Two launches over all views at once, 128-bit loads:
+//   1. refine_minmax: per-view min/max of z over valid pixels.  min/max are
+//      exact in any order, so blocks reduce in registers + warp shuffles and
+//      publish one order-preserving-key atomicMin/atomicMax per block.
+//   2. refine_apply: the elementwise pass, visiting views in reverse order so
+//      the z / n_samples tiles the reduction read last are still L2-resident.
+// HBM bytes per pixel: 8 (reduction) + 16 (apply) minus the L2 hits.
+#include "common.cuh"
+
+namespace divas {
+
+constexpr int kRefineThreads = 256;
+
+__global__ void refine_init(uint32_t *ws, int nv) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nv) {
+        ws[2 * i] = 0xffffffffu;  // min key
+        ws[2 * i + 1] = 0u;       // max key
+    }
+}
+
+__device__ __forceinline__ void block_minmax_publish(uint32_t kmin, uint32_t kmax, uint32_t *slot) {
+    __shared__ uint32_t s_min[kRefineThreads / 32], s_max[kRefineThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { s_min[warp] = kmin; s_max[warp] = kmax; }
+    __syncthreads();
+    if (warp == 0) {
+        kmin = lane < kRefineThreads / 32 ? s_min[lane] : 0xffffffffu;
+        kmax = lane < kRefineThreads / 32 ? s_max[lane] : 0u;
+        for (int o = 16; o > 0; o >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+        }
+        if (lane == 0 && kmin <= kmax) {
+            atomicMin(slot, kmin);
+            atomicMax(slot + 1, kmax);
+        }
+    }
+}
+
+// grid = (blocks_per_view, nv); VEC = 4 (float4/int4) or 1 (scalar fallback)
+template <int VEC>
+__global__ void __launch_bounds__(kRefineThreads)
+refine_minmax(const float *__restrict__ z, const int32_t *__restrict__ n, int64_t plane,
+              uint32_t *__restrict__ ws) {
+    const int v = blockIdx.y;
+    const float *zv = z + (int64_t)v * plane;
+    const int32_t *nvp = n + (int64_t)v * plane;
+    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    const int64_t nvec = plane / VEC;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (VEC == 4) {
+            const float4 zz = __ldg(reinterpret_cast<const float4 *>(zv) + i);
+            const int4 nn = __ldg(reinterpret_cast<const int4 *>(nvp) + i);
+            if (nn.x > 0) { uint32_t k = f32_key(zz.x); kmin = min(kmin, k); kmax = max(kmax, k); }
+            if (nn.y > 0) { uint32_t k = f32_key(zz.y); kmin = min(kmin, k); kmax = max(kmax, k); }
+            if (nn.z > 0) { uint32_t k = f32_key(zz.z); kmin = min(kmin, k); kmax = max(kmax, k); }
+            if (nn.w > 0) { uint32_t k = f32_key(zz.w); kmin = min(kmin, k); kmax = max(kmax, k); }
+        } else {
+            if (__ldg(nvp + i) > 0) {
+                uint32_t k = f32_key(__ldg(zv + i));
+                kmin = min(kmin, k);
+                kmax = max(kmax, k);
+            }
+        }
+    }
+    block_minmax_publish(kmin, kmax, ws + 2 * v);
+}
+
+__device__ __forceinline__ float refine_px(float m, float z, int32_t n, bool any, double lo,
+                                           double span) {
+    double o = 0.0;
+    if (any && n > 0) {
+        const double zh = span > 0.0 ? ((double)z - lo) / span : 0.0;
+        o = (double)m * (1.0 - zh);
+    }
+    if (o < 0.0) o = 0.0;   // np.clip keeps NaN, so do these compares
+    if (o > 1.0) o = 1.0;
+    return __double2float_rn(o);
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(kRefineThreads)
+refine_apply(const float *__restrict__ mask, const float *__restrict__ z,
+             const int32_t *__restrict__ n, float *__restrict__ out, int64_t plane,
+             const uint32_t *__restrict__ ws) {
+    const int v = gridDim.y - 1 - blockIdx.y;   // reverse view order: L2 reuse
+    const uint32_t kmin = ws[2 * v], kmax = ws[2 * v + 1];
+    const bool any = kmin <= kmax;
+    const double lo = any ? (double)key_f32(kmin) : 0.0;
+    const double hi = any ? (double)key_f32(kmax) : 0.0;
+    const double span = hi - lo;
+    const int64_t off = (int64_t)v * plane;
+    const int64_t nvec = plane / VEC;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (VEC == 4) {
+            const float4 m = __ldg(reinterpret_cast<const float4 *>(mask + off) + i);
+            const float4 zz = __ldg(reinterpret_cast<const float4 *>(z + off) + i);
+            const int4 nn = __ldg(reinterpret_cast<const int4 *>(n + off) + i);
+            float4 o;
+            o.x = refine_px(m.x, zz.x, nn.x, any, lo, span);
+            o.y = refine_px(m.y, zz.y, nn.y, any, lo, span);
+            o.z = refine_px(m.z, zz.z, nn.z, any, lo, span);
+            o.w = refine_px(m.w, zz.w, nn.w, any, lo, span);
+            __stcs(reinterpret_cast<float4 *>(out + off) + i, o);
+        } else {
+            out[off + i] = refine_px(mask[off + i], z[off + i], n[off + i], any, lo, span);
+        }
+    }
+}
+
+static int blocks_per_view(int64_t plane, int nv) {
+    int64_t b = (plane / 4 + 4 * kRefineThreads - 1) / (4 * kRefineThreads);
+    int64_t cap = 4096 / (nv > 0 ? nv : 1);
+    if (cap < 1) cap = 1;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+}  // namespace divas
+
+using namespace divas;
+
+extern "C" size_t divas_refine_workspace_size(int32_t nv) { return (size_t)(nv > 0 ? nv : 1) * 8; }
+
+extern "C" int divas_refine(int32_t nv, int64_t hm, int64_t wm, const float *mask,
+                            const float *z_surface, const int32_t *n_samples, float *out,
+                            void *workspace, size_t workspace_bytes, void *stream) {
+    if (nv <= 0 || hm <= 0 || wm <= 0) { set_error("divas_refine: empty view set"); return DIVAS_EINVAL; }
+    if (nv > 65535) { set_error("divas_refine: too many views (%d)", nv); return DIVAS_EINVAL; }
+    if (!mask || !z_surface || !n_samples || !out || !workspace) {
+        set_error("divas_refine: null pointer");
+        return DIVAS_EINVAL;
+    }
+    if (workspace_bytes < divas_refine_workspace_size(nv)) {
+        set_error("divas_refine: workspace too small");
+        return DIVAS_EWORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t *ws = (uint32_t *)workspace;
+    const int64_t plane = hm * wm;
+    const bool vec = (plane % 4 == 0) &&
+                     ((((uintptr_t)mask) | ((uintptr_t)z_surface) | ((uintptr_t)n_samples) |
+                       ((uintptr_t)out)) & 15) == 0;
+    refine_init<<<(nv + 255) / 256, 256, 0, s>>>(ws, nv);
+    dim3 grid(blocks_per_view(plane, nv), nv);
+    if (vec) {
+        refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
+        refine_apply<4><<<grid, kRefineThreads, 0, s>>>(mask, z_surface, n_samples, out, plane, ws);
+    } else {
+        refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
+        refine_apply<1><<<grid, kRefineThreads, 0, s>>>(mask, z_surface, n_samples, out, plane, ws);
+    }
+    return check_launch("divas_refine");
+}

@@ -1,0 +1,523 @@
+"""Multi-view voxel fusion on the B200 (stages (b) and (c) of the path).
+
+Drop-in for the reference's fusion entry points
+(/root/reference/pkg/src/divas/fusion.py):
+
+* ``FusionParams`` (:46-106) and ``OccupancyGrid`` (:109-123) -- same fields,
+  validation, ``as_vector`` layout and JSON helpers;
+* ``fuse(grid, density, views, params, bounds=None, workers=None,
+  trace_path=None)`` (:692-724) -- same signature, same ValueErrors, same
+  probabilities (integer votes and occupancy bit-exact; p equal to the last
+  bit except where CUDA's ``exp`` and glibc's differ by an ulp in a thick
+  weight);
+* ``project_grid_overlay`` (:846-865);
+* threshold / extract (``probs >= thr`` and ``np.argwhere``, ablation.py:109).
+
+Extensions, not in the reference: ``fuse_with_stats`` (votes and sorted
+sums), ``DeviceViews`` / ``Fuser`` for device-resident repeated fusion and
+slab sharding (``vox_range``), and ``threshold_device`` / ``extract_device``.
+
+All arithmetic runs in libdivas_b200.so (csrc/*.cu); this module validates,
+packs and moves data.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import asdict, dataclass, replace
+
+import numpy as np
+
+from . import _native
+from ._device import as_device, device, empty
+
+__all__ = [
+    "FusionParams", "OccupancyGrid", "FusionStats", "DeviceViews", "Fuser",
+    "fuse", "fuse_with_stats", "project_grid_overlay",
+    "threshold", "extract", "threshold_device", "extract_device", "gradient_maps_device",
+    "pack_cameras", "bounds_arrays",
+]
+
+
+# ---------------------------------------------------------------------------
+# parameter / result types
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class FusionParams:
+    """Kernel hyperparameters (fusion.py:46-106; the code defaults are authoritative)."""
+
+    base_tolerance_multiplier: float = 1.5   # gamma
+    per_sample_bonus: float = 0.5            # beta
+    max_bonus: float = 16.0
+    depth_range_factor: float = 0.1          # lambda_range
+    density_thresh: float = 0.5
+    thin_density_thresh: float = 2.0
+    thin_percent_cover: float = 0.5
+    depth_falloff: float = 4.0               # alpha1
+    thin_accept: float = 0.6
+    eps: float = 1e-8
+    mask_threshold: float = 0.5
+    thin_mask_floor: float = 0.1
+    grad_kappa: float = 1.0
+    enable_thin: bool = True
+
+    def __post_init__(self):
+        for name in ("base_tolerance_multiplier", "per_sample_bonus", "max_bonus",
+                     "depth_range_factor", "density_thresh", "thin_density_thresh",
+                     "thin_percent_cover", "depth_falloff", "eps"):
+            if getattr(self, name) < 0:
+                raise ValueError(f"{name} must be >= 0")
+        if not 0.0 < self.thin_accept < 1.0:
+            raise ValueError("thin acceptance threshold must lie in (0, 1)")
+        if self.mask_threshold != 0.5:
+            raise ValueError("mask threshold is fixed at 0.5")
+
+    def as_vector(self) -> np.ndarray:
+        return np.array([
+            self.base_tolerance_multiplier, self.per_sample_bonus, self.max_bonus,
+            self.depth_range_factor, self.density_thresh, self.thin_density_thresh,
+            self.thin_percent_cover, self.depth_falloff, self.thin_accept,
+            self.eps, self.mask_threshold, self.thin_mask_floor, self.grad_kappa,
+            1.0 if self.enable_thin else 0.0,
+        ], dtype=np.float64)
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "FusionParams":
+        return cls(**d)
+
+    def save(self, path):
+        with open(path, "w") as f:
+            json.dump(self.to_dict(), f, indent=2)
+
+    @classmethod
+    def load(cls, path) -> "FusionParams":
+        with open(path) as f:
+            return cls.from_dict(json.load(f))
+
+    def with_overrides(self, **kw) -> "FusionParams":
+        return replace(self, **kw)
+
+
+@dataclass
+class OccupancyGrid:
+    """Fused probabilities on a VoxelGrid layout, (G, G, G) float64 [ix, iy, iz]."""
+
+    grid: object
+    probs: np.ndarray
+    version: int = 0
+
+    def __post_init__(self):
+        g = self.grid.resolution
+        self.probs = np.asarray(self.probs, dtype=np.float64).reshape(g, g, g)
+
+    def check(self):
+        assert np.all(np.isfinite(self.probs))
+        assert self.probs.min() >= 0.0 and self.probs.max() <= 1.0
+
+
+@dataclass
+class FusionStats:
+    """Per-voxel integer votes and value-sorted sums.
+
+    p == (smw + st) / (sw + n_thin) where that denominator exceeds eps, else 0.
+    """
+
+    n_thick: np.ndarray   # (G,G,G) int32 -- views whose thick path passed
+    n_thin: np.ndarray    # (G,G,G) int32 -- accepted thin scores
+    sw: np.ndarray        # (G,G,G) f64   -- sum of thick depth weights
+    smw: np.ndarray       # (G,G,G) f64   -- sum of m * w
+    st: np.ndarray        # (G,G,G) f64   -- sum of accepted thin scores
+    gated: int            # voxels that passed the exact density gate
+
+
+def _params_vector(params) -> np.ndarray:
+    if hasattr(params, "as_vector"):
+        return np.asarray(params.as_vector(), dtype=np.float64)
+    pv = np.asarray(params, dtype=np.float64)
+    if pv.shape != (_native.NPARAM,):
+        raise ValueError("params vector must have 14 entries")
+    return pv
+
+
+def bounds_arrays(bounds):
+    """(centre, half, unbounded) as the kernel takes them (fusion.py:542-546)."""
+    if bounds is None or not bounds.unbounded:
+        return np.zeros(3), np.ones(3), 0
+    return (np.asarray(bounds.center, dtype=np.float64).reshape(3),
+            np.asarray(bounds.half, dtype=np.float64).reshape(3), 1)
+
+
+def _check_layout(grid, density):
+    """fusion.py:701-704."""
+    if density.grid.resolution != grid.resolution or \
+            not np.allclose(density.grid.origin, grid.origin) or \
+            density.grid.half_extents != grid.half_extents:
+        raise ValueError("density grid layout does not match the fusion grid")
+
+
+# ---------------------------------------------------------------------------
+# device-resident view set
+# ---------------------------------------------------------------------------
+
+def pack_cameras(cameras) -> np.ndarray:
+    """[nv, 18] f64 records: rotation (row-major), position, fx fy cx cy w h."""
+    out = np.zeros((len(cameras), _native.CAM_STRIDE), dtype=np.float64)
+    for i, c in enumerate(cameras):
+        out[i, 0:9] = np.asarray(c.rotation, dtype=np.float64).reshape(9)
+        out[i, 9:12] = np.asarray(c.position, dtype=np.float64).reshape(3)
+        out[i, 12:18] = (c.fx, c.fy, c.cx, c.cy, float(c.width), float(c.height))
+    return out
+
+
+class DeviceViews:
+    """A view set resident in HBM as padded SoA planes ``[nv, hm, wm]``.
+
+    Layout as ``fusion._pack_views`` builds it (fusion.py:653-681): the largest
+    view sets (hm, wm); smaller views occupy the top-left corner; padding is
+    zero (so it is invalid: ``n_samples == 0``).  ``masks`` holds the refined
+    confidences the fusion consumes; ``z_surface`` (optional) lets
+    ``refine()`` produce them on device from ``raw_masks``.
+    """
+
+    def __init__(self, cams, masks, dmins, dmaxs, dexps, nsamps, z_surface=None,
+                 raw_masks=None, sizes=None):
+        self.cams = cams
+        self.masks = masks
+        self.dmins = dmins
+        self.dmaxs = dmaxs
+        self.dexps = dexps
+        self.nsamps = nsamps
+        self.z_surface = z_surface
+        self.raw_masks = raw_masks
+        self.sizes = sizes
+
+    @property
+    def nv(self):
+        return int(self.masks.shape[0])
+
+    @property
+    def hm(self):
+        return int(self.masks.shape[1])
+
+    @property
+    def wm(self):
+        return int(self.masks.shape[2])
+
+    @property
+    def device(self):
+        return self.masks.device
+
+    def nbytes(self) -> int:
+        ts = [self.masks, self.dmins, self.dmaxs, self.dexps, self.nsamps, self.cams,
+              self.z_surface, self.raw_masks]
+        return sum(int(t.numel() * t.element_size()) for t in ts if t is not None)
+
+    @classmethod
+    def from_views(cls, views, dev=None, pinned=True, with_z=False):
+        """Pack (ViewGeometry, ConfidenceMask) pairs and copy them to ``dev``.
+
+        Raises ValueError on a mask/view size mismatch (fusion.py:669-670).
+        """
+        import torch
+        dev = dev or device()
+        cams = [vg.camera for vg, _m in views]
+        hm = max(int(c.height) for c in cams)
+        wm = max(int(c.width) for c in cams)
+        nv = len(views)
+        pin = pinned and torch.cuda.is_available()
+
+        def host(dtype):
+            t = torch.zeros((nv, hm, wm), dtype=dtype, pin_memory=pin)
+            return t, t.numpy()
+
+        planes = {k: host(torch.float32) for k in ("masks", "dmins", "dmaxs", "dexps")}
+        planes["nsamps"] = host(torch.int32)
+        if with_z:
+            planes["z_surface"] = host(torch.float32)
+        sizes = []
+        for i, (vg, m) in enumerate(views):
+            c = vg.camera
+            mv = m.values if hasattr(m, "values") else np.asarray(m)
+            if tuple(mv.shape) != (c.height, c.width):
+                raise ValueError("mask and view dimensions differ")
+            h, w = int(c.height), int(c.width)
+            sizes.append((h, w))
+            planes["masks"][1][i, :h, :w] = mv
+            planes["dmins"][1][i, :h, :w] = vg.d_min
+            planes["dmaxs"][1][i, :h, :w] = vg.d_max
+            planes["dexps"][1][i, :h, :w] = vg.d_exp
+            planes["nsamps"][1][i, :h, :w] = vg.n_samples
+            if with_z:
+                planes["z_surface"][1][i, :h, :w] = vg.z_surface
+        dv = {k: t.to(dev, non_blocking=pin) for k, (t, _a) in planes.items()}
+        cam_t = torch.from_numpy(pack_cameras(cams)).to(dev)
+        return cls(cam_t, dv["masks"], dv["dmins"], dv["dmaxs"], dv["dexps"], dv["nsamps"],
+                   z_surface=dv.get("z_surface"), sizes=sizes)
+
+    def refine(self, raw_masks=None, stream=None):
+        """Refine ``raw_masks`` (default: the stored raw masks) into ``masks`` on device."""
+        from .segmenter import refine_masks_device
+        raw = raw_masks if raw_masks is not None else self.raw_masks
+        if raw is None or self.z_surface is None:
+            raise ValueError("refine() needs raw masks and z_surface planes")
+        refine_masks_device(raw, self.z_surface, self.nsamps, out=self.masks, stream=stream)
+        return self
+
+
+# ---------------------------------------------------------------------------
+# the fusion operator
+# ---------------------------------------------------------------------------
+
+class Fuser:
+    """Reusable device-side fusion of one grid layout with fixed parameters.
+
+    ``run`` enqueues ``divas_fuse`` on the current stream (no host sync) and
+    returns the device outputs.  ``vox_range`` restricts the call to a flat
+    voxel range -- an axis-0 slab is ``[ix0 * G^2, ix1 * G^2)``.
+    """
+
+    def __init__(self, grid, params, bounds=None):
+        self.grid = grid
+        self.g = int(grid.resolution)
+        self.origin = np.asarray(grid.origin, dtype=np.float64).reshape(3)
+        self.dx = float(grid.voxel_size())
+        self.pv = _params_vector(params)
+        self.bc, self.bh, self.unb = bounds_arrays(bounds)
+
+    def run(self, density, views: DeviceViews, probs=None, stats=False, occ=False,
+            occ_thr=0.5, vox_range=None, workspace=None, stream=None):
+        import torch
+        g = self.g
+        nvox = g ** 3
+        lo, hi = (0, nvox) if vox_range is None else (int(vox_range[0]), int(vox_range[1]))
+        dev = views.device
+        if density.dtype != torch.float32 or not density.is_cuda or density.numel() != nvox:
+            raise ValueError("density must be a CUDA float32 tensor with G^3 entries")
+        density = density.contiguous()
+        if probs is None:
+            probs = torch.empty(nvox, dtype=torch.float64, device=dev)
+        out = {"probs": probs}
+        if stats:
+            out["n_thick"] = torch.empty(nvox, dtype=torch.int32, device=dev)
+            out["n_thin"] = torch.empty(nvox, dtype=torch.int32, device=dev)
+            for k in ("sw", "smw", "st"):
+                out[k] = torch.empty(nvox, dtype=torch.float64, device=dev)
+        if occ:
+            out["occ"] = torch.empty(nvox, dtype=torch.uint8, device=dev)
+        lib = _native.lib()
+        wsb = lib.divas_fuse_workspace_size(hi - lo, views.nv)
+        if workspace is None or workspace.numel() < wsb:
+            workspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        out["workspace"] = workspace
+        a = _native.FuseArgs()
+        a.g = g
+        a.origin[:] = self.origin.tolist()
+        a.dx_vox = self.dx
+        a.density = _native.ptr(density)
+        a.nv, a.hm, a.wm = views.nv, views.hm, views.wm
+        a.cams = _native.ptr(views.cams)
+        a.masks, a.dmins = _native.ptr(views.masks), _native.ptr(views.dmins)
+        a.dmaxs, a.dexps = _native.ptr(views.dmaxs), _native.ptr(views.dexps)
+        a.nsamps = _native.ptr(views.nsamps)
+        a.pv[:] = self.pv.tolist()
+        a.bc[:] = self.bc.tolist()
+        a.bh[:] = self.bh.tolist()
+        a.unbounded = int(self.unb)
+        a.vox_lo, a.vox_hi = lo, hi
+        a.probs = _native.ptr(probs)
+        a.n_thick = _native.ptr(out.get("n_thick"))
+        a.n_thin = _native.ptr(out.get("n_thin"))
+        a.sw, a.smw, a.st = (_native.ptr(out.get(k)) for k in ("sw", "smw", "st"))
+        a.occ = _native.ptr(out.get("occ"))
+        a.occ_thr = float(occ_thr)
+        import ctypes
+        _native.check(lib.divas_fuse(ctypes.byref(a), _native.ptr(workspace), wsb,
+                                     _native.stream_handle(stream)), "divas_fuse")
+        return out
+
+    @staticmethod
+    def gated_count(out) -> "torch.Tensor":
+        """Device int64 scalar: voxels that cleared the density gate."""
+        return out["workspace"][:8].view(__import__("torch").int64)
+
+    @staticmethod
+    def gated_voxels(out, count=None):
+        """Flat indices of the gated voxels (a superset of the nonzero p)."""
+        import torch
+        n = int(Fuser.gated_count(out).item()) if count is None else int(count)
+        ws = out["workspace"]
+        return ws[256:256 + 4 * n].view(torch.int32).to(torch.int64) & 0xffffffff
+
+
+def _sparse_probs_to_host(out, nvox) -> np.ndarray:
+    """Dense host probabilities from the gated list: only ~1 % of voxels can be
+    nonzero, so copy (index, p) pairs instead of the whole G^3 f64 grid."""
+    idx = Fuser.gated_voxels(out)
+    vals = out["probs"][idx]
+    probs = np.zeros(nvox, dtype=np.float64)
+    probs[idx.cpu().numpy()] = vals.cpu().numpy()
+    return probs
+
+
+def _device_inputs(grid, density, views, params, bounds):
+    _check_layout(grid, density)
+    dev = device()
+    dv = DeviceViews.from_views(views, dev)
+    dens = as_device(density.values, np.float32, dev)
+    return Fuser(grid, params, bounds), dens, dv
+
+
+def fuse(grid, density, views, params, bounds=None, workers=None,
+         trace_path=None) -> OccupancyGrid:
+    """Fuse refined multi-view masks into an occupancy grid (fusion.py:692-724).
+
+    ``views`` is a list of (ViewGeometry, ConfidenceMask) pairs.  ``workers``
+    is accepted for signature compatibility and ignored (the kernel's result
+    does not depend on it, as the reference's does not).  With ``trace_path``
+    the GPU additionally records one JSON line per (voxel, view) decision.
+    """
+    g = int(grid.resolution)
+    _check_layout(grid, density)
+    if not views:
+        return OccupancyGrid(grid, np.zeros((g, g, g)))
+    if trace_path is not None:
+        from .trace import fuse_traced
+        return OccupancyGrid(grid, fuse_traced(grid, density, views, params, bounds, trace_path))
+    fuser, dens, dv = _device_inputs(grid, density, views, params, bounds)
+    out = fuser.run(dens, dv)
+    return OccupancyGrid(grid, _sparse_probs_to_host(out, g ** 3).reshape(g, g, g))
+
+
+def fuse_with_stats(grid, density, views, params, bounds=None):
+    """``fuse`` plus the per-voxel integer votes and sorted sums."""
+    g = int(grid.resolution)
+    _check_layout(grid, density)
+    if not views:
+        z = np.zeros((g, g, g))
+        zi = np.zeros((g, g, g), np.int32)
+        return OccupancyGrid(grid, z), FusionStats(zi, zi.copy(), z, z.copy(), z.copy(), 0)
+    fuser, dens, dv = _device_inputs(grid, density, views, params, bounds)
+    out = fuser.run(dens, dv, stats=True)
+    host = {k: out[k].cpu().numpy().reshape(g, g, g)
+            for k in ("probs", "n_thick", "n_thin", "sw", "smw", "st")}
+    gated = int(Fuser.gated_count(out).item())
+    stats = FusionStats(host["n_thick"], host["n_thin"], host["sw"], host["smw"], host["st"],
+                        gated)
+    return OccupancyGrid(grid, host["probs"]), stats
+
+
+def gradient_maps_device(views: DeviceViews, eps: float, kappa: float, stream=None):
+    """f64 depth-gradient maps on the padded planes (fusion._gradient_maps)."""
+    import torch
+    out = torch.empty(views.masks.shape, dtype=torch.float64, device=views.device)
+    lib = _native.lib()
+    _native.check(lib.divas_gradient_maps(views.nv, views.hm, views.wm,
+                                          _native.ptr(views.dexps), _native.ptr(views.dmins),
+                                          _native.ptr(views.dmaxs), _native.ptr(views.nsamps),
+                                          float(eps), float(kappa), _native.ptr(out),
+                                          _native.stream_handle(stream)), "divas_gradient_maps")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# threshold / extract  (kernel (c))
+# ---------------------------------------------------------------------------
+
+def threshold_device(probs, thr=0.5, g=0, want_indices=False, stream=None):
+    """``probs >= thr`` on device; optionally the C-order indices too.
+
+    Returns (occ uint8 tensor, idx int64 tensor or None, count int64 tensor).
+    ``idx`` rows are (ix, iy, iz) when ``g > 0`` (np.argwhere of the (G,G,G)
+    grid), flat indices otherwise; only the first ``count`` rows are valid.
+    """
+    import torch
+    p = probs.reshape(-1)
+    if p.dtype != torch.float64 or not p.is_cuda:
+        raise ValueError("threshold_device expects a CUDA float64 tensor")
+    p = p.contiguous()
+    n = p.numel()
+    dev = p.device
+    occ = torch.empty(n, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    idx = None
+    if want_indices:
+        idx = torch.empty((n, 3) if g > 0 else (n,), dtype=torch.int64, device=dev)
+    lib = _native.lib()
+    wsb = lib.divas_threshold_workspace_size(n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    _native.check(lib.divas_threshold(_native.ptr(p), n, float(thr), int(g), _native.ptr(occ),
+                                      _native.ptr(idx), _native.ptr(cnt), _native.ptr(ws), wsb,
+                                      _native.stream_handle(stream)), "divas_threshold")
+    return occ, idx, cnt
+
+
+def extract_device(probs, thr=0.5, stream=None):
+    """Device ``np.argwhere(probs >= thr)`` of a (G,G,G) CUDA f64 grid.
+
+    Returns (idx (G^3, 3) int64 tensor, count int64 tensor); rows past
+    ``count`` are unspecified.  No host synchronisation.
+    """
+    g = int(probs.shape[0])
+    _occ, idx, cnt = threshold_device(probs, thr, g=g, want_indices=True, stream=stream)
+    return idx, cnt
+
+
+def _as_probs_tensor(probs):
+    import torch
+    if isinstance(probs, torch.Tensor) and probs.is_cuda:
+        return probs, True
+    return as_device(np.asarray(probs), np.float64, device()), False
+
+
+def threshold(probs, thr: float = 0.5):
+    """Binary occupancy ``probs >= thr`` (ablation.py:109); same shape as probs."""
+    p, on_dev = _as_probs_tensor(probs)
+    occ, _idx, _cnt = threshold_device(p, thr)
+    occ = occ.reshape(p.shape).bool()
+    return occ if on_dev else occ.cpu().numpy()
+
+
+def extract(probs, thr: float = 0.5):
+    """``np.argwhere(probs >= thr)`` for a (G, G, G) grid: (N, 3) int64, C order."""
+    p, on_dev = _as_probs_tensor(probs)
+    if p.dim() != 3 or not (p.shape[0] == p.shape[1] == p.shape[2]):
+        raise ValueError("extract expects a (G, G, G) probability grid")
+    _occ, idx, cnt = threshold_device(p, thr, g=int(p.shape[0]), want_indices=True)
+    n = int(cnt.item())
+    idx = idx[:n]
+    return idx if on_dev else idx.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# overlay (fusion.py:846-865)
+# ---------------------------------------------------------------------------
+
+def project_grid_overlay(ogrid: OccupancyGrid, view, threshold: float = 0.5,
+                         bounds=None) -> np.ndarray:
+    """Binary (H, W) mask of pixels whose ray meets a voxel with p >= threshold."""
+    import ctypes
+    import torch
+    dev = device()
+    cam = view.camera
+    h, w = int(cam.height), int(cam.width)
+    probs = ogrid.probs
+    p = probs if isinstance(probs, torch.Tensor) else as_device(probs, np.float64, dev)
+    dmin = as_device(view.d_min, np.float32, dev)
+    dmax = as_device(view.d_max, np.float32, dev)
+    ns = as_device(view.n_samples, np.int32, dev)
+    out = empty((h, w), np.uint8, dev)
+    rec = pack_cameras([cam])[0]
+    bc, bh, unb = bounds_arrays(bounds)
+    D3 = ctypes.c_double * 3
+    grid = ogrid.grid
+    origin = np.asarray(grid.origin, dtype=np.float64).reshape(3)
+    _native.check(_native.lib().divas_overlay(
+        rec.ctypes.data_as(ctypes.c_void_p), h, w, _native.ptr(dmin), _native.ptr(dmax),
+        _native.ptr(ns), _native.ptr(p.contiguous()), int(grid.resolution), D3(*origin),
+        float(grid.voxel_size()), D3(*bc), D3(*bh), int(unb), float(threshold),
+        _native.ptr(out), _native.stream_handle()), "divas_overlay")
+    return out.cpu().numpy().astype(bool)

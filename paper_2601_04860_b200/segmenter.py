@@ -1,0 +1,85 @@
+"""Depth-weighted confidence refinement on the B200 (stage (a) of the path).
+
+Drop-in for ``divas.segmenter.refine_mask`` / ``ConfidenceMask``
+(/root/reference/pkg/src/divas/segmenter.py:46-62, :129-152): same signature,
+same validation and error types, bit-identical float32 output.  The work runs
+in ``divas_refine`` (csrc/refine.cu); there is no CPU path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._device import as_device, device, empty
+
+__all__ = ["ConfidenceMask", "refine_mask", "refine_masks_device"]
+
+
+@dataclass
+class ConfidenceMask:
+    """Per-pixel segmentation confidence in [0, 1] (segmenter.py:46-62)."""
+
+    values: np.ndarray  # (H, W) float32
+    refined: bool = False
+
+    def __post_init__(self):
+        self.values = np.asarray(self.values, dtype=np.float32)
+        if self.values.ndim != 2:
+            raise ValueError("mask must be 2D")
+        if self.values.size and (self.values.min() < 0 or self.values.max() > 1):
+            raise ValueError("mask confidences must lie in [0, 1]")
+
+    @property
+    def shape(self):
+        return self.values.shape
+
+
+def refine_masks_device(masks, z_surface, n_samples, out=None, stream=None):
+    """Batched refinement of device-resident planes ``[nv, hm, wm]``.
+
+    ``masks``/``z_surface`` float32, ``n_samples`` int32 (CUDA tensors, C
+    order).  Each view is normalised over its own valid pixels (padding with
+    ``n_samples == 0`` is ignored and comes out as 0).  Returns ``out``.
+    """
+    import torch
+    if masks.dim() == 2:
+        masks, z_surface, n_samples = masks[None], z_surface[None], n_samples[None]
+        if out is not None:
+            out = out[None]
+    nv, hm, wm = masks.shape
+    if z_surface.shape != masks.shape or n_samples.shape != masks.shape:
+        raise ValueError("mask and view dimensions differ")
+    for t, dt in ((masks, torch.float32), (z_surface, torch.float32), (n_samples, torch.int32)):
+        if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("refine_masks_device expects contiguous CUDA float32/int32 planes")
+    if out is None:
+        out = torch.empty_like(masks)
+    lib = _native.lib()
+    wsb = lib.divas_refine_workspace_size(nv)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=masks.device)
+    _native.check(lib.divas_refine(nv, hm, wm, _native.ptr(masks), _native.ptr(z_surface),
+                                   _native.ptr(n_samples), _native.ptr(out), _native.ptr(ws),
+                                   wsb, _native.stream_handle(stream)), "divas_refine")
+    return out
+
+
+def refine_mask(mask: ConfidenceMask, view) -> ConfidenceMask:
+    """Depth-weight a confidence mask by one minus the normalised depth.
+
+    Same contract as the reference (segmenter.py:129-152): rejects refined
+    masks and shape mismatches with ValueError; returns a new refined mask.
+    """
+    if mask.refined:
+        raise ValueError("mask is already refined")
+    if mask.shape != view.z_surface.shape:
+        raise ValueError("mask and view dimensions differ")
+    dev = device()
+    m = as_device(mask.values, np.float32, dev)
+    z = as_device(view.z_surface, np.float32, dev)
+    n = as_device(view.n_samples, np.int32, dev)
+    out = empty(m.shape, np.float32, dev)
+    refine_masks_device(m, z, n, out=out)
+    return ConfidenceMask(out.cpu().numpy(), refined=True)

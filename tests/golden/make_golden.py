@@ -68,6 +68,7 @@ def _record(store, prefix, grid, dens, views, params, bounds, probs):
         f"{prefix}_g": np.int64(grid.resolution),
         f"{prefix}_origin": np.asarray(grid.origin, dtype=np.float64),
         f"{prefix}_dx": np.float64(grid.voxel_size()),
+        f"{prefix}_half": np.float64(grid.half_extents[0]),
         f"{prefix}_density": np.asarray(dens.values, dtype=np.float32),
         f"{prefix}_rots": rots, f"{prefix}_poss": poss, f"{prefix}_intr": intr,
         f"{prefix}_masks": masks, f"{prefix}_dmins": dmins, f"{prefix}_dmaxs": dmaxs,
@@ -171,6 +172,13 @@ def make_scene():
     store["sop_raw_masks"] = np.stack([r[0] for r in raw])
     store["sop_z"] = np.stack([r[1] for r in raw])
     store["sop_refined"] = np.stack([r[3] for r in raw])
+    # project_grid_overlay of the fused grid onto every view (fusion.py:846-865)
+    from divas.fusion import OccupancyGrid, project_grid_overlay
+    og = OccupancyGrid(grid, probs)
+    store["sop_overlay"] = np.stack([project_grid_overlay(og, vg, bounds=prof.scene.bounds)
+                                     for vg, _m in views]).astype(np.uint8)
+    store["sop_overlay_thr03"] = np.stack([project_grid_overlay(og, vg, threshold=0.3)
+                                           for vg, _m in views]).astype(np.uint8)
     # small_instance (test_fusion.py:82-96), sigma=2.5, g=14
     bounds = SceneBounds((-4, -4, -4), (4, 4, 4))
     INTR = dict(fx=96.0, fy=96.0, cx=32.0, cy=32.0, width=64, height=64)
@@ -207,8 +215,11 @@ def make_scene():
     mixed = sviews + [(vg3, ConfidenceMask(np.where(vg3.valid, 0.8, 0.05).astype(np.float32),
                                            refined=True))]
     unb = SceneBounds((-1, -1, -4), (1, 1, -2), unbounded=True)
-    _record(store, "mixed", g14, d14, mixed, p, unb,
-            fuse(g14, d14, mixed, p, bounds=unb).probs)
+    pm = fuse(g14, d14, mixed, p, bounds=unb).probs
+    _record(store, "mixed", g14, d14, mixed, p, unb, pm)
+    og14 = OccupancyGrid(g14, pm)
+    store["mixed_overlay"] = np.stack([project_grid_overlay(og14, vg, threshold=0.2, bounds=unb)
+                                       .astype(np.uint8).ravel() for vg, _m in mixed[:2]])
     np.savez_compressed(os.path.join(OUT, "scene.npz"), **store)
 
 

@@ -25,6 +25,7 @@ class FuseCase:
     g: int
     origin: np.ndarray
     dx: float
+    half: float
     density: np.ndarray
     rots: np.ndarray
     poss: np.ndarray
@@ -55,7 +56,7 @@ def _case(d, prefix):
     p = np.zeros(g ** 3, dtype=np.float64)
     p[d[f"{prefix}_p_idx"]] = d[f"{prefix}_p_val"]
     return FuseCase(
-        name=prefix, g=g, origin=d[f"{prefix}_origin"], dx=float(d[f"{prefix}_dx"]),
+        name=prefix, g=g, origin=d[f"{prefix}_origin"], dx=float(d[f"{prefix}_dx"]), half=float(d[f"{prefix}_half"]),
         density=d[f"{prefix}_density"], rots=d[f"{prefix}_rots"], poss=d[f"{prefix}_poss"],
         intr=d[f"{prefix}_intr"], masks=d[f"{prefix}_masks"], dmins=d[f"{prefix}_dmins"],
         dmaxs=d[f"{prefix}_dmaxs"], dexps=d[f"{prefix}_dexps"], nsamps=d[f"{prefix}_nsamps"],

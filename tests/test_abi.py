@@ -1,0 +1,79 @@
+"""The C-ABI library: builds, loads, exports exactly what the header declares,
+and its argument struct matches the ctypes mirror.  No compute calls (CPU)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2601_04860_b200 import _native, build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "divas_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _native.lib()
+
+
+def _declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(divas_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_exports():
+    assert _declared() == sorted(_native.EXPORTS)
+
+
+def test_library_exports_every_symbol(lib):
+    nm = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH],
+                        capture_output=True, text=True, check=True).stdout
+    syms = {line.split()[-1] for line in nm.splitlines() if line.strip()}
+    for name in _declared():
+        assert name in syms, name
+        assert getattr(lib, name) is not None
+
+
+def test_version_and_error(lib):
+    assert lib.divas_abi_version() == 1
+    assert isinstance(lib.divas_last_error(), bytes)
+
+
+def test_sm100a_code_only(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_struct_layout_matches_header(tmp_path):
+    prog = tmp_path / "layout.c"
+    fields = [f[0] for f in _native.FuseArgs._fields_]
+    body = "\n".join(f'printf("%zu\\n", offsetof(divas_fuse_args, {f}));' for f in fields)
+    prog.write_text(f"""
+#include <stdio.h>
+#include <stddef.h>
+#include "divas_b200.h"
+int main(void) {{ printf("%zu\\n", sizeof(divas_fuse_args)); {body} return 0; }}
+""")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.dirname(HEADER), str(prog), "-o", str(exe)], check=True)
+    vals = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                           check=True).stdout.split()]
+    assert vals[0] == ctypes.sizeof(_native.FuseArgs)
+    for f, off in zip(fields, vals[1:]):
+        assert getattr(_native.FuseArgs, f).offset == off, f
+
+
+def test_invalid_arguments_rejected_without_gpu(lib):
+    """Argument validation happens before any CUDA call."""
+    a = _native.FuseArgs()
+    a.g = 0
+    rc = lib.divas_fuse(ctypes.byref(a), None, 0, None)
+    assert rc == 1
+    assert b"grid" in lib.divas_last_error()
+    assert lib.divas_refine(0, 1, 1, None, None, None, None, None, 0, None) == 1
+    assert lib.divas_threshold(None, 10, 0.5, 0, None, None, None, None, 0, None) == 1
