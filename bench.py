@@ -1,0 +1,521 @@
+#!/usr/bin/env python
+"""bench.py -- DivAS fusion hot path (refine -> fuse -> threshold) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C3]
+
+One JSON line on rank 0 (contract in the task statement; fields explained in
+DESIGN.md section 5).  Metric: voxel-view updates/s of one fusion update over
+BASELINE.json's headline configuration C3 (256^3 grid x 32 views at
+1008x756); ``latency_ms`` is the same step's fusion latency.
+
+A step, device-resident (``value``): refine all 32 masks (divas_refine) + fuse
+the rank's slab with the threshold fused in (divas_fuse) + (N > 1) all-gather
+of the occupancy slabs.  L2 is flushed between steps, outside the events.
+
+``e2e``: the same update through the public drop-in API with host buffers
+(pinned): ``refine_masks`` + ``fuse`` -> host OccupancyGrid, every copy inside
+the timed region.
+
+``--impl reference``: the reference's CPU path as restated by the oracle
+(``oracle/``, pthreads over all host cores) on a bounded slab sample of the
+same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG_DESC = {
+    "C1": "C1: 128^3 grid x 8 Fibonacci views at 504x378, sphere_on_plane",
+    "C2": "C2: 256^3 grid x 20 forward-facing views (5x4) at 1008x756, sphere_on_plane",
+    "C3": "C3: 256^3 grid x 32 views (16 Fibonacci + 16 centroid-zoom) at 1008x756, sphere_on_plane",
+    "C5": "C5: 512^3 grid x 128 Fibonacci views at 1920x1080, sphere_on_plane",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0,
+                    help="CPU seconds for the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--slabs", default="balanced", choices=["balanced", "equal"])
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks (NVML, sampled in a thread during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index, period=0.002):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], 0
+        self._stop = threading.Event()
+        self._t = None
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:   # NVML unavailable: report no clocks rather than guess
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml-unavailable"]}
+        reasons = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples), "reasons": reasons}
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(config, op):
+    """dram bytes per launch of ``op`` from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(config, {}).get(op)
+    except Exception:
+        return None
+
+
+def host_copy(wl):
+    """numpy copies of the workload planes (oracle inputs)."""
+    return {k: getattr(wl, k).cpu().numpy() for k in
+            ("raw_masks", "z_surface", "dmins", "dmaxs", "dexps", "nsamps", "density")}
+
+
+def oracle_sample(wl, h, pv, budget_s, early_out=False, slabs=None):
+    """Time the oracle (refine of every view + fuse of sampled ix-slabs).
+
+    Returns (seconds for one full-grid update extrapolated from the sample,
+    details).  ``early_out=False`` is the reference's algorithm as written:
+    every (voxel, view) pair is projected (fusion.py:505-509).
+    """
+    import oracle
+    nv = wl.nv
+    g = wl.g
+    t0 = time.perf_counter()
+    refined = np.stack([oracle.refine(h["raw_masks"][v], h["z_surface"][v], h["nsamps"][v])
+                        for v in range(nv)])
+    t_refine = time.perf_counter() - t0
+    cams = np.stack([np.concatenate([c.rotation.reshape(9), c.position,
+                                     [c.fx, c.fy, c.cx, c.cy, float(c.width), float(c.height)]])
+                     for c in wl.cams])
+    packed = (cams[:, :9].reshape(nv, 3, 3), cams[:, 9:12], cams[:, 12:18], refined,
+              h["dmins"], h["dmaxs"], h["dexps"], h["nsamps"], (h["nsamps"] > 0).astype(np.uint8))
+    t0 = time.perf_counter()
+    gm = oracle.gradient_maps(h["dexps"], h["dmins"], h["dmaxs"], packed[-1], pv[9], pv[12])
+    t_refine += time.perf_counter() - t0      # fuse() computes the maps serially too
+    nthreads = oracle.max_threads()
+
+    def run(ix):
+        return oracle.fuse_packed(g, wl.origin, wl.dx, h["density"], packed, pv,
+                                  np.zeros(3), np.ones(3), 0, gmaps=gm,
+                                  vox_range=(ix * g * g, (ix + 1) * g * g),
+                                  early_out=early_out, nthreads=nthreads)
+
+    if slabs is None:
+        t1 = time.perf_counter()
+        run(g // 2)
+        per = max(time.perf_counter() - t1, 1e-4)
+        k = int(max(1, min(g, budget_s / per)))
+        slabs = sorted(set(int(x) for x in np.linspace(0, g - 1, k + 2)[1:-1]) | {g // 2})
+    t2 = time.perf_counter()
+    results = {ix: run(ix) for ix in slabs}
+    t_fuse = time.perf_counter() - t2
+    full = t_refine + t_fuse * g / len(slabs)
+    return full, dict(refined=refined, results=results, slabs=slabs, t_refine=t_refine,
+                      t_fuse_sample=t_fuse, threads=nthreads)
+
+
+def parity_check(wl, details, probs, n_thick, n_thin, refined_gpu):
+    g = wl.g
+    gg = g * g
+    ok_votes = ok_occ = True
+    max_rel = 0.0
+    n_inexact = 0
+    for ix, r in details["results"].items():
+        sl = slice(ix * gg, (ix + 1) * gg)
+        ok_votes &= bool(np.array_equal(n_thick[sl], r["n_thick"][sl]) and
+                         np.array_equal(n_thin[sl], r["n_thin"][sl]))
+        ok_occ &= bool(np.array_equal(probs[sl] >= 0.5, r["p"][sl] >= 0.5))
+        w = r["p"][sl]
+        rel = np.abs(probs[sl] - w) / np.maximum(np.abs(w), 1e-300)
+        rel[(w == 0) & (probs[sl] == 0)] = 0.0
+        max_rel = max(max_rel, float(rel.max(initial=0.0)))
+        n_inexact += int((probs[sl] != w).sum())
+    refine_exact = bool(np.array_equal(refined_gpu, details["refined"]))
+    return {"sample_slabs": len(details["results"]), "refine_bit_exact": refine_exact,
+            "votes_exact": ok_votes, "occupancy_exact": ok_occ, "p_max_rel": max_rel,
+            "p_not_bit_exact": n_inexact, "tolerance": 1e-12}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import workloads
+    from paper_2601_04860_b200.fusion import FusionParams
+    import torch
+    # fixture generation only (torch ops, none of our kernels); timing is CPU-only
+    gen = "cuda" if torch.cuda.is_available() else "cpu"
+    wl = workloads.make(args.config, device=gen)
+    h = host_copy(wl)
+    pv = FusionParams().as_vector()
+    budget = max(0.5, min(args.cpu_budget_s / max(args.steps + args.warmup, 1), 4.0))
+    # one sample definition shared by every step
+    _t, det = oracle_sample(wl, h, pv, budget)
+    slabs = det["slabs"]
+    for _ in range(args.warmup):
+        oracle_sample(wl, h, pv, budget, slabs=slabs)
+    times = []
+    for _ in range(args.steps):
+        t, _d = oracle_sample(wl, h, pv, budget, slabs=slabs)
+        times.append(t)
+    ms = 1e3 * float(np.mean(times))
+    value = wl.updates() / (ms / 1e3)
+    sample = (f"refine of all {wl.nv} views + fuse of {len(slabs)}/{wl.g} ix-slabs "
+              f"(every voxel-view pair projected, as fusion.py:505-509), extrapolated to the "
+              f"full grid")
+    line = {
+        "impl": "reference", "metric": "voxel-view updates/s", "value": value,
+        "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "latency_ms": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_DESC[args.config], "grid": wl.g, "views": wl.nv,
+                   "width": wl.shape[2], "height": wl.shape[1]},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": oracle.max_threads(),
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import workloads
+    from paper_2601_04860_b200 import sharding
+    from paper_2601_04860_b200.fusion import DeviceViews, FusionParams, Fuser
+    from paper_2601_04860_b200.segmenter import refine_masks_device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    params = FusionParams()
+    pv = params.as_vector()
+
+    # --- inputs: rank 0 builds the view set, NCCL broadcasts it (once) ---------
+    cfg = workloads.CONFIGS[args.config]
+    if rank == 0:
+        wl = workloads.make(args.config, device=dev)
+    else:
+        wl = None
+    if world > 1:
+        shapes = [None]
+        if rank == 0:
+            shapes = [dict(nv=wl.nv, h=wl.shape[1], w=wl.shape[2], g=wl.g, cams=wl.cams,
+                           origin=wl.origin, dx=wl.dx)]
+        dist.broadcast_object_list(shapes, src=0)
+        meta = shapes[0]
+        if rank != 0:
+            nv, hh, ww, g = meta["nv"], meta["h"], meta["w"], meta["g"]
+            e = lambda dt: torch.empty((nv, hh, ww), dtype=dt, device=dev)  # noqa: E731
+            wl = workloads.Workload(args.config, g, meta["origin"], meta["dx"],
+                                    torch.empty(g ** 3, dtype=torch.float32, device=dev),
+                                    meta["cams"], e(torch.float32), e(torch.float32),
+                                    e(torch.float32), e(torch.float32), e(torch.float32),
+                                    e(torch.int32))
+    from paper_2601_04860_b200.fusion import pack_cameras
+    cams_t = torch.from_numpy(pack_cameras(wl.cams)).to(dev)
+    dv = DeviceViews(cams_t, torch.empty_like(wl.raw_masks), wl.dmins, wl.dmaxs, wl.dexps,
+                     wl.nsamps, z_surface=wl.z_surface, raw_masks=wl.raw_masks)
+    bcast_ms = 0.0
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sharding.broadcast_views(dv, src=0)
+        dist.broadcast(wl.density, src=0)
+        e1.record()
+        torch.cuda.synchronize()
+        bcast_ms = e0.elapsed_time(e1)
+    g, nv = wl.g, wl.nv
+    grid = type("G", (), {"resolution": g, "origin": wl.origin, "voxel_size": lambda s=None: wl.dx})()
+    fuser = Fuser(grid, params)
+
+    # --- slabs ------------------------------------------------------------------
+    if args.slabs == "balanced":
+        slabs = sharding.balanced_slabs(sharding.slice_weights(wl.density.reshape(g, g, g), pv, nv),
+                                        world)
+    else:
+        slabs = sharding.equal_slabs(g, world)
+    lo, hi = sharding.slab_voxel_range(slabs[rank], g)
+    probs = torch.empty(g ** 3, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    ws = None
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        nonlocal ws
+        if ev is not None:
+            ev[0].record(stream)
+        refine_masks_device(dv.raw_masks, dv.z_surface, dv.nsamps, out=dv.masks)
+        if ev is not None:
+            ev[1].record(stream)
+        out = fuser.run(wl.density, dv, probs=probs, occ=True, vox_range=(lo, hi), workspace=ws)
+        ws = out["workspace"]
+        if ev is not None:
+            ev[2].record(stream)
+        occ_full = None
+        if world > 1:
+            occ_full = sharding.gather_occupancy(out["occ"][lo:hi], slabs, g, rank)
+        if ev is not None:
+            ev[3].record(stream)
+        return out, occ_full
+
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for k in range(K):
+            flush.zero_()
+            step(evs[k])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    t_ref = [a.elapsed_time(b) for a, b, _c, _d in evs]
+    t_fuse = [b.elapsed_time(c) for _a, b, c, _d in evs]
+    t_gath = [c.elapsed_time(d) for _a, _b, c, d in evs]
+    t_step = [a.elapsed_time(d) for a, _b, _c, d in evs]
+    ms_local = float(np.mean(t_step))
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    updates = g ** 3 * nv
+    value = updates / (ms / 1e3)
+
+    # --- roofline of the dominant operator --------------------------------------
+    peak, peak_kind = measured_peak()
+    H, W = wl.shape[1], wl.shape[2]
+    b_refine = 16 * nv * H * W
+    b_fuse = 12 * (hi - lo) + 20 * nv * H * W
+    refine_ms, fuse_ms = float(np.mean(t_ref)), float(np.mean(t_fuse))
+    ops = {"refine": (refine_ms, b_refine, "divas_refine: refine_minmax + refine_apply"),
+           "fuse": (fuse_ms, b_fuse, "divas_fuse: fuse_gate + fuse_sparse")}
+    dom = max(ops, key=lambda k: ops[k][0])
+    d_ms, d_bytes, d_desc = ops[dom]
+    achieved = d_bytes / (d_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(args.config, dom),
+                "kernel": d_desc, "algorithmic_bytes": d_bytes, "launch_ms": d_ms,
+                "peak_kind": peak_kind,
+                "other": {k: {"launch_ms": v[0], "algorithmic_bytes": v[1],
+                              "achieved_gbs": v[1] / (v[0] / 1e3) / 1e9,
+                              "frac": v[1] / (v[0] / 1e3) / 1e9 / peak}
+                          for k, v in ops.items() if k != dom}}
+
+    # --- stats / parity / cpu baseline (rank 0, N = 1) --------------------------
+    torch.cuda.synchronize()
+    gated = int(Fuser.gated_count({"workspace": ws}).item())
+    extra = {}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        h = host_copy(wl)
+        out = fuser.run(wl.density, dv, stats=True, occ=True)
+        torch.cuda.synchronize()
+        full_s, det = oracle_sample(wl, h, pv, args.cpu_budget_s)
+        cpu_val = updates / full_s
+        cpu = {"value": cpu_val, "unit": "updates/s", "cores": det["threads"], "kind": "port",
+               "sample": (f"oracle (C restatement of fusion.py:410-509, segmenter.py:129-152), "
+                          f"refine of all {nv} views + fuse of {len(det['slabs'])}/{g} ix-slabs "
+                          f"with every voxel-view pair projected as the reference does, "
+                          f"{det['t_refine'] + det['t_fuse_sample']:.1f} s of CPU time, "
+                          f"extrapolated to the full grid"),
+               "ms_per_update": full_s * 1e3}
+        extra["parity"] = parity_check(wl, det, out["probs"].cpu().numpy(),
+                                       out["n_thick"].cpu().numpy(), out["n_thin"].cpu().numpy(),
+                                       dv.masks.cpu().numpy())
+
+    # --- e2e through the public API, host buffers (rank-local, N = 1 semantics) --
+    e2e = None
+    if rank == 0:
+        e2e = run_e2e(args, wl, params, dev)
+
+    launches_per_step = 3 + 2          # refine: init, minmax, apply; fuse: gate, sparse
+    line = {
+        "metric": "voxel-view updates/s", "value": value, "unit": "updates/s",
+        "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+        "latency_ms": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_DESC[args.config], "grid": g, "views": nv,
+                   "width": W, "height": H, "parallelism": f"slab x{world}" if world > 1 else "1 GPU",
+                   "slabs": slabs, "slab_policy": args.slabs,
+                   "step": "refine(all views) + fuse(slab, threshold fused)"
+                           + (" + all-gather(occupancy)" if world > 1 else ""),
+                   "l2": "flushed (256 MiB write) between steps, outside the events",
+                   "params": "FusionParams() defaults"},
+        "breakdown_ms": {"refine": refine_ms, "fuse": fuse_ms, "gather": float(np.mean(t_gath)),
+                         "broadcast_once": bcast_ms},
+        "gated_voxels": gated,
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+        "gpu_launches": launches_per_step * K,
+        "clocks": clk.summary(),
+    }
+    line.update(extra)
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, wl, params, dev):
+    """refine_masks + fuse through the drop-in API from pinned host buffers."""
+    import torch
+
+    import workloads
+    from paper_2601_04860_b200 import (ConfidenceMask, DensityGrid, VoxelGrid, fuse,
+                                       refine_masks, ViewGeometry)
+    from paper_2601_04860_b200.geometry import Camera
+    nv, H, W = wl.shape
+
+    def pinned(t):
+        p = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        p.copy_(t)
+        return p.numpy()
+
+    planes = {k: pinned(getattr(wl, k)) for k in
+              ("raw_masks", "z_surface", "dmins", "dmaxs", "dexps", "nsamps")}
+    grid = VoxelGrid(wl.g, workloads.GRID_HALF, wl.origin)
+    dens = DensityGrid(grid, pinned(wl.density).reshape(wl.g, wl.g, wl.g))
+    views = []
+    for v, c in enumerate(wl.cams):
+        cam = Camera(c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.world_from_camera)
+        views.append(ViewGeometry(cam, None, planes["dmins"][v], planes["dmaxs"][v],
+                                  planes["dexps"][v], planes["nsamps"][v], planes["z_surface"][v]))
+    raw = [ConfidenceMask(planes["raw_masks"][v]) for v in range(nv)]
+
+    def once():
+        refined = refine_masks(raw, views)
+        og = fuse(grid, dens, list(zip(views, refined)), params)
+        return og, refined
+
+    once()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(max(1, args.e2e_steps)):
+        t0 = time.perf_counter()
+        og, refined = once()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.median(times))
+    px = nv * H * W
+    h2d = px * 12 + px * 20 + wl.g ** 3 * 4 + nv * 18 * 8
+    rho = planes_density = np.asarray(dens.values, dtype=np.float64)
+    pv = params.as_vector()
+    gated = int(((rho >= pv[4]) | ((pv[13] != 0) & (rho >= pv[5]))).sum())
+    del planes_density
+    d2h = px * 4 + 8 + gated * 12
+    return {"value": wl.updates() / (ms / 1e3), "unit": "updates/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "api": "refine_masks(raw, views) + fuse(grid, density, views, params) -> OccupancyGrid",
+            "host_buffers": "pinned"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

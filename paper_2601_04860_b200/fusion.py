@@ -217,10 +217,12 @@ class DeviceViews:
         return sum(int(t.numel() * t.element_size()) for t in ts if t is not None)
 
     @classmethod
-    def from_views(cls, views, dev=None, pinned=True, with_z=False):
-        """Pack (ViewGeometry, ConfidenceMask) pairs and copy them to ``dev``.
+    def from_views(cls, views, dev=None, with_z=False):
+        """Copy (ViewGeometry, ConfidenceMask) pairs into device planes.
 
-        Raises ValueError on a mask/view size mismatch (fusion.py:669-670).
+        Each host map is uploaded straight into its slot of the padded device
+        plane (no host-side packing pass).  Raises ValueError on a mask/view
+        size mismatch (fusion.py:669-670).
         """
         import torch
         dev = dev or device()
@@ -228,35 +230,28 @@ class DeviceViews:
         hm = max(int(c.height) for c in cams)
         wm = max(int(c.width) for c in cams)
         nv = len(views)
-        pin = pinned and torch.cuda.is_available()
-
-        def host(dtype):
-            t = torch.zeros((nv, hm, wm), dtype=dtype, pin_memory=pin)
-            return t, t.numpy()
-
-        planes = {k: host(torch.float32) for k in ("masks", "dmins", "dmaxs", "dexps")}
-        planes["nsamps"] = host(torch.int32)
-        if with_z:
-            planes["z_surface"] = host(torch.float32)
         sizes = []
-        for i, (vg, m) in enumerate(views):
+        for vg, m in views:
             c = vg.camera
             mv = m.values if hasattr(m, "values") else np.asarray(m)
             if tuple(mv.shape) != (c.height, c.width):
                 raise ValueError("mask and view dimensions differ")
-            h, w = int(c.height), int(c.width)
-            sizes.append((h, w))
-            planes["masks"][1][i, :h, :w] = mv
-            planes["dmins"][1][i, :h, :w] = vg.d_min
-            planes["dmaxs"][1][i, :h, :w] = vg.d_max
-            planes["dexps"][1][i, :h, :w] = vg.d_exp
-            planes["nsamps"][1][i, :h, :w] = vg.n_samples
+            sizes.append((int(c.height), int(c.width)))
+        alloc = torch.empty if all(s == (hm, wm) for s in sizes) else torch.zeros
+        names = ["masks", "dmins", "dmaxs", "dexps", "nsamps"] + (["z_surface"] if with_z else [])
+        planes = {k: alloc((nv, hm, wm), dtype=torch.int32 if k == "nsamps" else torch.float32,
+                           device=dev) for k in names}
+        for i, ((vg, m), (h, w)) in enumerate(zip(views, sizes)):
+            src = {"masks": m.values if hasattr(m, "values") else m, "dmins": vg.d_min,
+                   "dmaxs": vg.d_max, "dexps": vg.d_exp, "nsamps": vg.n_samples}
             if with_z:
-                planes["z_surface"][1][i, :h, :w] = vg.z_surface
-        dv = {k: t.to(dev, non_blocking=pin) for k, (t, _a) in planes.items()}
+                src["z_surface"] = vg.z_surface
+            for k in names:
+                dt = np.int32 if k == "nsamps" else np.float32
+                planes[k][i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(src[k], dt)))
         cam_t = torch.from_numpy(pack_cameras(cams)).to(dev)
-        return cls(cam_t, dv["masks"], dv["dmins"], dv["dmaxs"], dv["dexps"], dv["nsamps"],
-                   z_surface=dv.get("z_surface"), sizes=sizes)
+        return cls(cam_t, planes["masks"], planes["dmins"], planes["dmaxs"], planes["dexps"],
+                   planes["nsamps"], z_surface=planes.get("z_surface"), sizes=sizes)
 
     def refine(self, raw_masks=None, stream=None):
         """Refine ``raw_masks`` (default: the stored raw masks) into ``masks`` on device."""

@@ -15,7 +15,7 @@ import numpy as np
 from . import _native
 from ._device import as_device, device, empty
 
-__all__ = ["ConfidenceMask", "refine_mask", "refine_masks_device"]
+__all__ = ["ConfidenceMask", "refine_mask", "refine_masks", "refine_masks_device"]
 
 
 @dataclass
@@ -83,3 +83,40 @@ def refine_mask(mask: ConfidenceMask, view) -> ConfidenceMask:
     out = empty(m.shape, np.float32, dev)
     refine_masks_device(m, z, n, out=out)
     return ConfidenceMask(out.cpu().numpy(), refined=True)
+
+
+def refine_masks(masks, views):
+    """Batched ``refine_mask``: one upload, one launch, one download for all views.
+
+    Same per-view validation and result as calling ``refine_mask`` on each
+    (mask, view) pair; views of different sizes are padded on the device.
+    """
+    import torch
+    masks, views = list(masks), list(views)
+    if len(masks) != len(views):
+        raise ValueError("need one view per mask")
+    if not masks:
+        return []
+    for m, v in zip(masks, views):
+        if m.refined:
+            raise ValueError("mask is already refined")
+        if m.shape != v.z_surface.shape:
+            raise ValueError("mask and view dimensions differ")
+    dev = device()
+    hm = max(m.shape[0] for m in masks)
+    wm = max(m.shape[1] for m in masks)
+    nv = len(masks)
+    same = all(m.shape == (hm, wm) for m in masks)
+    alloc = torch.empty if same else torch.zeros
+    M = alloc((nv, hm, wm), dtype=torch.float32, device=dev)
+    Z = alloc((nv, hm, wm), dtype=torch.float32, device=dev)
+    N = alloc((nv, hm, wm), dtype=torch.int32, device=dev)
+    for i, (m, v) in enumerate(zip(masks, views)):
+        h, w = m.shape
+        M[i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(m.values, np.float32)))
+        Z[i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(v.z_surface, np.float32)))
+        N[i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(v.n_samples, np.int32)))
+    out = refine_masks_device(M, Z, N)
+    host = out.cpu().numpy()
+    return [ConfidenceMask(host[i, :m.shape[0], :m.shape[1]], refined=True)
+            for i, m in enumerate(masks)]

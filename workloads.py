@@ -200,29 +200,37 @@ def silhouette_mask(core):
 
 
 def density_grid(g, device="cpu"):
-    """bake_density_grid of the scene at voxel centres: (G,G,G) f32 [ix,iy,iz]."""
+    """bake_density_grid of the scene at voxel centres: (G,G,G) f32 [ix,iy,iz].
+
+    Primitives whose soft-edged box cannot reach the grid (the room walls)
+    contribute exactly 0 and are skipped.
+    """
     import torch
     dx = 2.0 * GRID_HALF / g
     origin = np.asarray(CENTER) - GRID_HALF
     ax = [origin[a] + (torch.arange(g, device=device, dtype=torch.float64) + 0.5) * dx
           for a in range(3)]
-    out = torch.zeros((g, g, g), dtype=torch.float64, device=device)
-    for i in range(g):                      # slab by slab keeps memory flat at G=512
-        X = ax[0][i]
-        Y, Z = torch.meshgrid(ax[1], ax[2], indexing="ij")
+    lo, hi = origin, origin + 2 * GRID_HALF
+    boxes = [(bc, bh) for bc, bh in _boxes()
+             if all(bc[j] - bh[j] - SOFT <= hi[j] and bc[j] + bh[j] + SOFT >= lo[j] for j in range(3))]
+    out = torch.empty((g, g, g), dtype=torch.float32, device=device)
+    Y, Z = torch.meshgrid(ax[1], ax[2], indexing="ij")
+    step = max(1, (1 << 22) // (g * g))
+    for i0 in range(0, g, step):
+        X = ax[0][i0:i0 + step].view(-1, 1, 1)
         dist = torch.sqrt((X - CENTER[0]) ** 2 + (Y - CENTER[1]) ** 2 + (Z - CENTER[2]) ** 2)
         sd = torch.maximum(dist - SPHERE_R, SPHERE_IN - dist)
         val = torch.where(sd <= 0, SPHERE_SIGMA, 0.0)
-        for bc, bh in _boxes():
-            q = [(c - bc[j]).abs() - bh[j] for j, c in enumerate((X, Y, Z))]
-            qx, qy, qz = (torch.as_tensor(t, dtype=torch.float64, device=device) for t in q)
-            qx = qx.expand_as(Y)
+        for bc, bh in boxes:
+            qx = ((X - bc[0]).abs() - bh[0]).expand_as(dist)
+            qy = ((Y - bc[1]).abs() - bh[1]).expand_as(dist)
+            qz = ((Z - bc[2]).abs() - bh[2]).expand_as(dist)
             outside = torch.sqrt(qx.clamp(min=0) ** 2 + qy.clamp(min=0) ** 2 + qz.clamp(min=0) ** 2)
             inside = torch.maximum(torch.maximum(qx, qy), qz).clamp(max=0)
             fall = (1.0 - (outside + inside) / SOFT).clamp(0.0, 1.0)
-            val = torch.maximum(val, 40.0 * fall)
-        out[i] = val
-    return out.to(torch.float32), origin, dx
+            val = torch.maximum(val, PAD_SIGMA * fall)
+        out[i0:i0 + step] = val.to(torch.float32)
+    return out, origin, dx
 
 
 @dataclass
