@@ -39,7 +39,9 @@ def slice_weights(density, pv, nv: int) -> np.ndarray:
         import torch
         if isinstance(density, torch.Tensor):
             d = density.reshape(density.shape[0], -1).to(torch.float64)
-            gate = (d >= pv[4]) | ((pv[13] != 0) & (d >= pv[5]))
+            gate = d >= float(pv[4])
+            if pv[13] != 0:
+                gate = gate | (d >= float(pv[5]))
             gated = gate.sum(dim=1).cpu().numpy().astype(np.float64)
             per = float(d.shape[1])
             return gated * nv + STREAM_WEIGHT * per
@@ -47,7 +49,9 @@ def slice_weights(density, pv, nv: int) -> np.ndarray:
         pass
     d = np.asarray(density, dtype=np.float64)
     d = d.reshape(d.shape[0], -1)
-    gate = (d >= pv[4]) | ((pv[13] != 0) & (d >= pv[5]))
+    gate = d >= pv[4]
+    if pv[13] != 0:
+        gate = gate | (d >= pv[5])
     return gate.sum(axis=1).astype(np.float64) * nv + STREAM_WEIGHT * d.shape[1]
 
 

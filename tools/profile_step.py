@@ -1,0 +1,36 @@
+"""Run a few device-resident fusion steps of a config (for ncu / launch lists)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--steps", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+    import workloads
+    from paper_2601_04860_b200.fusion import DeviceViews, FusionParams, Fuser, pack_cameras
+    from paper_2601_04860_b200.segmenter import refine_masks_device
+    dev = torch.device("cuda", 0)
+    wl = workloads.make(args.config, device=dev)
+    dv = DeviceViews(torch.from_numpy(pack_cameras(wl.cams)).to(dev), torch.empty_like(wl.raw_masks),
+                     wl.dmins, wl.dmaxs, wl.dexps, wl.nsamps, z_surface=wl.z_surface,
+                     raw_masks=wl.raw_masks)
+    grid = type("G", (), {"resolution": wl.g, "origin": wl.origin, "voxel_size": lambda s=None: wl.dx})()
+    fuser = Fuser(grid, FusionParams())
+    probs = torch.empty(wl.g ** 3, dtype=torch.float64, device=dev)
+    ws = None
+    for _ in range(args.steps):
+        refine_masks_device(dv.raw_masks, dv.z_surface, dv.nsamps, out=dv.masks)
+        out = fuser.run(wl.density, dv, probs=probs, occ=True, workspace=ws)
+        ws = out["workspace"]
+    torch.cuda.synchronize()
+    print("gated", int(Fuser.gated_count(out).item()))
+
+
+if __name__ == "__main__":
+    main()
