@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define DIVAS_ABI_VERSION 1
+#define DIVAS_ABI_VERSION 2
 
 /* error codes */
 #define DIVAS_OK          0
@@ -87,16 +87,29 @@ typedef struct divas_fuse_args {
     double *sw, *smw, *st;       /* [G^3] sorted sums, or NULL                */
     uint8_t *occ;                /* [G^3] fused threshold p >= occ_thr, or NULL */
     double occ_thr;
+    int64_t max_gated;           /* slot capacity: upper bound on voxels that pass
+                                    the density gate in [lo, hi); <= 0 means
+                                    hi - lo (always safe).  divas_gate_count
+                                    gives the exact figure for a density grid. */
 } divas_fuse_args;
 
-/* Workspace for divas_fuse over `n_vox` voxels (the slab length). */
-size_t divas_fuse_workspace_size(int64_t n_vox, int32_t nv);
+/* Workspace bytes for divas_fuse with slot capacity `max_gated` and `nv` views
+ * (~ max_gated * (4 + nv * 24.25) bytes; contributions are [view][slot]). */
+size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv);
 int divas_fuse(const divas_fuse_args *args, void *workspace, size_t workspace_bytes,
                void *stream);
 
-/* Number of voxels that passed the exact density gate in the last
- * divas_fuse that used `workspace` (device pointer to one int64). */
+/* Count the voxels of [vox_lo, vox_hi) that pass the exact density gate
+ * rho >= pv[4] || (pv[13] != 0 && rho >= pv[5]); only args->g, vox_lo, vox_hi,
+ * density and pv are read.  The count lands in divas_fuse_gated_count(ws)
+ * (workspace >= 256 bytes). */
+int divas_gate_count(const divas_fuse_args *args, void *workspace, void *stream);
+
+/* Device pointers into a divas_fuse workspace: the gated-voxel count of the
+ * last call (int64) and its overflow flag (int32, nonzero when the count
+ * exceeded max_gated -- voxels past the capacity were then left at p = 0). */
 const int64_t *divas_fuse_gated_count(const void *workspace);
+const int32_t *divas_fuse_overflow(const void *workspace);
 
 /* The f64 depth-gradient maps of fusion._gradient_maps on the padded planes
  * (divas_fuse computes g on the fly; this export is for parity tests). */
@@ -117,8 +130,9 @@ int divas_threshold(const double *p, int64_t n, double thr, int64_t g,
 
 /* ---------------------------------------------------------------------- */
 /* Overlay: binary mask of pixels whose ray meets a voxel with p >= thr     */
-/* (project_grid_overlay).  cam: one DIVAS_CAM_STRIDE record; dmin/dmax/    */
-/* nsamp: [h][w] planes of the view; probs: [G^3]; out: [h][w] uint8.       */
+/* (project_grid_overlay).  HOST arrays: cam (one DIVAS_CAM_STRIDE record), */
+/* origin, bc, bh.  DEVICE arrays: dmin/dmax/nsamp [h][w] planes of the     */
+/* view, probs [G^3], out [h][w] uint8.                                     */
 /* ---------------------------------------------------------------------- */
 int divas_overlay(const double *cam, int32_t h, int32_t w, const float *dmin,
                   const float *dmax, const int32_t *nsamp, const double *probs,

@@ -20,7 +20,8 @@ NPARAM = 14
 # every symbol include/divas_b200.h declares
 EXPORTS = (
     "divas_refine_workspace_size", "divas_refine",
-    "divas_fuse_workspace_size", "divas_fuse", "divas_fuse_gated_count",
+    "divas_fuse_workspace_size", "divas_fuse", "divas_gate_count", "divas_fuse_gated_count",
+    "divas_fuse_overflow",
     "divas_gradient_maps",
     "divas_threshold_workspace_size", "divas_threshold",
     "divas_overlay",
@@ -42,7 +43,7 @@ class FuseArgs(ctypes.Structure):
         ("pv", ctypes.c_double * NPARAM), ("bc", _D3), ("bh", _D3),
         ("unbounded", ctypes.c_int32), ("vox_lo", ctypes.c_int64), ("vox_hi", ctypes.c_int64),
         ("probs", _VP), ("n_thick", _VP), ("n_thin", _VP), ("sw", _VP), ("smw", _VP),
-        ("st", _VP), ("occ", _VP), ("occ_thr", ctypes.c_double),
+        ("st", _VP), ("occ", _VP), ("occ_thr", ctypes.c_double), ("max_gated", ctypes.c_int64),
     ]
 
 
@@ -57,7 +58,9 @@ def _declare(lib):
         "divas_refine": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP, S, _VP]),
         "divas_fuse_workspace_size": (S, [I64, I32]),
         "divas_fuse": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, S, _VP]),
+        "divas_gate_count": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, _VP]),
         "divas_fuse_gated_count": (_VP, [_VP]),
+        "divas_fuse_overflow": (_VP, [_VP]),
         "divas_gradient_maps": (ctypes.c_int, [I32, I32, I32, _VP, _VP, _VP, _VP, D, D, _VP, _VP]),
         "divas_threshold_workspace_size": (S, [I64]),
         "divas_threshold": (ctypes.c_int, [_VP, I64, D, I64, _VP, _VP, _VP, _VP, S, _VP]),

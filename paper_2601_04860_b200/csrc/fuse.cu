@@ -6,22 +6,34 @@
 // _gradient_maps :684-689), _contract_pt (:243-254), _thick_pair (:257-303),
 // _thin_pair (:306-370) and the value-sorted sums (:373-407).
 //
-// Pipeline (both launches on the caller's stream, no host sync):
+// Three launches on the caller's stream, no host synchronisation:
+//
 //   fuse_gate    dense stream over the slab [lo, hi): 16-byte rho loads, 32-byte
-//                zero stores of p (and optional votes / occupancy), and a
+//                zero stores of p (and optional votes / occupancy) and a
 //                warp-aggregated append of every voxel that clears the exact
 //                density gate  rho >= rho_thr || (enable_thin && rho >= rho_thin)
-//                to a work list.  Below both gates no pair can vote, so p = 0
+//                to the slot list.  Below both gates no pair can vote, so p = 0
 //                exactly ("exact shortcuts").
-//   fuse_sparse  persistent grid (SM count x occupancy) walking the work list,
-//                one voxel per thread, all views per thread.  Camera records
-//                are staged once per CTA in shared memory (broadcast reads).
-//                Contributions are inserted into per-thread sorted scratch so
-//                the sums run in the reference's value-sorted order: results
-//                are bit-identical under view permutation, as the reference's.
+//   fuse_pairs   one thread per (view, gated voxel) pair; grid (slots, views),
+//                so a CTA works on one view and its 256 threads on adjacent
+//                voxels: their centre pixels and footprints are neighbours in
+//                the same view plane (L1/L2 locality).  Decisions that hinge on
+//                a floor / compare of a projected coordinate are CERTIFIED with
+//                a cheap reciprocal-based projection plus a rigorous error
+//                margin; only pairs within the margin of a boundary (or that
+//                reach the thick spatial test, which needs the exact u, v)
+//                evaluate the reference's exact IEEE division chain.  Every
+//                vote-deciding quantity is therefore bit-identical to numba's.
+//                Contributions land in [view][slot] arrays with one bit per
+//                (slot, view) set by atomicOr.
+//   fuse_reduce  one thread per gated voxel: gathers its flagged contributions,
+//                sorts them (w, then m*w; t) and sums in the reference's
+//                value-sorted order -> p bit-identical under view permutation,
+//                writes p, votes, sums and the fused occupancy.
 //
-// Arithmetic: IEEE f64 in the reference's evaluation order, no FMA (this TU is
-// compiled with -fmad=false), binary32 exactly at the 8 numba f32 sites.
+// Arithmetic: IEEE f64 in the reference's evaluation order, no FMA contraction
+// (the TU is compiled with -fmad=false; explicit fma() appears only inside the
+// certified approximations), binary32 exactly at the 8 numba f32 sites.
 #include <algorithm>
 
 #include "common.cuh"
@@ -31,7 +43,8 @@ namespace divas {
 struct FuseConst {
     int64_t g, lo, hi;
     double origin0, origin1, origin2, dx;
-    int nv, hm, wm;
+    int nv, hm, wm, w32;
+    int64_t cap;   // slot capacity of the workspace (max gated voxels)
     double gamma, beta, bmax, lam, rho_thr, rho_thin, thin_pct, alpha1, thin_accept, eps,
         mask_thr, thin_floor, kappa;
     int enable_thin;
@@ -52,6 +65,16 @@ struct FuseMaps {
     const int32_t *nsamps;
 };
 
+struct Contrib {                 // all [view or word][cap]
+    uint32_t *bits_thick, *bits_thin;
+    double *w, *mw, *t;
+};
+
+struct WsHeader {
+    unsigned long long count;    // gated voxels found
+    unsigned int overflow;       // count > cap
+};
+
 // ---------------------------------------------------------------------------
 // dense gate pass
 // ---------------------------------------------------------------------------
@@ -66,7 +89,7 @@ __device__ __forceinline__ bool density_gate(float rho, const FuseConst &C) {
 // warp-uniform strides so all 32 lanes reach the shuffles together.
 __global__ void __launch_bounds__(kGateThreads)
 fuse_gate(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__restrict__ work,
-          unsigned long long *__restrict__ count) {
+          WsHeader *__restrict__ hdr, int count_only) {
     const int lane = threadIdx.x & 31;
     const int64_t n = C.hi - C.lo;
     const int64_t nquads = (n + 3) / 4;
@@ -77,44 +100,41 @@ fuse_gate(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__re
          wbase += stride) {
         const int64_t q = wbase + lane;
         const int64_t base = C.lo + 4 * q;
-        float r[4];
+        float r[4] = {0.f, 0.f, 0.f, 0.f};
         int k4 = 0;
         if (q < nquads) {
-            { const int64_t left = C.hi - base; k4 = left < 4 ? (int)left : 4; }
+            const int64_t left = C.hi - base;
+            k4 = left < 4 ? (int)left : 4;
             if (aligned && k4 == 4) {
                 const float4 v = __ldg(reinterpret_cast<const float4 *>(dens + base));
                 r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
             } else {
-                for (int k = 0; k < 4; ++k) r[k] = k < k4 ? __ldg(dens + base + k) : 0.f;
+                for (int k = 0; k < k4; ++k) r[k] = __ldg(dens + base + k);
             }
-            if (aligned && k4 == 4) {
-                const double2 z2 = make_double2(0.0, 0.0);
-                __stcs(reinterpret_cast<double2 *>(O.probs + base), z2);
-                __stcs(reinterpret_cast<double2 *>(O.probs + base) + 1, z2);
-                if (O.n_thick) *reinterpret_cast<int4 *>(O.n_thick + base) = make_int4(0, 0, 0, 0);
-                if (O.n_thin) *reinterpret_cast<int4 *>(O.n_thin + base) = make_int4(0, 0, 0, 0);
-                if (O.sw) {
-                    reinterpret_cast<double2 *>(O.sw + base)[0] = z2;
-                    reinterpret_cast<double2 *>(O.sw + base)[1] = z2;
-                }
-                if (O.smw) {
-                    reinterpret_cast<double2 *>(O.smw + base)[0] = z2;
-                    reinterpret_cast<double2 *>(O.smw + base)[1] = z2;
-                }
-                if (O.st) {
-                    reinterpret_cast<double2 *>(O.st + base)[0] = z2;
-                    reinterpret_cast<double2 *>(O.st + base)[1] = z2;
-                }
-                if (O.occ) *reinterpret_cast<uchar4 *>(O.occ + base) = make_uchar4(occ0, occ0, occ0, occ0);
-            } else {
-                for (int k = 0; k < k4; ++k) {
-                    O.probs[base + k] = 0.0;
-                    if (O.n_thick) O.n_thick[base + k] = 0;
-                    if (O.n_thin) O.n_thin[base + k] = 0;
-                    if (O.sw) O.sw[base + k] = 0.0;
-                    if (O.smw) O.smw[base + k] = 0.0;
-                    if (O.st) O.st[base + k] = 0.0;
-                    if (O.occ) O.occ[base + k] = occ0;
+            if (!count_only) {
+                if (aligned && k4 == 4) {
+                    const double2 z2 = make_double2(0.0, 0.0);
+                    __stcs(reinterpret_cast<double2 *>(O.probs + base), z2);
+                    __stcs(reinterpret_cast<double2 *>(O.probs + base) + 1, z2);
+                    if (O.n_thick) *reinterpret_cast<int4 *>(O.n_thick + base) = make_int4(0, 0, 0, 0);
+                    if (O.n_thin) *reinterpret_cast<int4 *>(O.n_thin + base) = make_int4(0, 0, 0, 0);
+                    double *sums[3] = {O.sw, O.smw, O.st};
+                    for (int s = 0; s < 3; ++s)
+                        if (sums[s]) {
+                            reinterpret_cast<double2 *>(sums[s] + base)[0] = z2;
+                            reinterpret_cast<double2 *>(sums[s] + base)[1] = z2;
+                        }
+                    if (O.occ) *reinterpret_cast<uchar4 *>(O.occ + base) = make_uchar4(occ0, occ0, occ0, occ0);
+                } else {
+                    for (int k = 0; k < k4; ++k) {
+                        O.probs[base + k] = 0.0;
+                        if (O.n_thick) O.n_thick[base + k] = 0;
+                        if (O.n_thin) O.n_thin[base + k] = 0;
+                        if (O.sw) O.sw[base + k] = 0.0;
+                        if (O.smw) O.smw[base + k] = 0.0;
+                        if (O.st) O.st[base + k] = 0.0;
+                        if (O.occ) O.occ[base + k] = occ0;
+                    }
                 }
             }
         }
@@ -130,31 +150,33 @@ fuse_gate(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__re
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         if (total == 0) continue;
         unsigned long long slot = 0;
-        if (lane == 31) slot = atomicAdd(count, (unsigned long long)total);
+        if (lane == 31) slot = atomicAdd(&hdr->count, (unsigned long long)total);
         slot = __shfl_sync(0xffffffffu, slot, 31) + (unsigned long long)(incl - cnt);
+        if (count_only) continue;
         while (bits) {
             const int k = __ffs(bits) - 1;
             bits &= bits - 1;
-            work[slot++] = (uint32_t)(base + k);
+            if ((long long)slot < C.cap) work[slot] = (uint32_t)(base + k);
+            else hdr->overflow = 1u;
+            ++slot;
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// per-pair arithmetic (exact restatement of the reference helpers)
+// exact restatement of the reference helpers
 // ---------------------------------------------------------------------------
 struct Cam {
-    const double *r;   // r[9] row-major: r[row*3 + col]
+    double r[9];   // row-major: r[row*3 + col]
     double p0, p1, p2, fx, fy, cx, cy, w, h;
 };
 
-__device__ __forceinline__ Cam load_cam(const double *s, int v) {
-    const double *c = s + v * kCamStride;
-    Cam k;
-    k.r = c;
-    k.p0 = c[9]; k.p1 = c[10]; k.p2 = c[11];
-    k.fx = c[12]; k.fy = c[13]; k.cx = c[14]; k.cy = c[15]; k.w = c[16]; k.h = c[17];
-    return k;
+__device__ __forceinline__ void load_cam(const double *__restrict__ c, Cam &k) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) k.r[i] = __ldg(c + i);
+    k.p0 = __ldg(c + 9); k.p1 = __ldg(c + 10); k.p2 = __ldg(c + 11);
+    k.fx = __ldg(c + 12); k.fy = __ldg(c + 13); k.cx = __ldg(c + 14); k.cy = __ldg(c + 15);
+    k.w = __ldg(c + 16); k.h = __ldg(c + 17);
 }
 
 // _project_px (fusion.py:170-184); returns in_front, writes u, v, d
@@ -213,11 +235,12 @@ __device__ __forceinline__ double grad_at(const float *__restrict__ dexp,
     return g;
 }
 
-// _thick_pair (fusion.py:257-303); returns ok, writes the depth weight
-__device__ __forceinline__ bool thick_pair(const FuseConst &C, const Cam &k, double xc0,
+// _thick_pair's spatial half and weight (fusion.py:268-303).  The depth test
+// |x_d - dexp| <= tau_dp is evaluated by the caller first: both are pure, so
+// the conjunction's value is unchanged.
+__device__ __noinline__ bool thick_spatial(const FuseConst &C, const Cam &k, double xc0,
                                            double xc1, double xc2, double u, double v,
-                                           double x_d, float dmin, float dmax, float dexp,
-                                           int32_t nsamp, double g, double &wd) {
+                                           float dmin, float dmax, double g, double &wd) {
     const double *R = k.r;
     const double rx = (u * k.w - k.cx) / k.fx;
     const double ry = (k.cy - v * k.h) / k.fy;
@@ -253,28 +276,110 @@ __device__ __forceinline__ bool thick_pair(const FuseConst &C, const Cam &k, dou
     const double delta = sqrt(dx * dx + dy * dy + dz * dz);
     const float span = dmax - dmin;                                   // f32 site
     const double tau_sp = C.dx * g + C.lam * (double)span;
-    double b = C.beta * (double)nsamp;
-    if (b > C.bmax) b = C.bmax;
-    const double tau_dp = (C.gamma + b) * C.dx;
-    const bool ok = (delta <= tau_sp) && (fabs(x_d - (double)dexp) <= tau_dp);
+    if (!(delta <= tau_sp)) return false;
     const float msum = dmin + dmax;                                   // f32 site
     const double mu = 0.5 * (double)msum;
     double hd = 0.5 * (double)span;                                   // f32 site
     if (hd < C.eps) hd = C.eps;
     const double r = fabs(t_c - mu) / hd;
     wd = exp(-C.alpha1 * r * r);
-    return ok;
+    return true;
 }
 
-// _thin_pair (fusion.py:306-370); returns ok_footprint, writes npix and t
-__device__ __forceinline__ bool thin_pair(const FuseConst &C, const Cam &k, double xc0,
-                                          double xc1, double xc2, double x_d,
-                                          const float *__restrict__ mask,
-                                          const float *__restrict__ dexp,
-                                          const int32_t *__restrict__ nsamp, long long &npix_out,
-                                          double &t_out) {
+// ---------------------------------------------------------------------------
+// certified fast projection
+// ---------------------------------------------------------------------------
+// Reciprocal accurate to ~1 ulp: f32 seed + two Newton steps in f64.  Only
+// used inside certified approximations (never for an output bit).
+__device__ __forceinline__ double rcp_fast(double d) {
+    double r = (double)__frcp_rn((float)d);
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
+// Relative error bound of the certified projections.  The exact chain
+// (fl(fl(fl(fx * fl(x/d)) + cx) / w) * w, 5 roundings) and the approximation
+// (rcp_fast, 3 roundings) each deviate from the real value by < 1e-15 times
+// the magnitudes involved; 1e-11 leaves four orders of magnitude of slack.
+constexpr double kCertRel = 1e-11;
+
+// floor(U) certified for |U - exact| <= E; returns false when undecidable.
+__device__ __forceinline__ bool cert_floor(double U, double E, long long &out) {
+    const double f = floor(U);
+    if (U - f > E && (f + 1.0) - U > E && fabs(f) < 9.0e18) { out = (long long)f; return true; }
+    return false;
+}
+
+// Classify one image axis of the centre projection from the approximation
+// Ua ~= fl(u * n) (== numerator of u).  0: certainly outside [0, 1);
+// 1: certainly inside with pixel idx; 2: undecided.
+__device__ __forceinline__ int cert_axis(double Ua, double E, double n, long long &idx) {
+    if (Ua < -E || Ua >= n + E) return 0;
+    if (Ua > E && Ua < n - E && cert_floor(Ua, E, idx)) return 1;
+    return 2;
+}
+
+// ---------------------------------------------------------------------------
+// pair kernel
+// ---------------------------------------------------------------------------
+constexpr int kPairThreads = 256;
+
+// _thin_pair (fusion.py:306-370): footprint bounds from the 8 projected
+// corners, certified; exact corner projections only when undecided.
+__device__ __forceinline__ bool thin_bounds(const FuseConst &C, const Cam &k, double xc0,
+                                            double xc1, double xc2, double d_c, double x_c,
+                                            double y_c, long long &xs, long long &xe,
+                                            long long &ys, long long &ye) {
     const double half = 0.5 * C.dx;
-    double umin = 1e30, umax = -1e30, vmin = 1e30, vmax = -1e30;
+    const double *R = k.r;
+    // corner offsets in camera coordinates
+    const double ox[3] = {half * R[0], half * R[3], half * R[6]};   // d xcam / d(sx, sy, sz)
+    const double oy[3] = {half * R[1], half * R[4], half * R[7]};
+    const double oz[3] = {half * R[2], half * R[5], half * R[8]};
+    const double S = fabs(xc0) + fabs(xc1) + fabs(xc2) + fabs(k.p0) + fabs(k.p1) + fabs(k.p2) +
+                     3.0 * half;
+    const double eabs = 4e-15 * S;   // abs error of the camera-frame corner coordinates
+    long long umin = 0x7fffffffffffffffLL, umax = -0x7fffffffffffffffLL;
+    long long vmin = 0x7fffffffffffffffLL, vmax = -0x7fffffffffffffffLL;
+    bool certain = true;
+#pragma unroll 1
+    for (int j = 0; j < 8; ++j) {
+        const double sx = (j & 1) ? 1.0 : -1.0;
+        const double sy = (j & 2) ? 1.0 : -1.0;
+        const double sz = (j & 4) ? 1.0 : -1.0;
+        const double zc = -d_c + (sx * oz[0] + sy * oz[1] + sz * oz[2]);
+        const double dj = -zc;
+        if (dj <= eabs) {
+            if (dj < -eabs) return false;        // certainly behind the camera
+            certain = false;
+            break;
+        }
+        const double xj = x_c + (sx * ox[0] + sy * ox[1] + sz * ox[2]);
+        const double yj = y_c + (sx * oy[0] + sy * oy[1] + sz * oy[2]);
+        const double r = rcp_fast(dj);
+        const double A = k.fx * xj * r;
+        const double B = k.fy * yj * r;
+        // |dA| <= fx * eabs * (d + |x|) / d^2 from the coordinate error, plus the
+        // rounding of both chains (kCertRel * magnitude)
+        const double id2 = r * r;
+        const double EU = kCertRel * (fabs(A) + fabs(k.cx) + 1.0) + 4.0 * k.fx * eabs * (dj + fabs(xj)) * id2;
+        const double EV = kCertRel * (fabs(B) + fabs(k.cy) + 1.0) + 4.0 * k.fy * eabs * (dj + fabs(yj)) * id2;
+        long long fu, fv;
+        if (!cert_floor(A + k.cx, EU, fu) || !cert_floor(k.cy - B, EV, fv)) {
+            certain = false;
+            break;
+        }
+        umin = min(umin, fu); umax = max(umax, fu);
+        vmin = min(vmin, fv); vmax = max(vmax, fv);
+    }
+    if (certain) {
+        xs = umin; xe = umax; ys = vmin; ye = vmax;
+        return true;
+    }
+    // exact corner chain (fusion.py:315-341)
+    double umn = 1e30, umx = -1e30, vmn = 1e30, vmx = -1e30;
 #pragma unroll 1
     for (int j = 0; j < 8; ++j) {
         const double sx = ((j & 1) == 0) ? -1.0 : 1.0;
@@ -283,22 +388,117 @@ __device__ __forceinline__ bool thin_pair(const FuseConst &C, const Cam &k, doub
         double cu, cv, cd;
         if (!project_px(k, xc0 + sx * half, xc1 + sy * half, xc2 + sz * half, cu, cv, cd))
             return false;
-        if (cu < umin) umin = cu;
-        if (cu > umax) umax = cu;
-        if (cv < vmin) vmin = cv;
-        if (cv > vmax) vmax = cv;
+        if (cu < umn) umn = cu;
+        if (cu > umx) umx = cu;
+        if (cv < vmn) vmn = cv;
+        if (cv > vmx) vmx = cv;
     }
-    const long long wi = (long long)k.w;
-    const long long hi = (long long)k.h;
-    long long xs = nb_floor_int(umin * k.w);
-    long long xe = nb_floor_int(umax * k.w);
-    long long ys = nb_floor_int(vmin * k.h);
-    long long ye = nb_floor_int(vmax * k.h);
-    if (xe < 0 || xs > wi - 1 || ye < 0 || ys > hi - 1) return false;
+    xs = nb_floor_int(umn * k.w);
+    xe = nb_floor_int(umx * k.w);
+    ys = nb_floor_int(vmn * k.h);
+    ye = nb_floor_int(vmx * k.h);
+    return true;
+}
+
+__global__ void __launch_bounds__(kPairThreads)
+fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
+           FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
+           const WsHeader *__restrict__ hdr) {
+    const long long n = min((long long)hdr->count, (long long)C.cap);
+    const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= n) return;
+    const int view = blockIdx.y;
+    Cam k;
+    load_cam(cams + (int64_t)view * kCamStride, k);
+    const uint32_t vi = __ldg(work + slot);
+    const uint32_t g = (uint32_t)C.g, gg = g * g;
+    const uint32_t ix = vi / gg;
+    const uint32_t rem = vi - ix * gg;
+    const uint32_t iy = rem / g;
+    const uint32_t iz = rem - iy * g;
+    const double rho = (double)__ldg(dens + vi);
+    const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
+    const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
+    const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
+
+    // centre projection: exact camera-frame coordinates (no division)
+    const double relx = xc0 - k.p0;
+    const double rely = xc1 - k.p1;
+    const double relz = xc2 - k.p2;
+    const double zc = k.r[2] * relx + k.r[5] * rely + k.r[8] * relz;
+    const double x_d = -zc;
+    if (!(x_d > 0.0)) return;                                  // behind the camera
+    const double xcam = k.r[0] * relx + k.r[3] * rely + k.r[6] * relz;
+    const double ycam = k.r[1] * relx + k.r[4] * rely + k.r[7] * relz;
+
+    // frustum + pixel: certified from one reciprocal, exact chain otherwise
+    const double r = rcp_fast(x_d);
+    const double A = k.fx * xcam * r;
+    const double B = k.fy * ycam * r;
+    long long px, py;
+    const int cu = cert_axis(A + k.cx, kCertRel * (fabs(A) + fabs(k.cx) + 1.0), k.w, px);
+    const int cv = cert_axis(k.cy - B, kCertRel * (fabs(B) + fabs(k.cy) + 1.0), k.h, py);
+    if (cu == 0 || cv == 0) return;
+    bool have_uv = false;
+    double u = 0.0, v = 0.0;
+    if (cu == 2 || cv == 2) {
+        u = (k.fx * (xcam / x_d) + k.cx) / k.w;
+        v = (k.cy - k.fy * (ycam / x_d)) / k.h;
+        have_uv = true;
+        if (u < 0.0 || u >= 1.0 || v < 0.0 || v >= 1.0) return;
+        px = pixel_index(u, (long long)k.w);
+        py = pixel_index(v, (long long)k.h);
+    }
+    const int64_t vplane = (int64_t)view * C.hm * C.wm;
+    const int64_t pix = vplane + py * (int64_t)C.wm + px;
+    const int32_t ns = __ldg(M.nsamps + pix);
+    if (ns <= 0) return;                                       // valids[view, py, px] == 0
+    const float m = __ldg(M.masks + pix);
+    const int64_t kidx = (int64_t)view * C.cap + slot;
+    const uint32_t bit = 1u << (view & 31);
+    const int64_t bidx = (int64_t)(view >> 5) * C.cap + slot;
+
+    if ((double)m >= C.mask_thr && rho >= C.rho_thr) {
+        const float dexp = __ldg(M.dexps + pix);
+        double b = C.beta * (double)ns;
+        if (b > C.bmax) b = C.bmax;
+        const double tau_dp = (C.gamma + b) * C.dx;
+        if (fabs(x_d - (double)dexp) <= tau_dp) {
+            if (!have_uv) {   // the spatial test needs the exact u, v bits
+                u = (k.fx * (xcam / x_d) + k.cx) / k.w;
+                v = (k.cy - k.fy * (ycam / x_d)) / k.h;
+            }
+            const double gr = grad_at(M.dexps + vplane, M.dmins + vplane, M.dmaxs + vplane, C.hm,
+                                      C.wm, (int)px, (int)py, C.eps, C.kappa);
+            double wd;
+            if (thick_spatial(C, k, xc0, xc1, xc2, u, v, __ldg(M.dmins + pix),
+                              __ldg(M.dmaxs + pix), gr, wd)) {
+                K.w[kidx] = wd;
+                K.mw[kidx] = (double)m * wd;
+                atomicOr(K.bits_thick + bidx, bit);
+                return;                                        // routed thick
+            }
+        }
+    }
+    if (!C.enable_thin) return;
+    if (!((double)m > C.thin_floor && rho >= C.rho_thin)) return;
+    {   // dx_vox * fmax / x_d >= 1.0, certified (division monotone and correctly rounded)
+        const double fmax = k.fx > k.fy ? k.fx : k.fy;
+        const double a = C.dx * fmax;
+        if (a < x_d * (1.0 - 1e-12)) return;
+        if (!(a > x_d * (1.0 + 1e-12)) && !(a / x_d >= 1.0)) return;
+    }
+    long long xs, xe, ys, ye;
+    if (!thin_bounds(C, k, xc0, xc1, xc2, x_d, xcam, ycam, xs, xe, ys, ye)) return;
+    const long long wi = (long long)k.w, hi = (long long)k.h;
+    if (xe < 0 || xs > wi - 1 || ye < 0 || ys > hi - 1) return;
     if (xs < 0) xs = 0;
     if (ys < 0) ys = 0;
     if (xe > wi - 1) xe = wi - 1;
     if (ye > hi - 1) ye = hi - 1;
+    const float *__restrict__ mk = M.masks + vplane;
+    const float *__restrict__ de = M.dexps + vplane;
+    const int32_t *__restrict__ nsp = M.nsamps + vplane;
     long long support = 0, npix = 0;
     double m_max = 0.0;
     const double tau_base = 2.0 * C.gamma;
@@ -306,118 +506,83 @@ __device__ __forceinline__ bool thin_pair(const FuseConst &C, const Cam &k, doub
         const int64_t row = yy * (int64_t)C.wm;
         for (long long xx = xs; xx <= xe; ++xx) {
             npix += 1;
-            const double mv = (double)__ldg(mask + row + xx);
+            const double mv = (double)__ldg(mk + row + xx);
             if (mv > m_max) m_max = mv;
             if (mv > 0.5) {
-                const int32_t ns = __ldg(nsamp + row + xx);
-                if (ns > 0) {
-                    double b = C.beta * (double)ns;
-                    if (b > C.bmax) b = C.bmax;
-                    const double tau_d = (tau_base + b) * C.dx;
-                    if (fabs(x_d - (double)__ldg(dexp + row + xx)) <= tau_d) support += 1;
+                const int32_t nn = __ldg(nsp + row + xx);
+                if (nn > 0) {
+                    double bb = C.beta * (double)nn;
+                    if (bb > C.bmax) bb = C.bmax;
+                    const double tau_d = (tau_base + bb) * C.dx;
+                    if (fabs(x_d - (double)__ldg(de + row + xx)) <= tau_d) support += 1;
                 }
             }
         }
     }
+    if (npix <= 0) return;
     const double p_cov = (double)support / (double)npix;
-    npix_out = npix;
-    t_out = (p_cov >= C.thin_pct) ? m_max : p_cov;
-    return true;
+    const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
+    if (t >= C.thin_accept) {
+        K.t[kidx] = t;
+        atomicOr(K.bits_thin + bidx, bit);
+    }
 }
 
 // ---------------------------------------------------------------------------
-// sparse pass: one gated voxel per thread
+// reduction: value-sorted sums per voxel
 // ---------------------------------------------------------------------------
-constexpr int kFuseThreads = 128;
+constexpr int kReduceThreads = 128;
 
 template <int MAXV>
-__global__ void __launch_bounds__(kFuseThreads)
-fuse_sparse(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
-            FuseMaps M, FuseOut O, const uint32_t *__restrict__ work,
-            const unsigned long long *__restrict__ count) {
-    extern __shared__ double s_cam[];
-    for (int i = threadIdx.x; i < C.nv * kCamStride; i += blockDim.x) s_cam[i] = cams[i];
-    __syncthreads();
-    const unsigned long long n = *count;
-    const int64_t plane = (int64_t)C.hm * C.wm;
-    const int64_t gg = C.g * C.g;
+__global__ void __launch_bounds__(kReduceThreads)
+fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work,
+            const WsHeader *__restrict__ hdr) {
+    const long long n = min((long long)hdr->count, (long long)C.cap);
+    const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= n) return;
     double tw[MAXV], tmw[MAXV], tt[MAXV];
-    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-         t += (unsigned long long)gridDim.x * blockDim.x) {
-        const int64_t vi = (int64_t)work[t];
-        const int64_t ix = vi / gg;
-        const int64_t rem = vi - ix * gg;
-        const int64_t iy = rem / C.g;
-        const int64_t iz = rem - iy * C.g;
-        const double rho = (double)__ldg(dens + vi);
-        const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
-        const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
-        const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
-        int n_thick = 0, n_thin = 0;
-        for (int view = 0; view < C.nv; ++view) {
-            const Cam k = load_cam(s_cam, view);
-            double u, v, x_d;
-            if (!project_px(k, xc0, xc1, xc2, u, v, x_d)) continue;
-            if (u < 0.0 || u >= 1.0 || v < 0.0 || v >= 1.0) continue;
-            const long long px = pixel_index(u, (long long)k.w);
-            const long long py = pixel_index(v, (long long)k.h);
-            const int64_t vplane = (int64_t)view * plane;
-            const int64_t pix = vplane + py * (int64_t)C.wm + px;
-            const int32_t ns = __ldg(M.nsamps + pix);
-            if (ns <= 0) continue;                       // valids[view, py, px] == 0
-            const float m = __ldg(M.masks + pix);
-            bool routed_thick = false;
-            if ((double)m >= C.mask_thr && rho >= C.rho_thr) {
-                const double g = grad_at(M.dexps + vplane, M.dmins + vplane, M.dmaxs + vplane,
-                                         C.hm, C.wm, (int)px, (int)py, C.eps, C.kappa);
-                double wd;
-                if (thick_pair(C, k, xc0, xc1, xc2, u, v, x_d, __ldg(M.dmins + pix),
-                               __ldg(M.dmaxs + pix), __ldg(M.dexps + pix), ns, g, wd)) {
-                    // stable sorted insert by (w, m*w): same order as the
-                    // reference's insertion sort (fusion.py:389-407)
-                    const double km = (double)m * wd;
-                    int j = n_thick - 1;
-                    while (j >= 0 && (tw[j] > wd || (tw[j] == wd && tmw[j] > km))) {
-                        tw[j + 1] = tw[j];
-                        tmw[j + 1] = tmw[j];
-                        --j;
-                    }
-                    tw[j + 1] = wd;
-                    tmw[j + 1] = km;
-                    ++n_thick;
-                    routed_thick = true;
-                }
+    int n_thick = 0, n_thin = 0;
+    for (int wd = 0; wd < C.w32; ++wd) {
+        uint32_t bt = K.bits_thick[(int64_t)wd * C.cap + slot];
+        while (bt) {
+            const int view = wd * 32 + __ffs(bt) - 1;
+            bt &= bt - 1;
+            const double kw = K.w[(int64_t)view * C.cap + slot];
+            const double km = K.mw[(int64_t)view * C.cap + slot];
+            int j = n_thick - 1;   // stable insertion by (w, m*w): fusion.py:389-407
+            while (j >= 0 && (tw[j] > kw || (tw[j] == kw && tmw[j] > km))) {
+                tw[j + 1] = tw[j];
+                tmw[j + 1] = tmw[j];
+                --j;
             }
-            if (!routed_thick && C.enable_thin) {
-                const double fmax = k.fx > k.fy ? k.fx : k.fy;
-                if ((double)m > C.thin_floor && rho >= C.rho_thin && x_d > 0.0 &&
-                    C.dx * fmax / x_d >= 1.0) {
-                    long long npix;
-                    double t_s;
-                    if (thin_pair(C, k, xc0, xc1, xc2, x_d, M.masks + vplane, M.dexps + vplane,
-                                  M.nsamps + vplane, npix, t_s) &&
-                        npix > 0 && t_s >= C.thin_accept) {
-                        int j = n_thin - 1;
-                        while (j >= 0 && tt[j] > t_s) { tt[j + 1] = tt[j]; --j; }
-                        tt[j + 1] = t_s;
-                        ++n_thin;
-                    }
-                }
-            }
+            tw[j + 1] = kw;
+            tmw[j + 1] = km;
+            ++n_thick;
         }
-        double sw = 0.0, smw = 0.0, st = 0.0;
-        for (int i = 0; i < n_thick; ++i) { sw += tw[i]; smw += tmw[i]; }
-        for (int i = 0; i < n_thin; ++i) st += tt[i];
-        const double denom = sw + (double)n_thin;
-        const double p = (denom > C.eps) ? (smw + st) / denom : 0.0;
-        O.probs[vi] = p;
-        if (O.n_thick) O.n_thick[vi] = n_thick;
-        if (O.n_thin) O.n_thin[vi] = n_thin;
-        if (O.sw) O.sw[vi] = sw;
-        if (O.smw) O.smw[vi] = smw;
-        if (O.st) O.st[vi] = st;
-        if (O.occ) O.occ[vi] = (p >= C.occ_thr) ? 1 : 0;
+        uint32_t bn = K.bits_thin[(int64_t)wd * C.cap + slot];
+        while (bn) {
+            const int view = wd * 32 + __ffs(bn) - 1;
+            bn &= bn - 1;
+            const double kt = K.t[(int64_t)view * C.cap + slot];
+            int j = n_thin - 1;    // fusion.py:373-386
+            while (j >= 0 && tt[j] > kt) { tt[j + 1] = tt[j]; --j; }
+            tt[j + 1] = kt;
+            ++n_thin;
+        }
     }
+    double sw = 0.0, smw = 0.0, st = 0.0;
+    for (int i = 0; i < n_thick; ++i) { sw += tw[i]; smw += tmw[i]; }
+    for (int i = 0; i < n_thin; ++i) st += tt[i];
+    const double denom = sw + (double)n_thin;
+    const double p = (denom > C.eps) ? (smw + st) / denom : 0.0;
+    const uint32_t vi = work[slot];
+    O.probs[vi] = p;
+    if (O.n_thick) O.n_thick[vi] = n_thick;
+    if (O.n_thin) O.n_thin[vi] = n_thin;
+    if (O.sw) O.sw[vi] = sw;
+    if (O.smw) O.smw[vi] = smw;
+    if (O.st) O.st[vi] = st;
+    if (O.occ) O.occ[vi] = (p >= C.occ_thr) ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -441,74 +606,46 @@ __global__ void gradient_maps_kernel(int nv, int hm, int wm, const float *__rest
     }
 }
 
-template <int MAXV>
-static int launch_sparse(const FuseConst &C, const double *cams, const float *dens,
-                         const FuseMaps &M, const FuseOut &O, const uint32_t *work,
-                         const unsigned long long *count, cudaStream_t s) {
-    const size_t smem = (size_t)C.nv * kCamStride * sizeof(double);
-    static int blocks_per_sm = 0, n_sm = 0;   // device properties only
-    if (blocks_per_sm == 0) {
+// ---------------------------------------------------------------------------
+// workspace layout
+// ---------------------------------------------------------------------------
+struct WsLayout {
+    size_t work, bits_thick, bits_thin, w, mw, t, total;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static WsLayout ws_layout(int64_t cap, int32_t nv) {
+    const size_t c = (size_t)(cap > 0 ? cap : 1);
+    const size_t w32 = (size_t)((nv + 31) / 32);
+    WsLayout L;
+    size_t off = 256;
+    L.work = off;       off = align256(off + c * 4);
+    L.bits_thick = off; off = align256(off + w32 * c * 4);
+    L.bits_thin = off;  off = align256(off + w32 * c * 4);
+    L.w = off;          off = align256(off + (size_t)nv * c * 8);
+    L.mw = off;         off = align256(off + (size_t)nv * c * 8);
+    L.t = off;          off = align256(off + (size_t)nv * c * 8);
+    L.total = off;
+    return L;
+}
+
+static int sm_count() {
+    static int n = 0;   // device property, same on every B200
+    if (n == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(fuse_sparse<MAXV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
-        int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fuse_sparse<MAXV>, kFuseThreads, smem);
-        blocks_per_sm = b > 0 ? b : 1;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     }
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fuse_sparse<MAXV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    fuse_sparse<MAXV><<<n_sm * blocks_per_sm, kFuseThreads, smem, s>>>(C, cams, dens, M, O, work,
-                                                                        count);
-    return check_launch("divas_fuse(sparse)");
+    return n;
 }
 
-}  // namespace divas
-
-using namespace divas;
-
-extern "C" size_t divas_fuse_workspace_size(int64_t n_vox, int32_t nv) {
-    (void)nv;
-    return 256 + (size_t)(n_vox > 0 ? n_vox : 0) * sizeof(uint32_t);
-}
-
-extern "C" const int64_t *divas_fuse_gated_count(const void *workspace) {
-    return (const int64_t *)workspace;
-}
-
-extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t workspace_bytes,
-                          void *stream) {
-    if (!a) { set_error("divas_fuse: null args"); return DIVAS_EINVAL; }
-    if (a->g < 1) { set_error("divas_fuse: bad grid resolution"); return DIVAS_EINVAL; }
-    const int64_t nvox = a->g * a->g * a->g;
-    if (a->vox_lo < 0 || a->vox_hi > nvox || a->vox_lo > a->vox_hi) {
-        set_error("divas_fuse: voxel range [%lld, %lld) outside [0, %lld)", (long long)a->vox_lo,
-                  (long long)a->vox_hi, (long long)nvox);
-        return DIVAS_EINVAL;
-    }
-    if (nvox > 0xffffffffLL) { set_error("divas_fuse: grid too large for 32-bit work list"); return DIVAS_EINVAL; }
-    if (a->nv < 1 || a->nv > 1024) { set_error("divas_fuse: view count %d outside [1, 1024]", a->nv); return DIVAS_EINVAL; }
-    if (a->hm < 1 || a->wm < 1) { set_error("divas_fuse: empty planes"); return DIVAS_EINVAL; }
-    if (!a->density || !a->cams || !a->masks || !a->dmins || !a->dmaxs || !a->dexps ||
-        !a->nsamps || !a->probs || !workspace) {
-        set_error("divas_fuse: null pointer");
-        return DIVAS_EINVAL;
-    }
-    const int64_t n = a->vox_hi - a->vox_lo;
-    if (workspace_bytes < divas_fuse_workspace_size(n, a->nv)) {
-        set_error("divas_fuse: workspace too small");
-        return DIVAS_EWORKSPACE;
-    }
-    if (n == 0) return DIVAS_OK;
-    cudaStream_t s = (cudaStream_t)stream;
-    FuseConst C;
+static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     C.g = a->g; C.lo = a->vox_lo; C.hi = a->vox_hi;
     C.origin0 = a->origin[0]; C.origin1 = a->origin[1]; C.origin2 = a->origin[2];
     C.dx = a->dx_vox;
-    C.nv = a->nv; C.hm = a->hm; C.wm = a->wm;
+    C.nv = a->nv; C.hm = a->hm; C.wm = a->wm; C.w32 = (a->nv + 31) / 32;
+    C.cap = cap;
     const double *pv = a->pv;
     C.gamma = pv[0]; C.beta = pv[1]; C.bmax = pv[2]; C.lam = pv[3]; C.rho_thr = pv[4];
     C.rho_thin = pv[5]; C.thin_pct = pv[6]; C.alpha1 = pv[7]; C.thin_accept = pv[8];
@@ -518,32 +655,111 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     C.bh0 = a->bh[0]; C.bh1 = a->bh[1]; C.bh2 = a->bh[2];
     C.unbounded = a->unbounded;
     C.occ_thr = a->occ_thr;
+}
+
+static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O, uint32_t *work,
+                        WsHeader *hdr, int count_only, cudaStream_t s) {
+    const int64_t n = C.hi - C.lo;
+    const int64_t nquads = (n + 3) / 4;
+    int64_t blocks = (nquads + kGateThreads - 1) / kGateThreads;
+    blocks = std::min<int64_t>(blocks, (int64_t)sm_count() * 16);
+    fuse_gate<<<(unsigned)std::max<int64_t>(blocks, 1), kGateThreads, 0, s>>>(dens, C, O, work,
+                                                                             hdr, count_only);
+}
+
+}  // namespace divas
+
+using namespace divas;
+
+extern "C" size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv) {
+    return ws_layout(max_gated, nv > 0 ? nv : 1).total;
+}
+
+extern "C" const int64_t *divas_fuse_gated_count(const void *workspace) {
+    return (const int64_t *)workspace;
+}
+
+extern "C" const int32_t *divas_fuse_overflow(const void *workspace) {
+    return (const int32_t *)((const char *)workspace + 8);
+}
+
+static int validate(const divas_fuse_args *a, const char *who) {
+    if (!a) { set_error("%s: null args", who); return DIVAS_EINVAL; }
+    if (a->g < 1) { set_error("%s: bad grid resolution", who); return DIVAS_EINVAL; }
+    const int64_t nvox = a->g * a->g * a->g;
+    if (a->vox_lo < 0 || a->vox_hi > nvox || a->vox_lo > a->vox_hi) {
+        set_error("%s: voxel range [%lld, %lld) outside [0, %lld)", who, (long long)a->vox_lo,
+                  (long long)a->vox_hi, (long long)nvox);
+        return DIVAS_EINVAL;
+    }
+    if (nvox > 0xffffffffLL) { set_error("%s: grid too large for 32-bit slots", who); return DIVAS_EINVAL; }
+    if (!a->density) { set_error("%s: null density", who); return DIVAS_EINVAL; }
+    return DIVAS_OK;
+}
+
+extern "C" int divas_gate_count(const divas_fuse_args *a, void *workspace, void *stream) {
+    int rc = validate(a, "divas_gate_count");
+    if (rc) return rc;
+    if (!workspace) { set_error("divas_gate_count: null workspace"); return DIVAS_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    FuseConst C;
+    fill_const(C, a, 0);
+    WsHeader *hdr = (WsHeader *)workspace;
+    if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess)
+        return check_launch("divas_gate_count(memset)");
+    if (a->vox_hi > a->vox_lo) {
+        FuseOut O{};
+        launch_gate(C, a->density, O, nullptr, hdr, 1, s);
+    }
+    return check_launch("divas_gate_count");
+}
+
+extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t workspace_bytes,
+                          void *stream) {
+    int rc = validate(a, "divas_fuse");
+    if (rc) return rc;
+    if (a->nv < 1 || a->nv > 1024) { set_error("divas_fuse: view count %d outside [1, 1024]", a->nv); return DIVAS_EINVAL; }
+    if (a->nv > 65535) { set_error("divas_fuse: too many views"); return DIVAS_EINVAL; }
+    if (a->hm < 1 || a->wm < 1) { set_error("divas_fuse: empty planes"); return DIVAS_EINVAL; }
+    if (!a->cams || !a->masks || !a->dmins || !a->dmaxs || !a->dexps || !a->nsamps ||
+        !a->probs || !workspace) {
+        set_error("divas_fuse: null pointer");
+        return DIVAS_EINVAL;
+    }
+    const int64_t cap = a->max_gated > 0 ? a->max_gated : (a->vox_hi - a->vox_lo);
+    const WsLayout L = ws_layout(cap, a->nv);
+    if (workspace_bytes < L.total) {
+        set_error("divas_fuse: workspace too small (%zu < %zu)", workspace_bytes, L.total);
+        return DIVAS_EWORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    FuseConst C;
+    fill_const(C, a, cap);
     FuseOut O{a->probs, a->n_thick, a->n_thin, a->sw, a->smw, a->st, a->occ};
     FuseMaps M{a->masks, a->dmins, a->dmaxs, a->dexps, a->nsamps};
-    unsigned long long *count = (unsigned long long *)workspace;
-    uint32_t *work = (uint32_t *)((char *)workspace + 256);
-    if (cudaMemsetAsync(count, 0, sizeof(unsigned long long), s) != cudaSuccess)
+    char *ws = (char *)workspace;
+    WsHeader *hdr = (WsHeader *)ws;
+    uint32_t *work = (uint32_t *)(ws + L.work);
+    Contrib K{(uint32_t *)(ws + L.bits_thick), (uint32_t *)(ws + L.bits_thin),
+              (double *)(ws + L.w), (double *)(ws + L.mw), (double *)(ws + L.t)};
+    if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess ||
+        cudaMemsetAsync(ws + L.bits_thick, 0, L.w - L.bits_thick, s) != cudaSuccess)
         return check_launch("divas_fuse(memset)");
-    {
-        static int n_sm = 0;
-        if (n_sm == 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        }
-        const int64_t nquads = (n + 3) / 4;
-        int64_t blocks = (nquads + kGateThreads - 1) / kGateThreads;
-        blocks = std::min<int64_t>(blocks, (int64_t)n_sm * 16);
-        fuse_gate<<<(unsigned)std::max<int64_t>(blocks, 1), kGateThreads, 0, s>>>(a->density, C, O,
-                                                                                 work, count);
-        int rc = check_launch("divas_fuse(gate)");
-        if (rc) return rc;
-    }
-    if (a->nv <= 32) return launch_sparse<32>(C, a->cams, a->density, M, O, work, count, s);
-    if (a->nv <= 64) return launch_sparse<64>(C, a->cams, a->density, M, O, work, count, s);
-    if (a->nv <= 128) return launch_sparse<128>(C, a->cams, a->density, M, O, work, count, s);
-    if (a->nv <= 256) return launch_sparse<256>(C, a->cams, a->density, M, O, work, count, s);
-    return launch_sparse<1024>(C, a->cams, a->density, M, O, work, count, s);
+    if (a->vox_hi == a->vox_lo) return DIVAS_OK;
+    launch_gate(C, a->density, O, work, hdr, 0, s);
+    if ((rc = check_launch("divas_fuse(gate)"))) return rc;
+    const int64_t cap_blocks = (cap + kPairThreads - 1) / kPairThreads;
+    if (cap_blocks > 0x7fffffffLL) { set_error("divas_fuse: too many slots"); return DIVAS_EINVAL; }
+    fuse_pairs<<<dim3((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)a->nv), kPairThreads, 0,
+                 s>>>(C, a->cams, a->density, M, K, work, hdr);
+    if ((rc = check_launch("divas_fuse(pairs)"))) return rc;
+    const unsigned rblocks = (unsigned)std::max<int64_t>((cap + kReduceThreads - 1) / kReduceThreads, 1);
+    if (a->nv <= 32) fuse_reduce<32><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+    else if (a->nv <= 64) fuse_reduce<64><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+    else if (a->nv <= 128) fuse_reduce<128><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+    else if (a->nv <= 256) fuse_reduce<256><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+    else fuse_reduce<1024><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+    return check_launch("divas_fuse(reduce)");
 }
 
 extern "C" int divas_gradient_maps(int32_t nv, int32_t hm, int32_t wm, const float *dexps,

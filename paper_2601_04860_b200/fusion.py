@@ -282,9 +282,45 @@ class Fuser:
         self.dx = float(grid.voxel_size())
         self.pv = _params_vector(params)
         self.bc, self.bh, self.unb = bounds_arrays(bounds)
+        self._cap_key = None
+        self._cap = None
+
+    def _args(self, density, lo, hi):
+        a = _native.FuseArgs()
+        a.g = self.g
+        a.origin[:] = self.origin.tolist()
+        a.dx_vox = self.dx
+        a.density = _native.ptr(density)
+        a.pv[:] = self.pv.tolist()
+        a.bc[:] = self.bc.tolist()
+        a.bh[:] = self.bh.tolist()
+        a.unbounded = int(self.unb)
+        a.vox_lo, a.vox_hi = lo, hi
+        return a
+
+    def capacity(self, density, lo, hi, stream=None) -> int:
+        """Exact count of voxels passing the density gate in [lo, hi).
+
+        One counting pass and one host sync per density tensor / range; the
+        result sizes the workspace and is cached (keyed on the tensor's
+        storage and version counter), so repeated fusions stay sync-free.
+        """
+        import ctypes
+        import torch
+        key = (density.data_ptr(), density._version, lo, hi, tuple(self.pv[[4, 5, 13]]))
+        if self._cap_key != key:
+            ws = torch.zeros(256, dtype=torch.uint8, device=density.device)
+            a = self._args(density, lo, hi)
+            _native.check(_native.lib().divas_gate_count(ctypes.byref(a), _native.ptr(ws),
+                                                         _native.stream_handle(stream)),
+                          "divas_gate_count")
+            self._cap = int(ws[:8].view(torch.int64).item())
+            self._cap_key = key
+        return self._cap
 
     def run(self, density, views: DeviceViews, probs=None, stats=False, occ=False,
-            occ_thr=0.5, vox_range=None, workspace=None, stream=None):
+            occ_thr=0.5, vox_range=None, workspace=None, stream=None, max_gated=None):
+        import ctypes
         import torch
         g = self.g
         nvox = g ** 3
@@ -293,6 +329,8 @@ class Fuser:
         if density.dtype != torch.float32 or not density.is_cuda or density.numel() != nvox:
             raise ValueError("density must be a CUDA float32 tensor with G^3 entries")
         density = density.contiguous()
+        cap = max_gated if max_gated is not None else self.capacity(density, lo, hi, stream)
+        cap = max(int(cap), 1)
         if probs is None:
             probs = torch.empty(nvox, dtype=torch.float64, device=dev)
         out = {"probs": probs}
@@ -301,35 +339,28 @@ class Fuser:
             out["n_thin"] = torch.empty(nvox, dtype=torch.int32, device=dev)
             for k in ("sw", "smw", "st"):
                 out[k] = torch.empty(nvox, dtype=torch.float64, device=dev)
-        if occ:
+        if occ is True:
             out["occ"] = torch.empty(nvox, dtype=torch.uint8, device=dev)
+        elif occ is not False and occ is not None:
+            out["occ"] = occ
         lib = _native.lib()
-        wsb = lib.divas_fuse_workspace_size(hi - lo, views.nv)
+        wsb = lib.divas_fuse_workspace_size(cap, views.nv)
         if workspace is None or workspace.numel() < wsb:
             workspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
         out["workspace"] = workspace
-        a = _native.FuseArgs()
-        a.g = g
-        a.origin[:] = self.origin.tolist()
-        a.dx_vox = self.dx
-        a.density = _native.ptr(density)
+        a = self._args(density, lo, hi)
         a.nv, a.hm, a.wm = views.nv, views.hm, views.wm
         a.cams = _native.ptr(views.cams)
         a.masks, a.dmins = _native.ptr(views.masks), _native.ptr(views.dmins)
         a.dmaxs, a.dexps = _native.ptr(views.dmaxs), _native.ptr(views.dexps)
         a.nsamps = _native.ptr(views.nsamps)
-        a.pv[:] = self.pv.tolist()
-        a.bc[:] = self.bc.tolist()
-        a.bh[:] = self.bh.tolist()
-        a.unbounded = int(self.unb)
-        a.vox_lo, a.vox_hi = lo, hi
         a.probs = _native.ptr(probs)
         a.n_thick = _native.ptr(out.get("n_thick"))
         a.n_thin = _native.ptr(out.get("n_thin"))
         a.sw, a.smw, a.st = (_native.ptr(out.get(k)) for k in ("sw", "smw", "st"))
         a.occ = _native.ptr(out.get("occ"))
         a.occ_thr = float(occ_thr)
-        import ctypes
+        a.max_gated = cap
         _native.check(lib.divas_fuse(ctypes.byref(a), _native.ptr(workspace), wsb,
                                      _native.stream_handle(stream)), "divas_fuse")
         return out
@@ -340,9 +371,17 @@ class Fuser:
         return out["workspace"][:8].view(__import__("torch").int64)
 
     @staticmethod
+    def check_overflow(out):
+        """Raise if the last run's workspace capacity was too small (syncs)."""
+        import torch
+        if int(out["workspace"][8:12].view(torch.int32).item()) != 0:
+            raise RuntimeError("divas_fuse: gated voxels exceeded the workspace capacity")
+
+    @staticmethod
     def gated_voxels(out, count=None):
         """Flat indices of the gated voxels (a superset of the nonzero p)."""
         import torch
+        Fuser.check_overflow(out)
         n = int(Fuser.gated_count(out).item()) if count is None else int(count)
         ws = out["workspace"]
         return ws[256:256 + 4 * n].view(torch.int32).to(torch.int64) & 0xffffffff
