@@ -238,7 +238,7 @@ __device__ __forceinline__ double grad_at(const float *__restrict__ dexp,
 // _thick_pair's spatial half and weight (fusion.py:268-303).  The depth test
 // |x_d - dexp| <= tau_dp is evaluated by the caller first: both are pure, so
 // the conjunction's value is unchanged.
-__device__ __noinline__ bool thick_spatial(const FuseConst &C, const Cam &k, double xc0,
+__device__ __forceinline__ bool thick_spatial(const FuseConst &C, const Cam &k, double xc0,
                                            double xc1, double xc2, double u, double v,
                                            float dmin, float dmax, double g, double &wd) {
     const double *R = k.r;
@@ -325,6 +325,14 @@ __device__ __forceinline__ int cert_axis(double Ua, double E, double n, long lon
 // pair kernel
 // ---------------------------------------------------------------------------
 constexpr int kPairThreads = 256;
+constexpr int kTauTable = 512;   // exact thin depth tolerance for n_samples < 512
+
+// (2 gamma + min(beta * n, bmax)) * dx, the reference's ops (fusion.py:362-365)
+__device__ __forceinline__ double tau_thin(const FuseConst &C, int32_t n) {
+    double b = C.beta * (double)n;
+    if (b > C.bmax) b = C.bmax;
+    return (2.0 * C.gamma + b) * C.dx;
+}
 
 // _thin_pair (fusion.py:306-370): footprint bounds from the 8 projected
 // corners, certified; exact corner projections only when undecided.
@@ -400,10 +408,13 @@ __device__ __forceinline__ bool thin_bounds(const FuseConst &C, const Cam &k, do
     return true;
 }
 
-__global__ void __launch_bounds__(kPairThreads)
+__global__ void __launch_bounds__(kPairThreads, 3)
 fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
            FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
            const WsHeader *__restrict__ hdr) {
+    __shared__ double s_tau[kTauTable];
+    for (int i = threadIdx.x; i < kTauTable; i += blockDim.x) s_tau[i] = tau_thin(C, i);
+    __syncthreads();
     const long long n = min((long long)hdr->count, (long long)C.cap);
     const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (slot >= n) return;
@@ -496,29 +507,32 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     if (ys < 0) ys = 0;
     if (xe > wi - 1) xe = wi - 1;
     if (ye > hi - 1) ye = hi - 1;
+    // footprint scan (fusion.py:352-367).  Exactness notes: the f32 -> f64
+    // widening is exact and monotone, so m_max is tracked in f32 (NaN never
+    // updates it, as `mv > m_max` is false) and `mv > 0.5` is the same compare
+    // in f32; tau_d(n) comes from a table built with the reference's ops.
     const float *__restrict__ mk = M.masks + vplane;
     const float *__restrict__ de = M.dexps + vplane;
     const int32_t *__restrict__ nsp = M.nsamps + vplane;
-    long long support = 0, npix = 0;
-    double m_max = 0.0;
-    const double tau_base = 2.0 * C.gamma;
-    for (long long yy = ys; yy <= ye; ++yy) {
-        const int64_t row = yy * (int64_t)C.wm;
-        for (long long xx = xs; xx <= xe; ++xx) {
-            npix += 1;
-            const double mv = (double)__ldg(mk + row + xx);
-            if (mv > m_max) m_max = mv;
-            if (mv > 0.5) {
-                const int32_t nn = __ldg(nsp + row + xx);
+    const int bw = (int)(xe - xs) + 1, bh = (int)(ye - ys) + 1;
+    int support = 0;
+    float m_max32 = 0.0f;
+    int rowoff = (int)ys * C.wm + (int)xs;
+    for (int yy = 0; yy < bh; ++yy, rowoff += C.wm) {
+        for (int xx = 0; xx < bw; ++xx) {
+            const float mv = __ldg(mk + rowoff + xx);
+            if (mv > m_max32) m_max32 = mv;
+            if (mv > 0.5f) {
+                const int32_t nn = __ldg(nsp + rowoff + xx);
                 if (nn > 0) {
-                    double bb = C.beta * (double)nn;
-                    if (bb > C.bmax) bb = C.bmax;
-                    const double tau_d = (tau_base + bb) * C.dx;
-                    if (fabs(x_d - (double)__ldg(de + row + xx)) <= tau_d) support += 1;
+                    const double tau_d = nn < kTauTable ? s_tau[nn] : tau_thin(C, nn);
+                    if (fabs(x_d - (double)__ldg(de + rowoff + xx)) <= tau_d) support += 1;
                 }
             }
         }
     }
+    const long long npix = (long long)bw * bh;
+    const double m_max = (double)m_max32;
     if (npix <= 0) return;
     const double p_cov = (double)support / (double)npix;
     const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
