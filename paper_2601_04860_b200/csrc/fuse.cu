@@ -408,20 +408,21 @@ __device__ __forceinline__ bool thin_bounds(const FuseConst &C, const Cam &k, do
     return true;
 }
 
-__global__ void __launch_bounds__(kPairThreads, 3)
-fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
-           FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
-           const WsHeader *__restrict__ hdr) {
-    __shared__ double s_tau[kTauTable];
-    for (int i = threadIdx.x; i < kTauTable; i += blockDim.x) s_tau[i] = tau_thin(C, i);
-    __syncthreads();
-    const long long n = min((long long)hdr->count, (long long)C.cap);
-    const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (slot >= n) return;
-    const int view = blockIdx.y;
-    Cam k;
-    load_cam(cams + (int64_t)view * kCamStride, k);
-    const uint32_t vi = __ldg(work + slot);
+struct ThinItem {
+    const float *mask;        // top-left pixel of the clipped footprint box
+    const float *dexp;
+    const int32_t *nsamp;
+    double x_d;
+    int bw, bh;
+};
+
+// Per-lane part of one (view, voxel) pair: centre projection, routing, the
+// thick path (exact), and the thin candidate's footprint box.  Returns true
+// when the pair needs a footprint scan (filled into `it`).
+__device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, const float *dens,
+                                           const FuseMaps &M, const Contrib &K, uint32_t vi,
+                                           int view, int64_t kidx, int64_t bidx, uint32_t bit,
+                                           ThinItem &it) {
     const uint32_t g = (uint32_t)C.g, gg = g * g;
     const uint32_t ix = vi / gg;
     const uint32_t rem = vi - ix * gg;
@@ -438,7 +439,7 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     const double relz = xc2 - k.p2;
     const double zc = k.r[2] * relx + k.r[5] * rely + k.r[8] * relz;
     const double x_d = -zc;
-    if (!(x_d > 0.0)) return;                                  // behind the camera
+    if (!(x_d > 0.0)) return false;                            // behind the camera
     const double xcam = k.r[0] * relx + k.r[3] * rely + k.r[6] * relz;
     const double ycam = k.r[1] * relx + k.r[4] * rely + k.r[7] * relz;
 
@@ -449,25 +450,22 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     long long px, py;
     const int cu = cert_axis(A + k.cx, kCertRel * (fabs(A) + fabs(k.cx) + 1.0), k.w, px);
     const int cv = cert_axis(k.cy - B, kCertRel * (fabs(B) + fabs(k.cy) + 1.0), k.h, py);
-    if (cu == 0 || cv == 0) return;
+    if (cu == 0 || cv == 0) return false;
     bool have_uv = false;
     double u = 0.0, v = 0.0;
     if (cu == 2 || cv == 2) {
         u = (k.fx * (xcam / x_d) + k.cx) / k.w;
         v = (k.cy - k.fy * (ycam / x_d)) / k.h;
         have_uv = true;
-        if (u < 0.0 || u >= 1.0 || v < 0.0 || v >= 1.0) return;
+        if (u < 0.0 || u >= 1.0 || v < 0.0 || v >= 1.0) return false;
         px = pixel_index(u, (long long)k.w);
         py = pixel_index(v, (long long)k.h);
     }
     const int64_t vplane = (int64_t)view * C.hm * C.wm;
     const int64_t pix = vplane + py * (int64_t)C.wm + px;
     const int32_t ns = __ldg(M.nsamps + pix);
-    if (ns <= 0) return;                                       // valids[view, py, px] == 0
+    if (ns <= 0) return false;                                 // valids[view, py, px] == 0
     const float m = __ldg(M.masks + pix);
-    const int64_t kidx = (int64_t)view * C.cap + slot;
-    const uint32_t bit = 1u << (view & 31);
-    const int64_t bidx = (int64_t)(view >> 5) * C.cap + slot;
 
     if ((double)m >= C.mask_thr && rho >= C.rho_thr) {
         const float dexp = __ldg(M.dexps + pix);
@@ -487,58 +485,113 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
                 K.w[kidx] = wd;
                 K.mw[kidx] = (double)m * wd;
                 atomicOr(K.bits_thick + bidx, bit);
-                return;                                        // routed thick
+                return false;                                  // routed thick
             }
         }
     }
-    if (!C.enable_thin) return;
-    if (!((double)m > C.thin_floor && rho >= C.rho_thin)) return;
+    if (!C.enable_thin) return false;
+    if (!((double)m > C.thin_floor && rho >= C.rho_thin)) return false;
     {   // dx_vox * fmax / x_d >= 1.0, certified (division monotone and correctly rounded)
         const double fmax = k.fx > k.fy ? k.fx : k.fy;
         const double a = C.dx * fmax;
-        if (a < x_d * (1.0 - 1e-12)) return;
-        if (!(a > x_d * (1.0 + 1e-12)) && !(a / x_d >= 1.0)) return;
+        if (a < x_d * (1.0 - 1e-12)) return false;
+        if (!(a > x_d * (1.0 + 1e-12)) && !(a / x_d >= 1.0)) return false;
     }
     long long xs, xe, ys, ye;
-    if (!thin_bounds(C, k, xc0, xc1, xc2, x_d, xcam, ycam, xs, xe, ys, ye)) return;
+    if (!thin_bounds(C, k, xc0, xc1, xc2, x_d, xcam, ycam, xs, xe, ys, ye)) return false;
     const long long wi = (long long)k.w, hi = (long long)k.h;
-    if (xe < 0 || xs > wi - 1 || ye < 0 || ys > hi - 1) return;
+    if (xe < 0 || xs > wi - 1 || ye < 0 || ys > hi - 1) return false;
     if (xs < 0) xs = 0;
     if (ys < 0) ys = 0;
     if (xe > wi - 1) xe = wi - 1;
     if (ye > hi - 1) ye = hi - 1;
-    // footprint scan (fusion.py:352-367).  Exactness notes: the f32 -> f64
-    // widening is exact and monotone, so m_max is tracked in f32 (NaN never
-    // updates it, as `mv > m_max` is false) and `mv > 0.5` is the same compare
-    // in f32; tau_d(n) comes from a table built with the reference's ops.
-    const float *__restrict__ mk = M.masks + vplane;
-    const float *__restrict__ de = M.dexps + vplane;
-    const int32_t *__restrict__ nsp = M.nsamps + vplane;
-    const int bw = (int)(xe - xs) + 1, bh = (int)(ye - ys) + 1;
-    int support = 0;
-    float m_max32 = 0.0f;
-    int rowoff = (int)ys * C.wm + (int)xs;
-    for (int yy = 0; yy < bh; ++yy, rowoff += C.wm) {
-        for (int xx = 0; xx < bw; ++xx) {
-            const float mv = __ldg(mk + rowoff + xx);
-            if (mv > m_max32) m_max32 = mv;
-            if (mv > 0.5f) {
-                const int32_t nn = __ldg(nsp + rowoff + xx);
-                if (nn > 0) {
-                    const double tau_d = nn < kTauTable ? s_tau[nn] : tau_thin(C, nn);
-                    if (fabs(x_d - (double)__ldg(de + rowoff + xx)) <= tau_d) support += 1;
+    const int64_t off = vplane + ys * (int64_t)C.wm + xs;
+    it.mask = M.masks + off;
+    it.dexp = M.dexps + off;
+    it.nsamp = M.nsamps + off;
+    it.x_d = x_d;
+    it.bw = (int)(xe - xs) + 1;
+    it.bh = (int)(ye - ys) + 1;
+    return true;
+}
+
+__global__ void __launch_bounds__(kPairThreads, 2)
+fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
+           FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
+           const WsHeader *__restrict__ hdr) {
+    __shared__ double s_tau[kTauTable];
+    for (int i = threadIdx.x; i < kTauTable; i += blockDim.x) s_tau[i] = tau_thin(C, i);
+    __syncthreads();
+    const long long n = min((long long)hdr->count, (long long)C.cap);
+    const long long block0 = (long long)blockIdx.x * blockDim.x;
+    if (block0 >= n) return;                                   // whole CTA idle
+    const long long slot = block0 + threadIdx.x;
+    const int view = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    Cam k;
+    load_cam(cams + (int64_t)view * kCamStride, k);
+    const int64_t kidx = (int64_t)view * C.cap + slot;
+    const int64_t bidx = (int64_t)(view >> 5) * C.cap + slot;
+    const uint32_t bit = 1u << (view & 31);
+    ThinItem it;
+    bool has = false;
+    if (slot < n) has = pair_route(C, k, dens, M, K, __ldg(work + slot), view, kidx, bidx, bit, it);
+
+    // Warp-cooperative footprint scans (fusion.py:352-370): the warp walks its
+    // lanes' thin items one at a time, lanes over the box's pixels.  support
+    // is an integer count and m_max a maximum, so the result is independent of
+    // the visiting order.  f32 -> f64 widening is exact and monotone: m_max is
+    // kept in f32 (NaN never updates it, as `mv > m_max` is false there too)
+    // and `mv > 0.5` is the same compare in f32.
+    unsigned pending = __ballot_sync(0xffffffffu, has);
+    while (pending) {
+        const int src = __ffs(pending) - 1;
+        pending &= pending - 1;
+        const float *mk = (const float *)__shfl_sync(0xffffffffu, (unsigned long long)it.mask, src);
+        const float *de = (const float *)__shfl_sync(0xffffffffu, (unsigned long long)it.dexp, src);
+        const int32_t *nsp = (const int32_t *)__shfl_sync(0xffffffffu, (unsigned long long)it.nsamp, src);
+        const double xd = __shfl_sync(0xffffffffu, it.x_d, src);
+        const int bw = __shfl_sync(0xffffffffu, it.bw, src);
+        const int bh = __shfl_sync(0xffffffffu, it.bh, src);
+        int sup = 0;
+        float mmax = 0.0f;
+        int r0, c0, rstep, cstep;
+        if (bw <= 32) {
+            const int rows = 32 / bw;
+            r0 = lane / bw;
+            c0 = lane - r0 * bw;
+            rstep = rows;
+            cstep = bw;                          // one column per lane
+            if (r0 >= rows) r0 = bh;             // surplus lanes idle
+        } else {
+            r0 = 0; c0 = lane; rstep = 1; cstep = 32;
+        }
+        for (int rr = r0; rr < bh; rr += rstep) {
+            const int64_t row = (int64_t)rr * C.wm;
+            for (int cc = c0; cc < bw; cc += cstep) {
+                const float mv = __ldg(mk + row + cc);
+                if (mv > mmax) mmax = mv;
+                if (mv > 0.5f) {
+                    const int32_t nn = __ldg(nsp + row + cc);
+                    if (nn > 0) {
+                        const double tau_d = nn < kTauTable ? s_tau[nn] : tau_thin(C, nn);
+                        if (fabs(xd - (double)__ldg(de + row + cc)) <= tau_d) ++sup;
+                    }
                 }
             }
         }
-    }
-    const long long npix = (long long)bw * bh;
-    const double m_max = (double)m_max32;
-    if (npix <= 0) return;
-    const double p_cov = (double)support / (double)npix;
-    const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
-    if (t >= C.thin_accept) {
-        K.t[kidx] = t;
-        atomicOr(K.bits_thin + bidx, bit);
+        sup = __reduce_add_sync(0xffffffffu, sup);
+        const unsigned mbits = __reduce_max_sync(0xffffffffu, __float_as_uint(mmax));
+        if (lane == src) {
+            const long long npix = (long long)bw * bh;
+            const double m_max = (double)__uint_as_float(mbits);
+            const double p_cov = (double)sup / (double)npix;
+            const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
+            if (npix > 0 && t >= C.thin_accept) {
+                K.t[kidx] = t;
+                atomicOr(K.bits_thin + bidx, bit);
+            }
+        }
     }
 }
 
