@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libdivas_b200.so")
+LIB_PATH = os.environ.get("DIVAS_LIB") or os.path.join(_HERE, "_lib", "libdivas_b200.so")
 
 CAM_STRIDE = 18
 NPARAM = 14

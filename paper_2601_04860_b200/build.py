@@ -50,9 +50,10 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, verbose):
-    obj = os.path.join(OBJDIR, src.replace(".cu", ".o"))
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src, verbose, objdir=None, defines=()):
+    obj = os.path.join(objdir or OBJDIR, src.replace(".cu", ".o"))
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c",
+           os.path.join(CSRC, src), "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -83,12 +84,32 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(out_lib: str, defines) -> str:
+    """Build an experiment variant (extra -D defines) to ``out_lib``; load it with
+    DIVAS_LIB=<out_lib>.  Always a full rebuild into its own object dir."""
+    objdir = out_lib + ".obj"
+    os.makedirs(objdir, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(lambda s: _compile(s, False, objdir, defines), SOURCES))
+    objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
+    r = subprocess.run([nvcc(), *ARCH, "-shared", "-o", out_lib, *objs, "-cudart", "static"],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stderr}")
+    return out_lib
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--variant", help="output .so path for an experiment build")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     args = ap.parse_args()
-    print(build(force=args.force, verbose=args.verbose))
+    if args.variant:
+        print(build_variant(args.variant, args.defines))
+    else:
+        print(build(force=args.force, verbose=args.verbose))
 
 
 if __name__ == "__main__":

@@ -48,6 +48,7 @@ struct FuseConst {
     double gamma, beta, bmax, lam, rho_thr, rho_thin, thin_pct, alpha1, thin_accept, eps,
         mask_thr, thin_floor, kappa;
     int enable_thin;
+    int tau_saturated;   // beta * (kTauTable - 1) >= bmax: the tau table covers every n
     double bc0, bc1, bc2, bh0, bh1, bh2;
     int unbounded;
     double occ_thr;
@@ -515,7 +516,10 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     return true;
 }
 
-__global__ void __launch_bounds__(kPairThreads, 2)
+#ifndef DIVAS_PAIR_MINB
+#define DIVAS_PAIR_MINB 3
+#endif
+__global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
 fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
            FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
            const WsHeader *__restrict__ hdr) {
@@ -537,61 +541,50 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     bool has = false;
     if (slot < n) has = pair_route(C, k, dens, M, K, __ldg(work + slot), view, kidx, bidx, bit, it);
 
-    // Warp-cooperative footprint scans (fusion.py:352-370): the warp walks its
-    // lanes' thin items one at a time, lanes over the box's pixels.  support
-    // is an integer count and m_max a maximum, so the result is independent of
-    // the visiting order.  f32 -> f64 widening is exact and monotone: m_max is
-    // kept in f32 (NaN never updates it, as `mv > m_max` is false there too)
-    // and `mv > 0.5` is the same compare in f32.
-    unsigned pending = __ballot_sync(0xffffffffu, has);
-    while (pending) {
-        const int src = __ffs(pending) - 1;
-        pending &= pending - 1;
-        const float *mk = (const float *)__shfl_sync(0xffffffffu, (unsigned long long)it.mask, src);
-        const float *de = (const float *)__shfl_sync(0xffffffffu, (unsigned long long)it.dexp, src);
-        const int32_t *nsp = (const int32_t *)__shfl_sync(0xffffffffu, (unsigned long long)it.nsamp, src);
-        const double xd = __shfl_sync(0xffffffffu, it.x_d, src);
-        const int bw = __shfl_sync(0xffffffffu, it.bw, src);
-        const int bh = __shfl_sync(0xffffffffu, it.bh, src);
-        int sup = 0;
-        float mmax = 0.0f;
-        int r0, c0, rstep, cstep;
-        if (bw <= 32) {
-            const int rows = 32 / bw;
-            r0 = lane / bw;
-            c0 = lane - r0 * bw;
-            rstep = rows;
-            cstep = bw;                          // one column per lane
-            if (r0 >= rows) r0 = bh;             // surplus lanes idle
-        } else {
-            r0 = 0; c0 = lane; rstep = 1; cstep = 32;
+    if (!has) return;
+    // Footprint scan (fusion.py:352-370), one thread per thin item, branch-free
+    // body with three independent loads per pixel.  Exactness: f32 -> f64
+    // widening is exact and monotone, so m_max is kept in f32 via fmaxf (NaN
+    // never wins, as `mv > m_max` is false in the reference) and `mv > 0.5` is
+    // the same compare in f32; tau_d(n) is read from a table built with the
+    // reference's ops, valid for every n once beta * n saturates at bmax
+    // (C.tau_saturated, checked on the host), else computed inline.
+    const float *__restrict__ mk = it.mask;
+    const float *__restrict__ de = it.dexp;
+    const int32_t *__restrict__ nsp = it.nsamp;
+    const double xd = it.x_d;
+    const int bw = it.bw;
+    const int npix = bw * it.bh;
+    int sup = 0;
+    float mmax = 0.0f;
+    int col = 0, off = 0;
+    if (C.tau_saturated) {
+#pragma unroll 4
+        for (int i = 0; i < npix; ++i) {
+            const float mv = __ldg(mk + off + col);
+            const int32_t nn = __ldg(nsp + off + col);
+            const float dv = __ldg(de + off + col);
+            mmax = fmaxf(mmax, mv);
+            const double tau_d = s_tau[min(max(nn, 0), kTauTable - 1)];
+            sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_d) ? 1 : 0;
+            if (++col == bw) { col = 0; off += C.wm; }
         }
-        for (int rr = r0; rr < bh; rr += rstep) {
-            const int64_t row = (int64_t)rr * C.wm;
-            for (int cc = c0; cc < bw; cc += cstep) {
-                const float mv = __ldg(mk + row + cc);
-                if (mv > mmax) mmax = mv;
-                if (mv > 0.5f) {
-                    const int32_t nn = __ldg(nsp + row + cc);
-                    if (nn > 0) {
-                        const double tau_d = nn < kTauTable ? s_tau[nn] : tau_thin(C, nn);
-                        if (fabs(xd - (double)__ldg(de + row + cc)) <= tau_d) ++sup;
-                    }
-                }
-            }
+    } else {
+        for (int i = 0; i < npix; ++i) {
+            const float mv = __ldg(mk + off + col);
+            const int32_t nn = __ldg(nsp + off + col);
+            const float dv = __ldg(de + off + col);
+            mmax = fmaxf(mmax, mv);
+            sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_thin(C, nn)) ? 1 : 0;
+            if (++col == bw) { col = 0; off += C.wm; }
         }
-        sup = __reduce_add_sync(0xffffffffu, sup);
-        const unsigned mbits = __reduce_max_sync(0xffffffffu, __float_as_uint(mmax));
-        if (lane == src) {
-            const long long npix = (long long)bw * bh;
-            const double m_max = (double)__uint_as_float(mbits);
-            const double p_cov = (double)sup / (double)npix;
-            const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
-            if (npix > 0 && t >= C.thin_accept) {
-                K.t[kidx] = t;
-                atomicOr(K.bits_thin + bidx, bit);
-            }
-        }
+    }
+    const double m_max = (double)mmax;
+    const double p_cov = (double)sup / (double)npix;
+    const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
+    if (npix > 0 && t >= C.thin_accept) {
+        K.t[kidx] = t;
+        atomicOr(K.bits_thin + bidx, bit);
     }
 }
 
@@ -718,6 +711,7 @@ static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     C.rho_thin = pv[5]; C.thin_pct = pv[6]; C.alpha1 = pv[7]; C.thin_accept = pv[8];
     C.eps = pv[9]; C.mask_thr = pv[10]; C.thin_floor = pv[11]; C.kappa = pv[12];
     C.enable_thin = pv[13] != 0.0;
+    C.tau_saturated = (C.beta * (double)(kTauTable - 1) >= C.bmax) ? 1 : 0;
     C.bc0 = a->bc[0]; C.bc1 = a->bc[1]; C.bc2 = a->bc[2];
     C.bh0 = a->bh[0]; C.bh1 = a->bh[1]; C.bh2 = a->bh[2];
     C.unbounded = a->unbounded;
