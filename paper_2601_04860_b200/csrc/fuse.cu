@@ -517,7 +517,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
 }
 
 #ifndef DIVAS_PAIR_MINB
-#define DIVAS_PAIR_MINB 3
+#define DIVAS_PAIR_MINB 4
 #endif
 __global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
 fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
@@ -553,30 +553,32 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     const float *__restrict__ de = it.dexp;
     const int32_t *__restrict__ nsp = it.nsamp;
     const double xd = it.x_d;
-    const int bw = it.bw;
-    const int npix = bw * it.bh;
+    const int bw = it.bw, bh = it.bh;
+    const int npix = bw * bh;
+    const int wm = C.wm;
     int sup = 0;
     float mmax = 0.0f;
-    int col = 0, off = 0;
     if (C.tau_saturated) {
+        for (int r = 0; r < bh; ++r, mk += wm, nsp += wm, de += wm) {
 #pragma unroll 4
-        for (int i = 0; i < npix; ++i) {
-            const float mv = __ldg(mk + off + col);
-            const int32_t nn = __ldg(nsp + off + col);
-            const float dv = __ldg(de + off + col);
-            mmax = fmaxf(mmax, mv);
-            const double tau_d = s_tau[min(max(nn, 0), kTauTable - 1)];
-            sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_d) ? 1 : 0;
-            if (++col == bw) { col = 0; off += C.wm; }
+            for (int c = 0; c < bw; ++c) {
+                const float mv = __ldg(mk + c);
+                const int32_t nn = __ldg(nsp + c);
+                const float dv = __ldg(de + c);
+                mmax = fmaxf(mmax, mv);
+                const double tau_d = s_tau[min(max(nn, 0), kTauTable - 1)];
+                sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_d) ? 1 : 0;
+            }
         }
     } else {
-        for (int i = 0; i < npix; ++i) {
-            const float mv = __ldg(mk + off + col);
-            const int32_t nn = __ldg(nsp + off + col);
-            const float dv = __ldg(de + off + col);
-            mmax = fmaxf(mmax, mv);
-            sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_thin(C, nn)) ? 1 : 0;
-            if (++col == bw) { col = 0; off += C.wm; }
+        for (int r = 0; r < bh; ++r, mk += wm, nsp += wm, de += wm) {
+            for (int c = 0; c < bw; ++c) {
+                const float mv = __ldg(mk + c);
+                const int32_t nn = __ldg(nsp + c);
+                const float dv = __ldg(de + c);
+                mmax = fmaxf(mmax, mv);
+                sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_thin(C, nn)) ? 1 : 0;
+            }
         }
     }
     const double m_max = (double)mmax;
