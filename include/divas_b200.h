@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define DIVAS_ABI_VERSION 2
+#define DIVAS_ABI_VERSION 3
 
 /* error codes */
 #define DIVAS_OK          0
@@ -64,6 +64,17 @@ int divas_refine(int32_t nv, int64_t hm, int64_t wm,
                  const float *mask, const float *z_surface, const int32_t *n_samples,
                  float *out, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Refinement fused with the fusion's per-view depth bands: same `out` as
+ * divas_refine, plus `bands` (divas_bands_size bytes, device) summarising,
+ * per 8x8 pixel tile, the depth interval in which a thin candidate can find
+ * support (pv = FusionParams.as_vector(), dx_vox = voxel size).  Pass the
+ * bands to divas_fuse to skip its own band pass.  Needs dexp [nv][hm][wm]. */
+size_t divas_bands_size(int32_t nv, int64_t hm, int64_t wm);
+int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm,
+                       const float *mask, const float *z_surface, const int32_t *n_samples,
+                       const float *dexp, float *out, const double *pv, double dx_vox,
+                       void *bands, void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---------------------------------------------------------------------- */
 /* Fusion                                                                   */
 /* ---------------------------------------------------------------------- */
@@ -91,11 +102,15 @@ typedef struct divas_fuse_args {
                                     the density gate in [lo, hi); <= 0 means
                                     hi - lo (always safe).  divas_gate_count
                                     gives the exact figure for a density grid. */
+    const void *bands;           /* depth bands from divas_refine_bands for these
+                                    views and pv / dx_vox, or NULL (divas_fuse
+                                    then builds them in its workspace) */
 } divas_fuse_args;
 
 /* Workspace bytes for divas_fuse with slot capacity `max_gated` and `nv` views
- * (~ max_gated * (4 + nv * 24.25) bytes; contributions are [view][slot]). */
-size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv);
+ * of padded size hm x wm (~ max_gated * (4 + nv * 24.25) bytes for the
+ * [view][slot] contributions, plus the depth bands). */
+size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv, int32_t hm, int32_t wm);
 int divas_fuse(const divas_fuse_args *args, void *workspace, size_t workspace_bytes,
                void *stream);
 

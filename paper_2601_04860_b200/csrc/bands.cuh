@@ -1,0 +1,122 @@
+// bands.cuh -- per-view 8x8-tile depth bands for exact thin-path rejection.
+//
+// A footprint pixel p supports a thin candidate at depth x_d iff
+//   mask_p > 0.5 && n_p > 0 && |fl(x_d - D_p)| <= tau(n_p)          (fusion.py:361-367)
+// which implies  D_p - tau(1 + 2^-52) <= x_d <= D_p + tau(1 + 2^-52).  A tile's
+// band is the hull of those intervals over its eligible pixels, widened by a
+// 1e-12 relative margin that dominates every rounding involved.  If x_d lies
+// outside the bands of all tiles that can contain the footprint box, support
+// is exactly 0, so p_cov = 0 and (for thin_percent_cover > 0) t = 0 < thin_accept:
+// the pair cannot vote and needs neither corner projections nor a scan.
+#pragma once
+
+#include "common.cuh"
+
+namespace divas {
+
+constexpr int kBandTile = 8;
+
+struct BandParams {
+    double gamma, beta, bmax, dx;
+    int hm, wm, ntx, nty;
+};
+
+__device__ __forceinline__ void band_px(float m, int32_t n, float d, const BandParams &B,
+                                        double &lo, double &hi) {
+    if (m > 0.5f && n > 0) {
+        double b = B.beta * (double)n;
+        if (b > B.bmax) b = B.bmax;
+        const double t = (2.0 * B.gamma + b) * B.dx;
+        const double D = (double)d;
+        const double mg = 1e-12 * (fabs(D) + t);
+        lo = fmin(lo, D - t - mg);
+        hi = fmax(hi, D + t + mg);
+    }
+}
+
+// One thread per VEC-pixel column chunk and 8 rows; TPW = 8 / VEC threads form
+// a tile row and combine with shuffles.  REFINE: also produce the refined mask
+// from the raw one (segmenter.py:141-152) and band on the refined values.
+template <int VEC, bool REFINE>
+__global__ void __launch_bounds__(256)
+band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict__ z,
+          const int32_t *__restrict__ nsamp, const float *__restrict__ dexp,
+          float *__restrict__ refined, const uint32_t *__restrict__ minmax,
+          double2 *__restrict__ bands, int nv) {
+    constexpr int TPW = kBandTile / VEC;
+    const int v = nv - 1 - (int)blockIdx.z;          // reverse view order: L2 reuse of z / n
+    const int64_t plane = (int64_t)B.hm * B.wm;
+    const int64_t off = (int64_t)v * plane;
+    const int chunk = blockIdx.x * blockDim.x + threadIdx.x;
+    const int x0 = chunk * VEC;
+    const bool active = x0 < B.wm;
+    bool any = false;
+    double lo_ref = 0.0, span = 0.0;
+    if (REFINE) {
+        const uint32_t kmin = minmax[2 * v], kmax = minmax[2 * v + 1];
+        any = kmin <= kmax;
+        lo_ref = any ? (double)key_f32(kmin) : 0.0;
+        const double hi_ref = any ? (double)key_f32(kmax) : 0.0;
+        span = hi_ref - lo_ref;
+    }
+    double lo = __longlong_as_double(0x7ff0000000000000LL);   // +inf
+    double hi = -lo;
+    if (active) {
+        for (int r = 0; r < kBandTile; ++r) {
+            const int row = blockIdx.y * kBandTile + r;
+            if (row >= B.hm) break;
+            const int64_t p = off + (int64_t)row * B.wm + x0;
+            float m[VEC], d[VEC];
+            int32_t n[VEC];
+            if (VEC == 4) {
+                const float4 mm = __ldg(reinterpret_cast<const float4 *>(mask + p));
+                const int4 nn = __ldg(reinterpret_cast<const int4 *>(nsamp + p));
+                const float4 dd = __ldg(reinterpret_cast<const float4 *>(dexp + p));
+                m[0] = mm.x; m[1] = mm.y; m[2] = mm.z; m[3] = mm.w;
+                n[0] = nn.x; n[1] = nn.y; n[2] = nn.z; n[3] = nn.w;
+                d[0] = dd.x; d[1] = dd.y; d[2] = dd.z; d[3] = dd.w;
+                if (REFINE) {
+                    const float4 zz = __ldg(reinterpret_cast<const float4 *>(z + p));
+                    const float zv[4] = {zz.x, zz.y, zz.z, zz.w};
+                    for (int k = 0; k < 4; ++k) m[k] = refine_px(m[k], zv[k], n[k], any, lo_ref, span);
+                    __stcs(reinterpret_cast<float4 *>(refined + p), make_float4(m[0], m[1], m[2], m[3]));
+                }
+            } else {
+                m[0] = __ldg(mask + p);
+                n[0] = __ldg(nsamp + p);
+                d[0] = __ldg(dexp + p);
+                if (REFINE) {
+                    m[0] = refine_px(m[0], __ldg(z + p), n[0], any, lo_ref, span);
+                    refined[p] = m[0];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) band_px(m[k], n[k], d[k], B, lo, hi);
+        }
+    }
+#pragma unroll
+    for (int o = 1; o < TPW; o <<= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (active && (threadIdx.x % TPW) == 0) {
+        const int tx = x0 / kBandTile;
+        bands[((int64_t)v * B.nty + blockIdx.y) * B.ntx + tx] = make_double2(lo, hi);
+    }
+}
+
+inline BandParams band_params(const double *pv, double dx, int hm, int wm) {
+    BandParams B;
+    B.gamma = pv[0]; B.beta = pv[1]; B.bmax = pv[2]; B.dx = dx;
+    B.hm = hm; B.wm = wm;
+    B.ntx = (wm + kBandTile - 1) / kBandTile;
+    B.nty = (hm + kBandTile - 1) / kBandTile;
+    return B;
+}
+
+inline size_t band_bytes(int nv, int hm, int wm) {
+    return (size_t)nv * ((hm + kBandTile - 1) / kBandTile) * ((wm + kBandTile - 1) / kBandTile) *
+           sizeof(double2);
+}
+
+}  // namespace divas

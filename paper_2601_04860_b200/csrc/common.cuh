@@ -33,6 +33,21 @@ __device__ __forceinline__ float key_f32(uint32_t k) {
     return __uint_as_float(b);
 }
 
+// refine_mask per pixel (segmenter.py:141-152): valid pixels get
+// clip(f64(m) * (1 - (z - lo) / (hi - lo)), 0, 1) (zhat = 0 for a constant
+// map), invalid ones 0; then round to f32.
+__device__ __forceinline__ float refine_px(float m, float z, int32_t n, bool any, double lo,
+                                           double span) {
+    double o = 0.0;
+    if (any && n > 0) {
+        const double zh = span > 0.0 ? ((double)z - lo) / span : 0.0;
+        o = (double)m * (1.0 - zh);
+    }
+    if (o < 0.0) o = 0.0;   // np.clip keeps NaN, so do these compares
+    if (o > 1.0) o = 1.0;
+    return __double2float_rn(o);
+}
+
 void set_error(const char *fmt, ...);
 int check_launch(const char *what);
 

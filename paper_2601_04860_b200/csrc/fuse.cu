@@ -36,7 +36,7 @@
 // certified approximations), binary32 exactly at the 8 numba f32 sites.
 #include <algorithm>
 
-#include "common.cuh"
+#include "bands.cuh"
 
 namespace divas {
 
@@ -49,6 +49,9 @@ struct FuseConst {
         mask_thr, thin_floor, kappa;
     int enable_thin;
     int tau_saturated;   // beta * (kTauTable - 1) >= bmax: the tau table covers every n
+    int band_ok;         // thin_percent_cover > 0: zero support can never vote
+    int ntx, nty;        // depth-band tiles per view
+    double cube_r;       // circumradius of a voxel, padded
     double bc0, bc1, bc2, bh0, bh1, bh2;
     int unbounded;
     double occ_thr;
@@ -64,6 +67,7 @@ struct FuseOut {
 struct FuseMaps {
     const float *masks, *dmins, *dmaxs, *dexps;
     const int32_t *nsamps;
+    const double2 *bands;   // [nv][nty][ntx] depth bands (bands.cuh)
 };
 
 struct Contrib {                 // all [view or word][cap]
@@ -335,57 +339,61 @@ __device__ __forceinline__ double tau_thin(const FuseConst &C, int32_t n) {
     return (2.0 * C.gamma + b) * C.dx;
 }
 
+// Reciprocal for certified bounds: f32 seed + one Newton step (rel. error
+// ~2^-46, far inside kCertRel).
+__device__ __forceinline__ double rcp_fast1(double d) {
+    const double r = (double)__frcp_rn((float)d);
+    return fma(r, fma(-d, r, 1.0), r);
+}
+
 // _thin_pair (fusion.py:306-370): footprint bounds from the 8 projected
-// corners, certified; exact corner projections only when undecided.
+// corners.  floor(fl(umin * w)) = min_j floor(fl(u_j * w)) (floor and
+// rounding are monotone), and |min_j a_j - min_j b_j| <= max_j |a_j - b_j|, so
+// it suffices to certify the floors of the approximate min / max with a bound
+// valid for every corner.  Corner camera coordinates are the centre's plus
+// +-half * rotation offsets; their distance to the reference's exact chain
+// is below eabs.  Undecided cases (and corners near the camera plane) run
+// the reference's exact corner chain.
 __device__ __forceinline__ bool thin_bounds(const FuseConst &C, const Cam &k, double xc0,
                                             double xc1, double xc2, double d_c, double x_c,
                                             double y_c, long long &xs, long long &xe,
                                             long long &ys, long long &ye) {
     const double half = 0.5 * C.dx;
     const double *R = k.r;
-    // corner offsets in camera coordinates
-    const double ox[3] = {half * R[0], half * R[3], half * R[6]};   // d xcam / d(sx, sy, sz)
-    const double oy[3] = {half * R[1], half * R[4], half * R[7]};
-    const double oz[3] = {half * R[2], half * R[5], half * R[8]};
     const double S = fabs(xc0) + fabs(xc1) + fabs(xc2) + fabs(k.p0) + fabs(k.p1) + fabs(k.p2) +
                      3.0 * half;
-    const double eabs = 4e-15 * S;   // abs error of the camera-frame corner coordinates
-    long long umin = 0x7fffffffffffffffLL, umax = -0x7fffffffffffffffLL;
-    long long vmin = 0x7fffffffffffffffLL, vmax = -0x7fffffffffffffffLL;
-    bool certain = true;
-#pragma unroll 1
-    for (int j = 0; j < 8; ++j) {
-        const double sx = (j & 1) ? 1.0 : -1.0;
-        const double sy = (j & 2) ? 1.0 : -1.0;
-        const double sz = (j & 4) ? 1.0 : -1.0;
-        const double zc = -d_c + (sx * oz[0] + sy * oz[1] + sz * oz[2]);
-        const double dj = -zc;
-        if (dj <= eabs) {
-            if (dj < -eabs) return false;        // certainly behind the camera
-            certain = false;
-            break;
+    const double eabs = 4e-15 * S;
+    const double rho = C.cube_r;
+    const double dmn = d_c - rho;                  // every corner is at least this deep
+    if (dmn > 2.0 * eabs && d_c < 1e30) {
+        const double ax = half * R[0], bx = half * R[3], cx_ = half * R[6];
+        const double ay = half * R[1], by = half * R[4], cy_ = half * R[7];
+        const double az = half * R[2], bz = half * R[5], cz_ = half * R[8];
+        const double FX = k.fx * x_c, FY = k.fy * y_c;
+        const double fax = k.fx * ax, fbx = k.fx * bx, fcx = k.fx * cx_;
+        const double fay = k.fy * ay, fby = k.fy * by, fcy = k.fy * cy_;
+        double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const double sx = (j & 1) ? 1.0 : -1.0;
+            const double sy = (j & 2) ? 1.0 : -1.0;
+            const double sz = (j & 4) ? 1.0 : -1.0;
+            const double dj = d_c - (sx * az + sy * bz + sz * cz_);
+            const double r = rcp_fast1(dj);
+            const double U = (FX + (sx * fax + sy * fbx + sz * fcx)) * r;
+            const double V = (FY + (sx * fay + sy * fby + sz * fcy)) * r;
+            umin = fmin(umin, U); umax = fmax(umax, U);
+            vmin = fmin(vmin, V); vmax = fmax(vmax, V);
         }
-        const double xj = x_c + (sx * ox[0] + sy * ox[1] + sz * ox[2]);
-        const double yj = y_c + (sx * oy[0] + sy * oy[1] + sz * oy[2]);
-        const double r = rcp_fast(dj);
-        const double A = k.fx * xj * r;
-        const double B = k.fy * yj * r;
-        // |dA| <= fx * eabs * (d + |x|) / d^2 from the coordinate error, plus the
-        // rounding of both chains (kCertRel * magnitude)
-        const double id2 = r * r;
-        const double EU = kCertRel * (fabs(A) + fabs(k.cx) + 1.0) + 4.0 * k.fx * eabs * (dj + fabs(xj)) * id2;
-        const double EV = kCertRel * (fabs(B) + fabs(k.cy) + 1.0) + 4.0 * k.fy * eabs * (dj + fabs(yj)) * id2;
-        long long fu, fv;
-        if (!cert_floor(A + k.cx, EU, fu) || !cert_floor(k.cy - B, EV, fv)) {
-            certain = false;
-            break;
-        }
-        umin = min(umin, fu); umax = max(umax, fu);
-        vmin = min(vmin, fv); vmax = max(vmax, fv);
-    }
-    if (certain) {
-        xs = umin; xe = umax; ys = vmin; ye = vmax;
-        return true;
+        const double idm = rcp_fast1(dmn) * (1.0 + 1e-9);
+        const double mx = fabs(x_c) + rho, my = fabs(y_c) + rho;
+        const double EU = kCertRel * (k.fx * mx * idm + fabs(k.cx) + 1.0) +
+                          4.0 * k.fx * eabs * (d_c + rho + mx) * idm * idm;
+        const double EV = kCertRel * (k.fy * my * idm + fabs(k.cy) + 1.0) +
+                          4.0 * k.fy * eabs * (d_c + rho + my) * idm * idm;
+        if (cert_floor(umin + k.cx, EU, xs) && cert_floor(umax + k.cx, EU, xe) &&
+            cert_floor(k.cy - vmax, EV, ys) && cert_floor(k.cy - vmin, EV, ye))
+            return true;
     }
     // exact corner chain (fusion.py:315-341)
     double umn = 1e30, umx = -1e30, vmn = 1e30, vmx = -1e30;
@@ -407,6 +415,34 @@ __device__ __forceinline__ bool thin_bounds(const FuseConst &C, const Cam &k, do
     ys = nb_floor_int(vmn * k.h);
     ye = nb_floor_int(vmx * k.h);
     return true;
+}
+
+// Exact rejection through the depth bands (bands.cuh): the footprint box lies
+// within +-R pixels of the centre projection, R bounding the projected
+// circumsphere of the voxel.  Returns true when no box pixel can support x_d.
+__device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &M, const Cam &k,
+                                            int view, double x_d, double xcam, double ycam,
+                                            double Uc, double Vc) {
+    const double rho = C.cube_r;
+    if (!(x_d > 2.0 * rho)) return false;
+    const double inv = rcp_fast1(x_d * (x_d - rho)) * (1.0 + 1e-9);
+    const double Ru = k.fx * rho * (x_d + fabs(xcam)) * inv + 2.0;
+    const double Rv = k.fy * rho * (x_d + fabs(ycam)) * inv + 2.0;
+    const double fx0 = floor((Uc - Ru) * (1.0 / kBandTile)), fx1 = floor((Uc + Ru) * (1.0 / kBandTile));
+    const double fy0 = floor((Vc - Rv) * (1.0 / kBandTile)), fy1 = floor((Vc + Rv) * (1.0 / kBandTile));
+    const int tx0 = (int)fmax(fx0, 0.0), tx1 = (int)fmin(fx1, (double)(C.ntx - 1));
+    const int ty0 = (int)fmax(fy0, 0.0), ty1 = (int)fmin(fy1, (double)(C.nty - 1));
+    if (tx1 < tx0 || ty1 < ty0) return false;
+    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16) return false;
+    double lo = 1e300, hi = -1e300;
+    const double2 *bv = M.bands + (int64_t)view * C.nty * C.ntx;
+    for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx) {
+            const double2 b = bv[ty * C.ntx + tx];
+            lo = fmin(lo, b.x);
+            hi = fmax(hi, b.y);
+        }
+    return !(x_d >= lo && x_d <= hi);
 }
 
 struct ThinItem {
@@ -498,6 +534,8 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
         if (a < x_d * (1.0 - 1e-12)) return false;
         if (!(a > x_d * (1.0 + 1e-12)) && !(a / x_d >= 1.0)) return false;
     }
+    if (C.band_ok && band_reject(C, M, k, view, x_d, xcam, ycam, A + k.cx, k.cy - B))
+        return false;                                          // support is exactly 0
     long long xs, xe, ys, ye;
     if (!thin_bounds(C, k, xc0, xc1, xc2, x_d, xcam, ycam, xs, xe, ys, ye)) return false;
     const long long wi = (long long)k.w, hi = (long long)k.h;
@@ -517,7 +555,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
 }
 
 #ifndef DIVAS_PAIR_MINB
-#define DIVAS_PAIR_MINB 4
+#define DIVAS_PAIR_MINB 3
 #endif
 __global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
 fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
@@ -553,36 +591,34 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     const float *__restrict__ de = it.dexp;
     const int32_t *__restrict__ nsp = it.nsamp;
     const double xd = it.x_d;
-    const int bw = it.bw, bh = it.bh;
-    const int npix = bw * bh;
-    const int wm = C.wm;
+    const int bw = it.bw;
+    const int npix = bw * it.bh;
     int sup = 0;
     float mmax = 0.0f;
+    int col = 0, off = 0;
     if (C.tau_saturated) {
-        for (int r = 0; r < bh; ++r, mk += wm, nsp += wm, de += wm) {
 #pragma unroll 4
-            for (int c = 0; c < bw; ++c) {
-                const float mv = __ldg(mk + c);
-                const int32_t nn = __ldg(nsp + c);
-                const float dv = __ldg(de + c);
-                mmax = fmaxf(mmax, mv);
-                const double tau_d = s_tau[min(max(nn, 0), kTauTable - 1)];
-                sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_d) ? 1 : 0;
-            }
+        for (int i = 0; i < npix; ++i) {
+            const float mv = __ldg(mk + off + col);
+            const int32_t nn = __ldg(nsp + off + col);
+            const float dv = __ldg(de + off + col);
+            mmax = fmaxf(mmax, mv);
+            const double tau_d = s_tau[min(max(nn, 0), kTauTable - 1)];
+            sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_d) ? 1 : 0;
+            if (++col == bw) { col = 0; off += C.wm; }
         }
     } else {
-        for (int r = 0; r < bh; ++r, mk += wm, nsp += wm, de += wm) {
-            for (int c = 0; c < bw; ++c) {
-                const float mv = __ldg(mk + c);
-                const int32_t nn = __ldg(nsp + c);
-                const float dv = __ldg(de + c);
-                mmax = fmaxf(mmax, mv);
-                sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_thin(C, nn)) ? 1 : 0;
-            }
+        for (int i = 0; i < npix; ++i) {
+            const float mv = __ldg(mk + off + col);
+            const int32_t nn = __ldg(nsp + off + col);
+            const float dv = __ldg(de + off + col);
+            mmax = fmaxf(mmax, mv);
+            sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_thin(C, nn)) ? 1 : 0;
+            if (++col == bw) { col = 0; off += C.wm; }
         }
     }
     const double m_max = (double)mmax;
-    const double p_cov = (double)sup / (double)npix;
+    const double p_cov = sup == 0 ? 0.0 : (double)sup / (double)npix;
     const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
     if (npix > 0 && t >= C.thin_accept) {
         K.t[kidx] = t;
@@ -672,12 +708,12 @@ __global__ void gradient_maps_kernel(int nv, int hm, int wm, const float *__rest
 // workspace layout
 // ---------------------------------------------------------------------------
 struct WsLayout {
-    size_t work, bits_thick, bits_thin, w, mw, t, total;
+    size_t work, bits_thick, bits_thin, w, mw, t, bands, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static WsLayout ws_layout(int64_t cap, int32_t nv) {
+static WsLayout ws_layout(int64_t cap, int32_t nv, int32_t hm, int32_t wm) {
     const size_t c = (size_t)(cap > 0 ? cap : 1);
     const size_t w32 = (size_t)((nv + 31) / 32);
     WsLayout L;
@@ -688,6 +724,7 @@ static WsLayout ws_layout(int64_t cap, int32_t nv) {
     L.w = off;          off = align256(off + (size_t)nv * c * 8);
     L.mw = off;         off = align256(off + (size_t)nv * c * 8);
     L.t = off;          off = align256(off + (size_t)nv * c * 8);
+    L.bands = off;      off = align256(off + band_bytes(nv, hm, wm));
     L.total = off;
     return L;
 }
@@ -714,6 +751,10 @@ static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     C.eps = pv[9]; C.mask_thr = pv[10]; C.thin_floor = pv[11]; C.kappa = pv[12];
     C.enable_thin = pv[13] != 0.0;
     C.tau_saturated = (C.beta * (double)(kTauTable - 1) >= C.bmax) ? 1 : 0;
+    C.band_ok = C.thin_pct > 0.0 ? 1 : 0;
+    C.ntx = (a->wm + kBandTile - 1) / kBandTile;
+    C.nty = (a->hm + kBandTile - 1) / kBandTile;
+    C.cube_r = 0.8660254037844387 * a->dx_vox * (1.0 + 1e-9);
     C.bc0 = a->bc[0]; C.bc1 = a->bc[1]; C.bc2 = a->bc[2];
     C.bh0 = a->bh[0]; C.bh1 = a->bh[1]; C.bh2 = a->bh[2];
     C.unbounded = a->unbounded;
@@ -734,8 +775,9 @@ static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O,
 
 using namespace divas;
 
-extern "C" size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv) {
-    return ws_layout(max_gated, nv > 0 ? nv : 1).total;
+extern "C" size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv, int32_t hm,
+                                            int32_t wm) {
+    return ws_layout(max_gated, nv > 0 ? nv : 1, hm > 0 ? hm : 1, wm > 0 ? wm : 1).total;
 }
 
 extern "C" const int64_t *divas_fuse_gated_count(const void *workspace) {
@@ -790,7 +832,7 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         return DIVAS_EINVAL;
     }
     const int64_t cap = a->max_gated > 0 ? a->max_gated : (a->vox_hi - a->vox_lo);
-    const WsLayout L = ws_layout(cap, a->nv);
+    const WsLayout L = ws_layout(cap, a->nv, a->hm, a->wm);
     if (workspace_bytes < L.total) {
         set_error("divas_fuse: workspace too small (%zu < %zu)", workspace_bytes, L.total);
         return DIVAS_EWORKSPACE;
@@ -799,7 +841,8 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     FuseConst C;
     fill_const(C, a, cap);
     FuseOut O{a->probs, a->n_thick, a->n_thin, a->sw, a->smw, a->st, a->occ};
-    FuseMaps M{a->masks, a->dmins, a->dmaxs, a->dexps, a->nsamps};
+    FuseMaps M{a->masks, a->dmins, a->dmaxs, a->dexps, a->nsamps,
+               (const double2 *)a->bands};
     char *ws = (char *)workspace;
     WsHeader *hdr = (WsHeader *)ws;
     uint32_t *work = (uint32_t *)(ws + L.work);
@@ -809,6 +852,24 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         cudaMemsetAsync(ws + L.bits_thick, 0, L.w - L.bits_thick, s) != cudaSuccess)
         return check_launch("divas_fuse(memset)");
     if (a->vox_hi == a->vox_lo) return DIVAS_OK;
+    if (!M.bands && C.enable_thin && C.band_ok) {   // depth bands of the views (bands.cuh)
+        double2 *bands = (double2 *)(ws + L.bands);
+        const BandParams B = band_params(a->pv, a->dx_vox, a->hm, a->wm);
+        const bool vec = (a->wm % 4 == 0) &&
+                         ((((uintptr_t)a->masks) | ((uintptr_t)a->nsamps) | ((uintptr_t)a->dexps)) & 15) == 0;
+        if (vec) {
+            dim3 bg((unsigned)((a->wm / 4 + 255) / 256), (unsigned)B.nty, (unsigned)a->nv);
+            band_pass<4, false><<<bg, 256, 0, s>>>(B, a->masks, nullptr, a->nsamps, a->dexps,
+                                                   nullptr, nullptr, bands, a->nv);
+        } else {
+            dim3 bg((unsigned)((a->wm + 255) / 256), (unsigned)B.nty, (unsigned)a->nv);
+            band_pass<1, false><<<bg, 256, 0, s>>>(B, a->masks, nullptr, a->nsamps, a->dexps,
+                                                   nullptr, nullptr, bands, a->nv);
+        }
+        if ((rc = check_launch("divas_fuse(bands)"))) return rc;
+        M.bands = bands;
+    }
+    if (!M.bands) C.band_ok = 0;
     launch_gate(C, a->density, O, work, hdr, 0, s);
     if ((rc = check_launch("divas_fuse(gate)"))) return rc;
     const int64_t cap_blocks = (cap + kPairThreads - 1) / kPairThreads;

@@ -12,7 +12,7 @@
 //   2. refine_apply: the elementwise pass, visiting views in reverse order so
 //      the z / n_samples tiles the reduction read last are still L2-resident.
 // HBM bytes per pixel: 8 (reduction) + 16 (apply) minus the L2 hits.
-#include "common.cuh"
+#include "bands.cuh"
 
 namespace divas {
 
@@ -77,18 +77,6 @@ refine_minmax(const float *__restrict__ z, const int32_t *__restrict__ n, int64_
         }
     }
     block_minmax_publish(kmin, kmax, ws + 2 * v);
-}
-
-__device__ __forceinline__ float refine_px(float m, float z, int32_t n, bool any, double lo,
-                                           double span) {
-    double o = 0.0;
-    if (any && n > 0) {
-        const double zh = span > 0.0 ? ((double)z - lo) / span : 0.0;
-        o = (double)m * (1.0 - zh);
-    }
-    if (o < 0.0) o = 0.0;   // np.clip keeps NaN, so do these compares
-    if (o > 1.0) o = 1.0;
-    return __double2float_rn(o);
 }
 
 template <int VEC>
@@ -166,4 +154,49 @@ extern "C" int divas_refine(int32_t nv, int64_t hm, int64_t wm, const float *mas
         refine_apply<1><<<grid, kRefineThreads, 0, s>>>(mask, z_surface, n_samples, out, plane, ws);
     }
     return check_launch("divas_refine");
+}
+
+extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const float *mask,
+                                  const float *z_surface, const int32_t *n_samples,
+                                  const float *dexp, float *out, const double *pv, double dx_vox,
+                                  void *bands, void *workspace, size_t workspace_bytes,
+                                  void *stream) {
+    if (nv <= 0 || hm <= 0 || wm <= 0) { set_error("divas_refine_bands: empty view set"); return DIVAS_EINVAL; }
+    if (nv > 65535 || hm > 0x7fffffff / 2 || wm > 0x7fffffff / 2) {
+        set_error("divas_refine_bands: plane too large");
+        return DIVAS_EINVAL;
+    }
+    if (!mask || !z_surface || !n_samples || !dexp || !out || !pv || !bands || !workspace) {
+        set_error("divas_refine_bands: null pointer");
+        return DIVAS_EINVAL;
+    }
+    if (workspace_bytes < divas_refine_workspace_size(nv)) {
+        set_error("divas_refine_bands: workspace too small");
+        return DIVAS_EWORKSPACE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t *ws = (uint32_t *)workspace;
+    const int64_t plane = hm * wm;
+    const bool vec = (wm % 4 == 0) &&
+                     ((((uintptr_t)mask) | ((uintptr_t)z_surface) | ((uintptr_t)n_samples) |
+                       ((uintptr_t)out) | ((uintptr_t)dexp)) & 15) == 0;
+    refine_init<<<(nv + 255) / 256, 256, 0, s>>>(ws, nv);
+    dim3 grid(blocks_per_view(plane, nv), nv);
+    const BandParams B = band_params(pv, dx_vox, (int)hm, (int)wm);
+    if (vec) {
+        refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
+        dim3 bg((unsigned)((wm / 4 + 255) / 256), (unsigned)B.nty, (unsigned)nv);
+        band_pass<4, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
+                                              (double2 *)bands, nv);
+    } else {
+        refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
+        dim3 bg((unsigned)((wm + 255) / 256), (unsigned)B.nty, (unsigned)nv);
+        band_pass<1, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
+                                              (double2 *)bands, nv);
+    }
+    return check_launch("divas_refine_bands");
+}
+
+extern "C" size_t divas_bands_size(int32_t nv, int64_t hm, int64_t wm) {
+    return band_bytes(nv, (int)hm, (int)wm);
 }

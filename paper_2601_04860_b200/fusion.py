@@ -319,7 +319,8 @@ class Fuser:
         return self._cap
 
     def run(self, density, views: DeviceViews, probs=None, stats=False, occ=False,
-            occ_thr=0.5, vox_range=None, workspace=None, stream=None, max_gated=None):
+            occ_thr=0.5, vox_range=None, workspace=None, stream=None, max_gated=None,
+            bands=None):
         import ctypes
         import torch
         g = self.g
@@ -344,7 +345,7 @@ class Fuser:
         elif occ is not False and occ is not None:
             out["occ"] = occ
         lib = _native.lib()
-        wsb = lib.divas_fuse_workspace_size(cap, views.nv)
+        wsb = lib.divas_fuse_workspace_size(cap, views.nv, views.hm, views.wm)
         if workspace is None or workspace.numel() < wsb:
             workspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
         out["workspace"] = workspace
@@ -361,6 +362,7 @@ class Fuser:
         a.occ = _native.ptr(out.get("occ"))
         a.occ_thr = float(occ_thr)
         a.max_gated = cap
+        a.bands = _native.ptr(bands)
         _native.check(lib.divas_fuse(ctypes.byref(a), _native.ptr(workspace), wsb,
                                      _native.stream_handle(stream)), "divas_fuse")
         return out

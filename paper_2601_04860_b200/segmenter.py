@@ -15,7 +15,8 @@ import numpy as np
 from . import _native
 from ._device import as_device, device, empty
 
-__all__ = ["ConfidenceMask", "refine_mask", "refine_masks", "refine_masks_device"]
+__all__ = ["ConfidenceMask", "refine_mask", "refine_masks", "refine_masks_device",
+           "refine_bands_device"]
 
 
 @dataclass
@@ -64,6 +65,43 @@ def refine_masks_device(masks, z_surface, n_samples, out=None, stream=None):
                                    _native.ptr(n_samples), _native.ptr(out), _native.ptr(ws),
                                    wsb, _native.stream_handle(stream)), "divas_refine")
     return out
+
+
+def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, out=None,
+                        bands=None, stream=None):
+    """``refine_masks_device`` fused with the fusion's per-view depth bands.
+
+    One pass over the planes writes the refined masks and, per 8x8 tile, the
+    depth interval in which a thin candidate can find support (used by
+    ``Fuser.run(bands=...)`` to skip footprint scans that provably find none).
+    Returns (out, bands).
+    """
+    import ctypes
+    import torch
+    nv, hm, wm = masks.shape
+    for t in (z_surface, n_samples, d_exp):
+        if t.shape != masks.shape:
+            raise ValueError("mask and view dimensions differ")
+    for t, dt in ((masks, torch.float32), (z_surface, torch.float32), (n_samples, torch.int32),
+                  (d_exp, torch.float32)):
+        if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("refine_bands_device expects contiguous CUDA float32/int32 planes")
+    pv = np.asarray(params.as_vector() if hasattr(params, "as_vector") else params, np.float64)
+    if out is None:
+        out = torch.empty_like(masks)
+    lib = _native.lib()
+    if bands is None:
+        bands = torch.empty(lib.divas_bands_size(nv, hm, wm), dtype=torch.uint8,
+                            device=masks.device)
+    wsb = lib.divas_refine_workspace_size(nv)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=masks.device)
+    pvc = (ctypes.c_double * 14)(*pv.tolist())
+    _native.check(lib.divas_refine_bands(nv, hm, wm, _native.ptr(masks), _native.ptr(z_surface),
+                                         _native.ptr(n_samples), _native.ptr(d_exp),
+                                         _native.ptr(out), pvc, float(voxel_size),
+                                         _native.ptr(bands), _native.ptr(ws), wsb,
+                                         _native.stream_handle(stream)), "divas_refine_bands")
+    return out, bands
 
 
 def refine_mask(mask: ConfidenceMask, view) -> ConfidenceMask:

@@ -287,3 +287,25 @@ def test_overlay_matches_reference(dev):
     for v in range(2):
         got = project_grid_overlay(mog, mviews[v][0], threshold=0.2, bounds=mb)
         assert np.array_equal(got.ravel(), d["mixed_overlay"][v].astype(bool)), v
+
+
+def test_refine_bands_matches_refine_and_fuse(dev):
+    """The fused refine+bands pass refines identically, and fusing with its
+    bands gives exactly the result of fusing with internally built bands."""
+    import torch
+    from paper_2601_04860_b200 import refine_bands_device, refine_masks_device
+    from paper_2601_04860_b200.fusion import Fuser
+    raw, z, refined = golden_io.scene_raw()
+    case = golden_io.scene_cases()["sop"]
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    out, bands = refine_bands_device(t(raw), t(z), t(case.nsamps), t(case.dexps), case.pv, case.dx)
+    assert np.array_equal(out.cpu().numpy(), refined)
+    dv = device_views(case, dev)
+    fuser = Fuser(grid_ns(case), case.pv, bounds_ns(case))
+    dens = torch.from_numpy(case.density.reshape(-1)).to(dev)
+    a = fuser.run(dens, dv, stats=True)
+    b = fuser.run(dens, dv, stats=True, bands=bands)
+    torch.cuda.synchronize()
+    for k in ("probs", "n_thick", "n_thin", "sw", "smw", "st"):
+        assert torch.equal(a[k], b[k]), k
+    assert np.array_equal(a["probs"].cpu().numpy(), _gpu_fuse(case, dev)[0]["probs"])
