@@ -240,6 +240,31 @@ __device__ __forceinline__ double grad_at(const float *__restrict__ dexp,
     return g;
 }
 
+// grad_at with one division: fl(a / rng) is monotone in a for rng > 0, so the
+// max over neighbours commutes with the division (NaN differences never win
+// in either form).  Falls back to the 4-division form otherwise.
+__device__ __forceinline__ double grad_at_fast(const float *__restrict__ dexp,
+                                               const float *__restrict__ dmin,
+                                               const float *__restrict__ dmax, int hm, int wm,
+                                               int ix, int iy, double eps, double kappa) {
+    const int64_t c = (int64_t)iy * wm + ix;
+    const float center = __ldg(dexp + c);
+    const float r32 = __ldg(dmax + c) - __ldg(dmin + c);            // f32 site
+    const double rng = (double)r32 + eps;
+    if (!(rng > 0.0)) return grad_at(dexp, dmin, dmax, hm, wm, ix, iy, eps, kappa);
+    float amax = 0.0f;
+    if (ix > 0) amax = fmaxf(amax, fabsf(__ldg(dexp + c - 1) - center));    // f32 sites
+    if (ix < wm - 1) amax = fmaxf(amax, fabsf(__ldg(dexp + c + 1) - center));
+    if (iy > 0) amax = fmaxf(amax, fabsf(__ldg(dexp + c - wm) - center));
+    if (iy < hm - 1) amax = fmaxf(amax, fabsf(__ldg(dexp + c + wm) - center));
+    const double gmax = amax > 0.0f ? (double)amax / rng : 0.0;
+    double g = 1.0 / (1.0 + kappa * gmax);
+    const double hi = 1.0 - eps;
+    if (g > hi) g = hi;
+    if (g < 0.0) g = 0.0;
+    return g;
+}
+
 // _thick_pair's spatial half and weight (fusion.py:268-303).  The depth test
 // |x_d - dexp| <= tau_dp is evaluated by the caller first: both are pure, so
 // the conjunction's value is unchanged.
@@ -445,21 +470,111 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     return !(x_d >= lo && x_d <= hi);
 }
 
-struct ThinItem {
-    const float *mask;        // top-left pixel of the clipped footprint box
-    const float *dexp;
-    const int32_t *nsamp;
-    double x_d;
-    int bw, bh;
+// Certified thick spatial test (fusion.py:268-296).  u, v are the projection
+// of the voxel centre X, so the reference's ray through (u, v) passes through X
+// up to rounding: dd ~ rel / |rel|, t_proj ~ |rel|, and the closest point of
+// the clamped segment is pos + dd * clamp(t_proj).  The approximations below
+// are within E of the exact chain's values; decisions farther than E from a
+// boundary are certain.  Returns 1 = ok, 0 = not ok, 2 = undecided (run the
+// exact chain).  On ok, `tc` is the clamped parameter when the clamp is
+// certain (then equal to dmin or dmax exactly) and `need_exact_t` tells
+// whether the weight needs the exact t_proj.
+__device__ __forceinline__ int thick_certified(const FuseConst &C, const Cam &k, double xc0,
+                                               double xc1, double xc2, double relx, double rely,
+                                               double relz, float dmin, float dmax, double g,
+                                               double &tc, bool &need_exact_t) {
+    const double L2 = relx * relx + rely * rely + relz * relz;
+    const double L = sqrt(L2);
+    const double scale = fabs(xc0) + fabs(xc1) + fabs(xc2) + fabs(k.p0) + fabs(k.p1) +
+                         fabs(k.p2) + L + fabs((double)dmin) + fabs((double)dmax) + 1.0;
+    double E = 1e-10 * scale;
+    if (C.unbounded)
+        E *= 16.0 * fmax(fmax(C.bh0, C.bh1), C.bh2) /
+             fmin(fmin(C.bh0, C.bh1), C.bh2);
+    const double lo = (double)dmin, hi = (double)dmax;
+    int clamp;                       // -1: t = dmin, +1: t = dmax, 0: t = t_proj
+    if (L < lo - E) clamp = -1;
+    else if (L > hi + E && L > lo + E) clamp = 1;
+    else if (L > lo + E && L < hi - E) clamp = 0;
+    else return 2;
+    const double t_c = clamp < 0 ? lo : (clamp > 0 ? hi : L);
+    double pcx, pcy, pcz;
+    if (clamp == 0) {
+        pcx = xc0; pcy = xc1; pcz = xc2;          // the ray point at t_proj is X
+    } else {
+        const double s = t_c / L;
+        pcx = k.p0 + relx * s;
+        pcy = k.p1 + rely * s;
+        pcz = k.p2 + relz * s;
+    }
+    if (C.unbounded != 0) {
+        const double nx = (pcx - C.bc0) / C.bh0;
+        const double ny = (pcy - C.bc1) / C.bh1;
+        const double nz = (pcz - C.bc2) / C.bh2;
+        const double r = sqrt(nx * nx + ny * ny + nz * nz);
+        if (fabs(r - 1.0) < 1e-9) return 2;       // contraction branch undecided
+        if (r > 1.0) {
+            const double sc = (2.0 - 1.0 / r) / r;
+            pcx = C.bc0 + nx * sc * C.bh0;
+            pcy = C.bc1 + ny * sc * C.bh1;
+            pcz = C.bc2 + nz * sc * C.bh2;
+        }
+    }
+    const double ex = xc0 - pcx, ey = xc1 - pcy, ez = xc2 - pcz;
+    const double delta = sqrt(ex * ex + ey * ey + ez * ez);
+    const float span = dmax - dmin;                                   // f32 site
+    const double tau_sp = C.dx * g + C.lam * (double)span;
+    if (delta > tau_sp + E) return 0;
+    if (delta < tau_sp - E) {
+        tc = t_c;
+        need_exact_t = clamp == 0;
+        return 1;
+    }
+    return 2;
+}
+
+// Depth weight from the clamped parameter (fusion.py:297-302).
+__device__ __forceinline__ double depth_weight(const FuseConst &C, double t_c, float dmin,
+                                               float dmax) {
+    const float span = dmax - dmin;                                   // f32 site
+    const float msum = dmin + dmax;                                   // f32 site
+    const double mu = 0.5 * (double)msum;
+    double hd = 0.5 * (double)span;
+    if (hd < C.eps) hd = C.eps;
+    const double r = fabs(t_c - mu) / hd;
+    return exp(-C.alpha1 * r * r);
+}
+
+// The exact t_proj of the reference's chain (fusion.py:268-277).
+__device__ __forceinline__ double exact_tproj(const Cam &k, double xc0, double xc1, double xc2,
+                                              double u, double v) {
+    const double *R = k.r;
+    const double rx = (u * k.w - k.cx) / k.fx;
+    const double ry = (k.cy - v * k.h) / k.fy;
+    double ddx = R[0] * rx + R[1] * ry - R[2];
+    double ddy = R[3] * rx + R[4] * ry - R[5];
+    double ddz = R[6] * rx + R[7] * ry - R[8];
+    const double norm = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
+    ddx /= norm;
+    ddy /= norm;
+    ddz /= norm;
+    return ((xc0 - k.p0) * ddx + (xc1 - k.p1) * ddy + (xc2 - k.p2) * ddz);
+}
+
+struct QItem {                  // a thin candidate that survived the band test
+    uint32_t slot, vi;
+    double x_d, xcam, ycam;
 };
 
+constexpr int kQueue = kPairThreads;
+
 // Per-lane part of one (view, voxel) pair: centre projection, routing, the
-// thick path (exact), and the thin candidate's footprint box.  Returns true
-// when the pair needs a footprint scan (filled into `it`).
+// thick path, the thin gates and the band test.  Returns true when the pair
+// needs corner projections + a footprint scan.
 __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, const float *dens,
                                            const FuseMaps &M, const Contrib &K, uint32_t vi,
                                            int view, int64_t kidx, int64_t bidx, uint32_t bit,
-                                           ThinItem &it) {
+                                           double &x_d_out, double &xcam_out, double &ycam_out) {
     const uint32_t g = (uint32_t)C.g, gg = g * g;
     const uint32_t ix = vi / gg;
     const uint32_t rem = vi - ix * gg;
@@ -488,12 +603,9 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     const int cu = cert_axis(A + k.cx, kCertRel * (fabs(A) + fabs(k.cx) + 1.0), k.w, px);
     const int cv = cert_axis(k.cy - B, kCertRel * (fabs(B) + fabs(k.cy) + 1.0), k.h, py);
     if (cu == 0 || cv == 0) return false;
-    bool have_uv = false;
-    double u = 0.0, v = 0.0;
     if (cu == 2 || cv == 2) {
-        u = (k.fx * (xcam / x_d) + k.cx) / k.w;
-        v = (k.cy - k.fy * (ycam / x_d)) / k.h;
-        have_uv = true;
+        const double u = (k.fx * (xcam / x_d) + k.cx) / k.w;
+        const double v = (k.cy - k.fy * (ycam / x_d)) / k.h;
         if (u < 0.0 || u >= 1.0 || v < 0.0 || v >= 1.0) return false;
         px = pixel_index(u, (long long)k.w);
         py = pixel_index(v, (long long)k.h);
@@ -503,6 +615,10 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     const int32_t ns = __ldg(M.nsamps + pix);
     if (ns <= 0) return false;                                 // valids[view, py, px] == 0
     const float m = __ldg(M.masks + pix);
+#if defined(DIVAS_ABL) && DIVAS_ABL >= 3
+    K.t[kidx] = (double)m;
+    return false;
+#endif
 
     if ((double)m >= C.mask_thr && rho >= C.rho_thr) {
         const float dexp = __ldg(M.dexps + pix);
@@ -510,15 +626,29 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
         if (b > C.bmax) b = C.bmax;
         const double tau_dp = (C.gamma + b) * C.dx;
         if (fabs(x_d - (double)dexp) <= tau_dp) {
-            if (!have_uv) {   // the spatial test needs the exact u, v bits
-                u = (k.fx * (xcam / x_d) + k.cx) / k.w;
-                v = (k.cy - k.fy * (ycam / x_d)) / k.h;
+            const float dmin = __ldg(M.dmins + pix), dmax = __ldg(M.dmaxs + pix);
+            const double gr = grad_at_fast(M.dexps + vplane, M.dmins + vplane, M.dmaxs + vplane,
+                                           C.hm, C.wm, (int)px, (int)py, C.eps, C.kappa);
+            double t_c = 0.0;
+            bool need_t = false;
+            int ok = thick_certified(C, k, xc0, xc1, xc2, relx, rely, relz, dmin, dmax, gr, t_c,
+                                     need_t);
+            double wd = 0.0;
+            if (ok == 1) {
+                if (need_t) {
+                    const double u = (k.fx * (xcam / x_d) + k.cx) / k.w;
+                    const double v = (k.cy - k.fy * (ycam / x_d)) / k.h;
+                    t_c = exact_tproj(k, xc0, xc1, xc2, u, v);
+                    if (t_c < (double)dmin) t_c = (double)dmin;
+                    else if (t_c > (double)dmax) t_c = (double)dmax;
+                }
+                wd = depth_weight(C, t_c, dmin, dmax);
+            } else if (ok == 2) {                  // exact reference chain
+                const double u = (k.fx * (xcam / x_d) + k.cx) / k.w;
+                const double v = (k.cy - k.fy * (ycam / x_d)) / k.h;
+                ok = thick_spatial(C, k, xc0, xc1, xc2, u, v, dmin, dmax, gr, wd) ? 1 : 0;
             }
-            const double gr = grad_at(M.dexps + vplane, M.dmins + vplane, M.dmaxs + vplane, C.hm,
-                                      C.wm, (int)px, (int)py, C.eps, C.kappa);
-            double wd;
-            if (thick_spatial(C, k, xc0, xc1, xc2, u, v, __ldg(M.dmins + pix),
-                              __ldg(M.dmaxs + pix), gr, wd)) {
+            if (ok == 1) {
                 K.w[kidx] = wd;
                 K.mw[kidx] = (double)m * wd;
                 atomicOr(K.bits_thick + bidx, bit);
@@ -526,6 +656,9 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
             }
         }
     }
+#if defined(DIVAS_ABL) && DIVAS_ABL >= 2
+    return false;
+#endif
     if (!C.enable_thin) return false;
     if (!((double)m > C.thin_floor && rho >= C.rho_thin)) return false;
     {   // dx_vox * fmax / x_d >= 1.0, certified (division monotone and correctly rounded)
@@ -536,63 +669,49 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     }
     if (C.band_ok && band_reject(C, M, k, view, x_d, xcam, ycam, A + k.cx, k.cy - B))
         return false;                                          // support is exactly 0
+    x_d_out = x_d;
+    xcam_out = xcam;
+    ycam_out = ycam;
+    return true;
+}
+
+// Corner projections + footprint scan of one queued thin candidate.
+__device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, const FuseMaps &M,
+                                          const Contrib &K, const double *s_tau, int view,
+                                          const QItem &q) {
+    const uint32_t g = (uint32_t)C.g, gg = g * g;
+    const uint32_t ix = q.vi / gg;
+    const uint32_t rem = q.vi - ix * gg;
+    const uint32_t iy = rem / g;
+    const uint32_t iz = rem - iy * g;
+    const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
+    const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
+    const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
     long long xs, xe, ys, ye;
-    if (!thin_bounds(C, k, xc0, xc1, xc2, x_d, xcam, ycam, xs, xe, ys, ye)) return false;
+    if (!thin_bounds(C, k, xc0, xc1, xc2, q.x_d, q.xcam, q.ycam, xs, xe, ys, ye)) return;
     const long long wi = (long long)k.w, hi = (long long)k.h;
-    if (xe < 0 || xs > wi - 1 || ye < 0 || ys > hi - 1) return false;
+    if (xe < 0 || xs > wi - 1 || ye < 0 || ys > hi - 1) return;
     if (xs < 0) xs = 0;
     if (ys < 0) ys = 0;
     if (xe > wi - 1) xe = wi - 1;
     if (ye > hi - 1) ye = hi - 1;
-    const int64_t off = vplane + ys * (int64_t)C.wm + xs;
-    it.mask = M.masks + off;
-    it.dexp = M.dexps + off;
-    it.nsamp = M.nsamps + off;
-    it.x_d = x_d;
-    it.bw = (int)(xe - xs) + 1;
-    it.bh = (int)(ye - ys) + 1;
-    return true;
-}
-
-#ifndef DIVAS_PAIR_MINB
-#define DIVAS_PAIR_MINB 3
+#if defined(DIVAS_ABL) && DIVAS_ABL >= 1
+    K.t[(int64_t)view * C.cap + q.slot] = q.x_d + (double)(xe - xs);
+    return;
 #endif
-__global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
-fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
-           FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
-           const WsHeader *__restrict__ hdr) {
-    __shared__ double s_tau[kTauTable];
-    for (int i = threadIdx.x; i < kTauTable; i += blockDim.x) s_tau[i] = tau_thin(C, i);
-    __syncthreads();
-    const long long n = min((long long)hdr->count, (long long)C.cap);
-    const long long block0 = (long long)blockIdx.x * blockDim.x;
-    if (block0 >= n) return;                                   // whole CTA idle
-    const long long slot = block0 + threadIdx.x;
-    const int view = blockIdx.y;
-    const int lane = threadIdx.x & 31;
-    Cam k;
-    load_cam(cams + (int64_t)view * kCamStride, k);
-    const int64_t kidx = (int64_t)view * C.cap + slot;
-    const int64_t bidx = (int64_t)(view >> 5) * C.cap + slot;
-    const uint32_t bit = 1u << (view & 31);
-    ThinItem it;
-    bool has = false;
-    if (slot < n) has = pair_route(C, k, dens, M, K, __ldg(work + slot), view, kidx, bidx, bit, it);
-
-    if (!has) return;
-    // Footprint scan (fusion.py:352-370), one thread per thin item, branch-free
-    // body with three independent loads per pixel.  Exactness: f32 -> f64
-    // widening is exact and monotone, so m_max is kept in f32 via fmaxf (NaN
-    // never wins, as `mv > m_max` is false in the reference) and `mv > 0.5` is
-    // the same compare in f32; tau_d(n) is read from a table built with the
+    // Footprint scan (fusion.py:352-370).  Exactness: f32 -> f64 widening is
+    // exact and monotone, so m_max is kept in f32 via fmaxf (NaN never wins,
+    // as `mv > m_max` is false in the reference) and `mv > 0.5` is the same
+    // compare in f32; tau_d(n) is read from a table built with the
     // reference's ops, valid for every n once beta * n saturates at bmax
     // (C.tau_saturated, checked on the host), else computed inline.
-    const float *__restrict__ mk = it.mask;
-    const float *__restrict__ de = it.dexp;
-    const int32_t *__restrict__ nsp = it.nsamp;
-    const double xd = it.x_d;
-    const int bw = it.bw;
-    const int npix = bw * it.bh;
+    const int64_t off0 = (int64_t)view * C.hm * C.wm + ys * (int64_t)C.wm + xs;
+    const float *__restrict__ mk = M.masks + off0;
+    const float *__restrict__ de = M.dexps + off0;
+    const int32_t *__restrict__ nsp = M.nsamps + off0;
+    const double xd = q.x_d;
+    const int bw = (int)(xe - xs) + 1;
+    const int npix = bw * ((int)(ye - ys) + 1);
     int sup = 0;
     float mmax = 0.0f;
     int col = 0, off = 0;
@@ -621,9 +740,51 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     const double p_cov = sup == 0 ? 0.0 : (double)sup / (double)npix;
     const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
     if (npix > 0 && t >= C.thin_accept) {
-        K.t[kidx] = t;
-        atomicOr(K.bits_thin + bidx, bit);
+        K.t[(int64_t)view * C.cap + q.slot] = t;
+        atomicOr(K.bits_thin + (int64_t)(view >> 5) * C.cap + q.slot, 1u << (view & 31));
     }
+}
+
+#ifndef DIVAS_PAIR_MINB
+#define DIVAS_PAIR_MINB 4
+#endif
+__global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
+fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
+           FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
+           const WsHeader *__restrict__ hdr) {
+    __shared__ double s_tau[kTauTable];
+    __shared__ QItem s_q[kQueue];
+    __shared__ int s_nq;
+    for (int i = threadIdx.x; i < kTauTable; i += blockDim.x) s_tau[i] = tau_thin(C, i);
+    if (threadIdx.x == 0) s_nq = 0;
+    __syncthreads();
+    const long long n = min((long long)hdr->count, (long long)C.cap);
+    const long long block0 = (long long)blockIdx.x * blockDim.x;
+    if (block0 >= n) return;                                   // whole CTA idle
+    const long long slot = block0 + threadIdx.x;
+    const int view = blockIdx.y;
+    Cam k;
+    load_cam(cams + (int64_t)view * kCamStride, k);
+    // phase A: route every pair; queue the thin candidates that need a scan
+    bool has = false;
+    QItem q;
+    if (slot < n) {
+        q.slot = (uint32_t)slot;
+        q.vi = __ldg(work + slot);
+        has = pair_route(C, k, dens, M, K, q.vi, view, (int64_t)view * C.cap + slot,
+                         (int64_t)(view >> 5) * C.cap + slot, 1u << (view & 31), q.x_d, q.xcam,
+                         q.ycam);
+    }
+    const unsigned ball = __ballot_sync(0xffffffffu, has);
+    int base = 0;
+    const int lane = threadIdx.x & 31;
+    if (lane == 0 && ball) base = atomicAdd(&s_nq, __popc(ball));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (has) s_q[base + __popc(ball & ((1u << lane) - 1u))] = q;
+    __syncthreads();
+    // phase B: the queued candidates, densely packed onto the first warps
+    const int nq = s_nq;
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) thin_item(C, k, M, K, s_tau, view, s_q[i]);
 }
 
 // ---------------------------------------------------------------------------
