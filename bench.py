@@ -267,7 +267,7 @@ def run_ours(args):
     import workloads
     from paper_2601_04860_b200 import sharding
     from paper_2601_04860_b200.fusion import DeviceViews, FusionParams, Fuser
-    from paper_2601_04860_b200.segmenter import refine_masks_device
+    from paper_2601_04860_b200.segmenter import refine_bands_device
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -329,16 +329,20 @@ def run_ours(args):
     probs = torch.empty(g ** 3, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     ws = None
+    bands = None
+    cap = fuser.capacity(wl.density, lo, hi)      # one counting pass + sync, outside the loop
     stream = torch.cuda.current_stream()
 
     def step(ev=None):
-        nonlocal ws
+        nonlocal ws, bands
         if ev is not None:
             ev[0].record(stream)
-        refine_masks_device(dv.raw_masks, dv.z_surface, dv.nsamps, out=dv.masks)
+        _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps, params,
+                                        wl.dx, out=dv.masks, bands=bands)
         if ev is not None:
             ev[1].record(stream)
-        out = fuser.run(wl.density, dv, probs=probs, occ=True, vox_range=(lo, hi), workspace=ws)
+        out = fuser.run(wl.density, dv, probs=probs, occ=True, vox_range=(lo, hi), workspace=ws,
+                        bands=bands, max_gated=cap)
         ws = out["workspace"]
         if ev is not None:
             ev[2].record(stream)
@@ -387,8 +391,9 @@ def run_ours(args):
     b_refine = 16 * nv * H * W
     b_fuse = 12 * (hi - lo) + 20 * nv * H * W
     refine_ms, fuse_ms = float(np.mean(t_ref)), float(np.mean(t_fuse))
-    ops = {"refine": (refine_ms, b_refine, "divas_refine: refine_minmax + refine_apply"),
-           "fuse": (fuse_ms, b_fuse, "divas_fuse: fuse_gate + fuse_sparse")}
+    ops = {"refine": (refine_ms, b_refine + 4 * nv * H * W,
+                      "divas_refine_bands: refine_minmax + band_pass<4,true> (refine + depth bands)"),
+           "fuse": (fuse_ms, b_fuse, "divas_fuse: fuse_gate + fuse_pairs + fuse_reduce")}
     dom = max(ops, key=lambda k: ops[k][0])
     d_ms, d_bytes, d_desc = ops[dom]
     achieved = d_bytes / (d_ms / 1e3) / 1e9
@@ -428,7 +433,7 @@ def run_ours(args):
     if rank == 0:
         e2e = run_e2e(args, wl, params, dev)
 
-    launches_per_step = 3 + 2          # refine: init, minmax, apply; fuse: gate, sparse
+    launches_per_step = 3 + 3          # refine: init, minmax, band_pass; fuse: gate, pairs, reduce
     line = {
         "metric": "voxel-view updates/s", "value": value, "unit": "updates/s",
         "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms,
@@ -437,7 +442,7 @@ def run_ours(args):
         "config": {"workload": CONFIG_DESC[args.config], "grid": g, "views": nv,
                    "width": W, "height": H, "parallelism": f"slab x{world}" if world > 1 else "1 GPU",
                    "slabs": slabs, "slab_policy": args.slabs,
-                   "step": "refine(all views) + fuse(slab, threshold fused)"
+                   "step": "refine+bands(all views) + fuse(slab, threshold fused)"
                            + (" + all-gather(occupancy)" if world > 1 else ""),
                    "l2": "flushed (256 MiB write) between steps, outside the events",
                    "params": "FusionParams() defaults"},
