@@ -25,7 +25,8 @@ def launches(path, pat="divas"):
         if re.search(pat, r[ki]):
             name = re.sub(r"\(.*", "", r[ki]).replace("void ", "")
             v = float(r[vi].replace(",", ""))
-            scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+            scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
+                     "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
             agg[name].append(v * scale)
     tot = sum(sum(v) for v in agg.values())
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):

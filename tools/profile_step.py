@@ -14,7 +14,7 @@ def main():
     import torch
     import workloads
     from paper_2601_04860_b200.fusion import DeviceViews, FusionParams, Fuser, pack_cameras
-    from paper_2601_04860_b200.segmenter import refine_masks_device
+    from paper_2601_04860_b200.segmenter import refine_bands_device
     dev = torch.device("cuda", 0)
     wl = workloads.make(args.config, device=dev)
     dv = DeviceViews(torch.from_numpy(pack_cameras(wl.cams)).to(dev), torch.empty_like(wl.raw_masks),
@@ -24,9 +24,12 @@ def main():
     fuser = Fuser(grid, FusionParams())
     probs = torch.empty(wl.g ** 3, dtype=torch.float64, device=dev)
     ws = None
-    for _ in range(args.steps):
-        refine_masks_device(dv.raw_masks, dv.z_surface, dv.nsamps, out=dv.masks)
-        out = fuser.run(wl.density, dv, probs=probs, occ=True, workspace=ws)
+    bands = None
+    params = FusionParams()
+    for _ in range(args.steps):      # the bench step: refine+bands, fuse with those bands
+        _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps, params,
+                                        wl.dx, out=dv.masks, bands=bands)
+        out = fuser.run(wl.density, dv, probs=probs, occ=True, workspace=ws, bands=bands)
         ws = out["workspace"]
     torch.cuda.synchronize()
     print("gated", int(Fuser.gated_count(out).item()))
