@@ -21,8 +21,13 @@ struct BandParams {
     int hm, wm, ntx, nty;
 };
 
-__device__ __forceinline__ void band_px(float m, int32_t n, float d, const BandParams &B,
-                                        double &lo, double &hi) {
+// Per-pixel scan record: {refined mask, d_exp, tau_d(n) as f32 (or -1e30 when
+// the pixel cannot support: mask <= 0.5 or n == 0), n_samples bits}.  One
+// 128-bit load gives the footprint scan everything it reads per pixel.
+constexpr float kIneligible = -1e30f;
+
+__device__ __forceinline__ float band_px(float m, int32_t n, float d, const BandParams &B,
+                                         double &lo, double &hi) {
     if (m > 0.5f && n > 0) {
         double b = B.beta * (double)n;
         if (b > B.bmax) b = B.bmax;
@@ -31,7 +36,9 @@ __device__ __forceinline__ void band_px(float m, int32_t n, float d, const BandP
         const double mg = 1e-12 * (fabs(D) + t);
         lo = fmin(lo, D - t - mg);
         hi = fmax(hi, D + t + mg);
+        return (float)t;
     }
+    return kIneligible;
 }
 
 // One thread per VEC-pixel column chunk and 8 rows; TPW = 8 / VEC threads form
@@ -42,7 +49,7 @@ __global__ void __launch_bounds__(256)
 band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict__ z,
           const int32_t *__restrict__ nsamp, const float *__restrict__ dexp,
           float *__restrict__ refined, const uint32_t *__restrict__ minmax,
-          double2 *__restrict__ bands, int nv) {
+          double2 *__restrict__ bands, float4 *__restrict__ records, int nv) {
     constexpr int TPW = kBandTile / VEC;
     const int v = nv - 1 - (int)blockIdx.z;          // reverse view order: L2 reuse of z / n
     const int64_t plane = (int64_t)B.hm * B.wm;
@@ -79,7 +86,8 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
                     const float4 zz = __ldg(reinterpret_cast<const float4 *>(z + p));
                     const float zv[4] = {zz.x, zz.y, zz.z, zz.w};
                     for (int k = 0; k < 4; ++k) m[k] = refine_px(m[k], zv[k], n[k], any, lo_ref, span);
-                    __stcs(reinterpret_cast<float4 *>(refined + p), make_float4(m[0], m[1], m[2], m[3]));
+                    if (refined)
+                        __stcs(reinterpret_cast<float4 *>(refined + p), make_float4(m[0], m[1], m[2], m[3]));
                 }
             } else {
                 m[0] = __ldg(mask + p);
@@ -87,11 +95,14 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
                 d[0] = __ldg(dexp + p);
                 if (REFINE) {
                     m[0] = refine_px(m[0], __ldg(z + p), n[0], any, lo_ref, span);
-                    refined[p] = m[0];
+                    if (refined) refined[p] = m[0];
                 }
             }
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) band_px(m[k], n[k], d[k], B, lo, hi);
+            for (int k = 0; k < VEC; ++k) {
+                const float t32 = band_px(m[k], n[k], d[k], B, lo, hi);
+                records[p + k] = make_float4(m[k], d[k], t32, __int_as_float(n[k]));
+            }
         }
     }
 #pragma unroll
@@ -117,6 +128,14 @@ inline BandParams band_params(const double *pv, double dx, int hm, int wm) {
 inline size_t band_bytes(int nv, int hm, int wm) {
     return (size_t)nv * ((hm + kBandTile - 1) / kBandTile) * ((wm + kBandTile - 1) / kBandTile) *
            sizeof(double2);
+}
+
+// "view aux" buffer: scan records [nv][hm][wm] float4, then the tile bands.
+inline size_t aux_records_bytes(int nv, int hm, int wm) {
+    return ((size_t)nv * hm * wm * sizeof(float4) + 255) & ~(size_t)255;
+}
+inline size_t aux_bytes(int nv, int hm, int wm) {
+    return aux_records_bytes(nv, hm, wm) + band_bytes(nv, hm, wm);
 }
 
 }  // namespace divas

@@ -48,10 +48,10 @@ struct FuseConst {
     double gamma, beta, bmax, lam, rho_thr, rho_thin, thin_pct, alpha1, thin_accept, eps,
         mask_thr, thin_floor, kappa;
     int enable_thin;
-    int tau_saturated;   // beta * (kTauTable - 1) >= bmax: the tau table covers every n
     int band_ok;         // thin_percent_cover > 0: zero support can never vote
     int ntx, nty;        // depth-band tiles per view
     double cube_r;       // circumradius of a voxel, padded
+    double tau_max;      // (2 gamma + bmax) dx >= tau_d(n) for every n
     double bc0, bc1, bc2, bh0, bh1, bh2;
     int unbounded;
     double occ_thr;
@@ -68,6 +68,7 @@ struct FuseMaps {
     const float *masks, *dmins, *dmaxs, *dexps;
     const int32_t *nsamps;
     const double2 *bands;   // [nv][nty][ntx] depth bands (bands.cuh)
+    const float4 *rec;      // [nv][hm][wm] scan records (bands.cuh)
 };
 
 struct Contrib {                 // all [view or word][cap]
@@ -355,7 +356,6 @@ __device__ __forceinline__ int cert_axis(double Ua, double E, double n, long lon
 // pair kernel
 // ---------------------------------------------------------------------------
 constexpr int kPairThreads = 256;
-constexpr int kTauTable = 512;   // exact thin depth tolerance for n_samples < 512
 
 // (2 gamma + min(beta * n, bmax)) * dx, the reference's ops (fusion.py:362-365)
 __device__ __forceinline__ double tau_thin(const FuseConst &C, int32_t n) {
@@ -612,16 +612,17 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     }
     const int64_t vplane = (int64_t)view * C.hm * C.wm;
     const int64_t pix = vplane + py * (int64_t)C.wm + px;
-    const int32_t ns = __ldg(M.nsamps + pix);
+    const float4 rc = __ldg(M.rec + pix);                      // {m, d_exp, tau32, n}
+    const int32_t ns = __float_as_int(rc.w);
     if (ns <= 0) return false;                                 // valids[view, py, px] == 0
-    const float m = __ldg(M.masks + pix);
+    const float m = rc.x;
 #if defined(DIVAS_ABL) && DIVAS_ABL >= 3
     K.t[kidx] = (double)m;
     return false;
 #endif
 
     if ((double)m >= C.mask_thr && rho >= C.rho_thr) {
-        const float dexp = __ldg(M.dexps + pix);
+        const float dexp = rc.y;
         double b = C.beta * (double)ns;
         if (b > C.bmax) b = C.bmax;
         const double tau_dp = (C.gamma + b) * C.dx;
@@ -677,7 +678,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
 
 // Corner projections + footprint scan of one queued thin candidate.
 __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, const FuseMaps &M,
-                                          const Contrib &K, const double *s_tau, int view,
+                                          const Contrib &K, int view,
                                           const QItem &q) {
     const uint32_t g = (uint32_t)C.g, gg = g * g;
     const uint32_t ix = q.vi / gg;
@@ -699,42 +700,31 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     K.t[(int64_t)view * C.cap + q.slot] = q.x_d + (double)(xe - xs);
     return;
 #endif
-    // Footprint scan (fusion.py:352-370).  Exactness: f32 -> f64 widening is
-    // exact and monotone, so m_max is kept in f32 via fmaxf (NaN never wins,
-    // as `mv > m_max` is false in the reference) and `mv > 0.5` is the same
-    // compare in f32; tau_d(n) is read from a table built with the
-    // reference's ops, valid for every n once beta * n saturates at bmax
-    // (C.tau_saturated, checked on the host), else computed inline.
-    const int64_t off0 = (int64_t)view * C.hm * C.wm + ys * (int64_t)C.wm + xs;
-    const float *__restrict__ mk = M.masks + off0;
-    const float *__restrict__ de = M.dexps + off0;
-    const int32_t *__restrict__ nsp = M.nsamps + off0;
+    // Footprint scan over the 16-byte records {m, D, tau32, n}.  m_max: f32
+    // widening is exact and monotone, so fmaxf in f32 equals the reference's
+    // f64 `if mv > m_max` (NaN never wins).  Support: the f32 margin test
+    // e = |f32(x_d) - D| - tau32 has |error| < 2^-22 (|x_d| + tau_max); beyond
+    // M = 2^-20 (|x_d| + tau_max) from 0 it decides the reference's f64 test
+    // |x_d - f64(D)| <= tau(n) exactly, inside M the f64 test runs.  Ineligible
+    // pixels (mask <= 0.5 or n == 0) carry tau32 = -1e30: never counted.
+    const float4 *__restrict__ rp = M.rec + (int64_t)view * C.hm * C.wm + ys * (int64_t)C.wm + xs;
     const double xd = q.x_d;
+    const float xd32 = (float)xd;
+    const float Mg = (float)(9.5367431640625e-07 * (fabs(xd) + C.tau_max));   // 2^-20
     const int bw = (int)(xe - xs) + 1;
     const int npix = bw * ((int)(ye - ys) + 1);
     int sup = 0;
     float mmax = 0.0f;
     int col = 0, off = 0;
-    if (C.tau_saturated) {
 #pragma unroll 4
-        for (int i = 0; i < npix; ++i) {
-            const float mv = __ldg(mk + off + col);
-            const int32_t nn = __ldg(nsp + off + col);
-            const float dv = __ldg(de + off + col);
-            mmax = fmaxf(mmax, mv);
-            const double tau_d = s_tau[min(max(nn, 0), kTauTable - 1)];
-            sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_d) ? 1 : 0;
-            if (++col == bw) { col = 0; off += C.wm; }
-        }
-    } else {
-        for (int i = 0; i < npix; ++i) {
-            const float mv = __ldg(mk + off + col);
-            const int32_t nn = __ldg(nsp + off + col);
-            const float dv = __ldg(de + off + col);
-            mmax = fmaxf(mmax, mv);
-            sup += (mv > 0.5f && nn > 0 && fabs(xd - (double)dv) <= tau_thin(C, nn)) ? 1 : 0;
-            if (++col == bw) { col = 0; off += C.wm; }
-        }
+    for (int i = 0; i < npix; ++i) {
+        const float4 r = __ldg(rp + off + col);
+        mmax = fmaxf(mmax, r.x);
+        const float e = fabsf(xd32 - r.y) - r.z;
+        sup += (e <= -Mg) ? 1 : 0;
+        if (fabsf(e) < Mg)    // within the margin: the reference's f64 compare
+            sup += (fabs(xd - (double)r.y) <= tau_thin(C, __float_as_int(r.w))) ? 1 : 0;
+        if (++col == bw) { col = 0; off += C.wm; }
     }
     const double m_max = (double)mmax;
     const double p_cov = sup == 0 ? 0.0 : (double)sup / (double)npix;
@@ -752,10 +742,8 @@ __global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
 fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
            FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
            const WsHeader *__restrict__ hdr) {
-    __shared__ double s_tau[kTauTable];
     __shared__ QItem s_q[kQueue];
     __shared__ int s_nq;
-    for (int i = threadIdx.x; i < kTauTable; i += blockDim.x) s_tau[i] = tau_thin(C, i);
     if (threadIdx.x == 0) s_nq = 0;
     __syncthreads();
     const long long n = min((long long)hdr->count, (long long)C.cap);
@@ -784,7 +772,7 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     __syncthreads();
     // phase B: the queued candidates, densely packed onto the first warps
     const int nq = s_nq;
-    for (int i = threadIdx.x; i < nq; i += blockDim.x) thin_item(C, k, M, K, s_tau, view, s_q[i]);
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) thin_item(C, k, M, K, view, s_q[i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -885,7 +873,7 @@ static WsLayout ws_layout(int64_t cap, int32_t nv, int32_t hm, int32_t wm) {
     L.w = off;          off = align256(off + (size_t)nv * c * 8);
     L.mw = off;         off = align256(off + (size_t)nv * c * 8);
     L.t = off;          off = align256(off + (size_t)nv * c * 8);
-    L.bands = off;      off = align256(off + band_bytes(nv, hm, wm));
+    L.bands = off;      off = align256(off + aux_bytes(nv, hm, wm));
     L.total = off;
     return L;
 }
@@ -911,11 +899,11 @@ static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     C.rho_thin = pv[5]; C.thin_pct = pv[6]; C.alpha1 = pv[7]; C.thin_accept = pv[8];
     C.eps = pv[9]; C.mask_thr = pv[10]; C.thin_floor = pv[11]; C.kappa = pv[12];
     C.enable_thin = pv[13] != 0.0;
-    C.tau_saturated = (C.beta * (double)(kTauTable - 1) >= C.bmax) ? 1 : 0;
     C.band_ok = C.thin_pct > 0.0 ? 1 : 0;
     C.ntx = (a->wm + kBandTile - 1) / kBandTile;
     C.nty = (a->hm + kBandTile - 1) / kBandTile;
     C.cube_r = 0.8660254037844387 * a->dx_vox * (1.0 + 1e-9);
+    C.tau_max = (2.0 * C.gamma + C.bmax) * C.dx;
     C.bc0 = a->bc[0]; C.bc1 = a->bc[1]; C.bc2 = a->bc[2];
     C.bh0 = a->bh[0]; C.bh1 = a->bh[1]; C.bh2 = a->bh[2];
     C.unbounded = a->unbounded;
@@ -1002,8 +990,11 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     FuseConst C;
     fill_const(C, a, cap);
     FuseOut O{a->probs, a->n_thick, a->n_thin, a->sw, a->smw, a->st, a->occ};
-    FuseMaps M{a->masks, a->dmins, a->dmaxs, a->dexps, a->nsamps,
-               (const double2 *)a->bands};
+    FuseMaps M{a->masks, a->dmins, a->dmaxs, a->dexps, a->nsamps, nullptr, nullptr};
+    if (a->bands) {
+        M.rec = (const float4 *)a->bands;
+        M.bands = (const double2 *)((const char *)a->bands + aux_records_bytes(a->nv, a->hm, a->wm));
+    }
     char *ws = (char *)workspace;
     WsHeader *hdr = (WsHeader *)ws;
     uint32_t *work = (uint32_t *)(ws + L.work);
@@ -1013,24 +1004,26 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         cudaMemsetAsync(ws + L.bits_thick, 0, L.w - L.bits_thick, s) != cudaSuccess)
         return check_launch("divas_fuse(memset)");
     if (a->vox_hi == a->vox_lo) return DIVAS_OK;
-    if (!M.bands && C.enable_thin && C.band_ok) {   // depth bands of the views (bands.cuh)
-        double2 *bands = (double2 *)(ws + L.bands);
+    if (!M.rec) {   // scan records + depth bands of the views (bands.cuh)
+        char *aux = ws + L.bands;
+        float4 *rec = (float4 *)aux;
+        double2 *bands = (double2 *)(aux + aux_records_bytes(a->nv, a->hm, a->wm));
         const BandParams B = band_params(a->pv, a->dx_vox, a->hm, a->wm);
         const bool vec = (a->wm % 4 == 0) &&
                          ((((uintptr_t)a->masks) | ((uintptr_t)a->nsamps) | ((uintptr_t)a->dexps)) & 15) == 0;
         if (vec) {
             dim3 bg((unsigned)((a->wm / 4 + 255) / 256), (unsigned)B.nty, (unsigned)a->nv);
             band_pass<4, false><<<bg, 256, 0, s>>>(B, a->masks, nullptr, a->nsamps, a->dexps,
-                                                   nullptr, nullptr, bands, a->nv);
+                                                   nullptr, nullptr, bands, rec, a->nv);
         } else {
             dim3 bg((unsigned)((a->wm + 255) / 256), (unsigned)B.nty, (unsigned)a->nv);
             band_pass<1, false><<<bg, 256, 0, s>>>(B, a->masks, nullptr, a->nsamps, a->dexps,
-                                                   nullptr, nullptr, bands, a->nv);
+                                                   nullptr, nullptr, bands, rec, a->nv);
         }
-        if ((rc = check_launch("divas_fuse(bands)"))) return rc;
+        if ((rc = check_launch("divas_fuse(aux)"))) return rc;
+        M.rec = rec;
         M.bands = bands;
     }
-    if (!M.bands) C.band_ok = 0;
     launch_gate(C, a->density, O, work, hdr, 0, s);
     if ((rc = check_launch("divas_fuse(gate)"))) return rc;
     const int64_t cap_blocks = (cap + kPairThreads - 1) / kPairThreads;

@@ -166,7 +166,7 @@ extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const floa
         set_error("divas_refine_bands: plane too large");
         return DIVAS_EINVAL;
     }
-    if (!mask || !z_surface || !n_samples || !dexp || !out || !pv || !bands || !workspace) {
+    if (!mask || !z_surface || !n_samples || !dexp || !pv || !bands || !workspace) {
         set_error("divas_refine_bands: null pointer");
         return DIVAS_EINVAL;
     }
@@ -182,21 +182,24 @@ extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const floa
                        ((uintptr_t)out) | ((uintptr_t)dexp)) & 15) == 0;
     refine_init<<<(nv + 255) / 256, 256, 0, s>>>(ws, nv);
     dim3 grid(blocks_per_view(plane, nv), nv);
+    auto bands_of = [](void *aux, int nv_, int64_t hm_, int64_t wm_) {
+        return (double2 *)((char *)aux + aux_records_bytes(nv_, (int)hm_, (int)wm_));
+    };
     const BandParams B = band_params(pv, dx_vox, (int)hm, (int)wm);
     if (vec) {
         refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((wm / 4 + 255) / 256), (unsigned)B.nty, (unsigned)nv);
         band_pass<4, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
-                                              (double2 *)bands, nv);
+                                              bands_of(bands, nv, hm, wm), (float4 *)bands, nv);
     } else {
         refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((wm + 255) / 256), (unsigned)B.nty, (unsigned)nv);
         band_pass<1, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
-                                              (double2 *)bands, nv);
+                                              bands_of(bands, nv, hm, wm), (float4 *)bands, nv);
     }
     return check_launch("divas_refine_bands");
 }
 
 extern "C" size_t divas_bands_size(int32_t nv, int64_t hm, int64_t wm) {
-    return band_bytes(nv, (int)hm, (int)wm);
+    return aux_bytes(nv, (int)hm, (int)wm);
 }
