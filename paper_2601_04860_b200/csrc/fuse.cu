@@ -677,103 +677,61 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
 }
 
 // Corner projections + footprint scan of one queued thin candidate.
-// Corner projections + footprint scan of queued thin candidates, T threads
-// per candidate (T in {1, 2, 4, 8}, uniform over the CTA): lane j of a group
-// scans rows j, j + T, ...; support (an integer count) and m_max (a maximum)
-// combine with shuffles, so the result is independent of the split.  The
-// group's first lane projects the corners and broadcasts the box.
-template <int T>
-__device__ __forceinline__ void thin_items(const FuseConst &C, const Cam &k, const FuseMaps &M,
-                                           const Contrib &K, int view, const QItem *s_q,
-                                           int nq) {
-    constexpr int G = kPairThreads / T;
-    const int gi = threadIdx.x / T, j = threadIdx.x % T;
-    const int lane = threadIdx.x & 31;
-    const int leader = lane & ~(T - 1);
-    for (int base = 0; base < nq; base += G) {          // uniform trip count
-        const int item = base + gi;
-        int xs = 0, ys = 0, bw = 0, bh = 0;
-        if (item < nq && j == 0) {
-            const QItem &q = s_q[item];
-            const uint32_t g = (uint32_t)C.g, gg = g * g;
-            const uint32_t ix = q.vi / gg;
-            const uint32_t rem = q.vi - ix * gg;
-            const uint32_t iy = rem / g;
-            const uint32_t iz = rem - iy * g;
-            const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
-            const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
-            const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
-            long long lxs, lxe, lys, lye;
-            if (thin_bounds(C, k, xc0, xc1, xc2, q.x_d, q.xcam, q.ycam, lxs, lxe, lys, lye)) {
-                const long long wi = (long long)k.w, hi = (long long)k.h;
-                if (!(lxe < 0 || lxs > wi - 1 || lye < 0 || lys > hi - 1)) {
-                    if (lxs < 0) lxs = 0;
-                    if (lys < 0) lys = 0;
-                    if (lxe > wi - 1) lxe = wi - 1;
-                    if (lye > hi - 1) lye = hi - 1;
-                    xs = (int)lxs; ys = (int)lys;
-                    bw = (int)(lxe - lxs) + 1;
-                    bh = (int)(lye - lys) + 1;
-                }
-            }
-        }
-        if (T > 1) {
-            xs = __shfl_sync(0xffffffffu, xs, leader);
-            ys = __shfl_sync(0xffffffffu, ys, leader);
-            bw = __shfl_sync(0xffffffffu, bw, leader);
-            bh = __shfl_sync(0xffffffffu, bh, leader);
-        }
+__device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, const FuseMaps &M,
+                                          const Contrib &K, int view,
+                                          const QItem &q) {
+    const uint32_t g = (uint32_t)C.g, gg = g * g;
+    const uint32_t ix = q.vi / gg;
+    const uint32_t rem = q.vi - ix * gg;
+    const uint32_t iy = rem / g;
+    const uint32_t iz = rem - iy * g;
+    const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
+    const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
+    const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
+    long long xs, xe, ys, ye;
+    if (!thin_bounds(C, k, xc0, xc1, xc2, q.x_d, q.xcam, q.ycam, xs, xe, ys, ye)) return;
+    const long long wi = (long long)k.w, hi = (long long)k.h;
+    if (xe < 0 || xs > wi - 1 || ye < 0 || ys > hi - 1) return;
+    if (xs < 0) xs = 0;
+    if (ys < 0) ys = 0;
+    if (xe > wi - 1) xe = wi - 1;
+    if (ye > hi - 1) ye = hi - 1;
 #if defined(DIVAS_ABL) && DIVAS_ABL >= 1
-        if (item < nq && j == 0 && bw > 0)
-            K.t[(int64_t)view * C.cap + s_q[item].slot] = s_q[item].x_d + (double)bw;
-        continue;
+    K.t[(int64_t)view * C.cap + q.slot] = q.x_d + (double)(xe - xs);
+    return;
 #endif
-        // Footprint scan over the 16-byte records {m, D, tau32, n}.  m_max: f32
-        // widening is exact and monotone, so fmaxf in f32 equals the
-        // reference's f64 `if mv > m_max` (NaN never wins).  Support: the f32
-        // margin test e = |f32(x_d) - D| - tau32 has |error| < 2^-22 (|x_d| +
-        // tau_max); beyond M = 2^-20 (|x_d| + tau_max) from 0 it decides the
-        // reference's f64 test |x_d - f64(D)| <= tau(n) exactly, inside M the
-        // f64 test runs.  Ineligible pixels (mask <= 0.5 or n == 0) carry
-        // tau32 = -1e30: never counted.
-        int sup = 0;
-        float mmax = 0.0f;
-        double xd = 0.0;
-        if (bw > 0) {
-            xd = s_q[item].x_d;
-            const float xd32 = (float)xd;
-            const float Mg = (float)(9.5367431640625e-07 * (fabs(xd) + C.tau_max));   // 2^-20
-            const float4 *__restrict__ rp =
-                M.rec + (int64_t)view * C.hm * C.wm + (int64_t)ys * C.wm + xs;
-            for (int r = j; r < bh; r += T) {
-                const float4 *__restrict__ row = rp + (int64_t)r * C.wm;
+    // Footprint scan over the 16-byte records {m, D, tau32, n}.  m_max: f32
+    // widening is exact and monotone, so fmaxf in f32 equals the reference's
+    // f64 `if mv > m_max` (NaN never wins).  Support: the f32 margin test
+    // e = |f32(x_d) - D| - tau32 has |error| < 2^-22 (|x_d| + tau_max); beyond
+    // M = 2^-20 (|x_d| + tau_max) from 0 it decides the reference's f64 test
+    // |x_d - f64(D)| <= tau(n) exactly, inside M the f64 test runs.  Ineligible
+    // pixels (mask <= 0.5 or n == 0) carry tau32 = -1e30: never counted.
+    const float4 *__restrict__ rp = M.rec + (int64_t)view * C.hm * C.wm + ys * (int64_t)C.wm + xs;
+    const double xd = q.x_d;
+    const float xd32 = (float)xd;
+    const float Mg = (float)(9.5367431640625e-07 * (fabs(xd) + C.tau_max));   // 2^-20
+    const int bw = (int)(xe - xs) + 1;
+    const int npix = bw * ((int)(ye - ys) + 1);
+    int sup = 0;
+    float mmax = 0.0f;
+    int col = 0, off = 0;
 #pragma unroll 4
-                for (int c = 0; c < bw; ++c) {
-                    const float4 v = __ldg(row + c);
-                    mmax = fmaxf(mmax, v.x);
-                    const float e = fabsf(xd32 - v.y) - v.z;
-                    sup += (e <= -Mg) ? 1 : 0;
-                    if (fabsf(e) < Mg)    // within the margin: the reference's f64 compare
-                        sup += (fabs(xd - (double)v.y) <= tau_thin(C, __float_as_int(v.w))) ? 1 : 0;
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 1; o < T; o <<= 1) {
-            sup += __shfl_xor_sync(0xffffffffu, sup, o);
-            mmax = fmaxf(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
-        }
-        if (bw > 0 && j == 0) {
-            const int npix = bw * bh;
-            const double m_max = (double)mmax;
-            const double p_cov = sup == 0 ? 0.0 : (double)sup / (double)npix;
-            const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
-            if (t >= C.thin_accept) {
-                const uint32_t slot = s_q[item].slot;
-                K.t[(int64_t)view * C.cap + slot] = t;
-                atomicOr(K.bits_thin + (int64_t)(view >> 5) * C.cap + slot, 1u << (view & 31));
-            }
-        }
+    for (int i = 0; i < npix; ++i) {
+        const float4 r = __ldg(rp + off + col);
+        mmax = fmaxf(mmax, r.x);
+        const float e = fabsf(xd32 - r.y) - r.z;
+        sup += (e <= -Mg) ? 1 : 0;
+        if (fabsf(e) < Mg)    // within the margin: the reference's f64 compare
+            sup += (fabs(xd - (double)r.y) <= tau_thin(C, __float_as_int(r.w))) ? 1 : 0;
+        if (++col == bw) { col = 0; off += C.wm; }
+    }
+    const double m_max = (double)mmax;
+    const double p_cov = sup == 0 ? 0.0 : (double)sup / (double)npix;
+    const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
+    if (npix > 0 && t >= C.thin_accept) {
+        K.t[(int64_t)view * C.cap + q.slot] = t;
+        atomicOr(K.bits_thin + (int64_t)(view >> 5) * C.cap + q.slot, 1u << (view & 31));
     }
 }
 
@@ -814,11 +772,7 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     __syncthreads();
     // phase B: the queued candidates, densely packed onto the first warps
     const int nq = s_nq;
-    if (nq == 0) return;
-    if (nq <= kPairThreads / 8) thin_items<8>(C, k, M, K, view, s_q, nq);
-    else if (nq <= kPairThreads / 4) thin_items<4>(C, k, M, K, view, s_q, nq);
-    else if (nq <= kPairThreads / 2) thin_items<2>(C, k, M, K, view, s_q, nq);
-    else thin_items<1>(C, k, M, K, view, s_q, nq);
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) thin_item(C, k, M, K, view, s_q[i]);
 }
 
 // ---------------------------------------------------------------------------
