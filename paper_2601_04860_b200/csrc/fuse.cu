@@ -715,6 +715,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     const int npix = bw * ((int)(ye - ys) + 1);
     int sup = 0;
     float mmax = 0.0f;
+    bool unsure = false;
     int col = 0, off = 0;
 #pragma unroll 4
     for (int i = 0; i < npix; ++i) {
@@ -722,9 +723,19 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
         mmax = fmaxf(mmax, r.x);
         const float e = fabsf(xd32 - r.y) - r.z;
         sup += (e <= -Mg) ? 1 : 0;
-        if (fabsf(e) < Mg)    // within the margin: the reference's f64 compare
-            sup += (fabs(xd - (double)r.y) <= tau_thin(C, __float_as_int(r.w))) ? 1 : 0;
+        unsure |= fabsf(e) < Mg;
         if (++col == bw) { col = 0; off += C.wm; }
+    }
+    if (unsure) {   // some pixel within the margin: recount with the reference's f64 test
+        sup = 0;
+        col = 0;
+        off = 0;
+        for (int i = 0; i < npix; ++i) {
+            const float4 r = __ldg(rp + off + col);
+            sup += (r.z > 0.0f && fabs(xd - (double)r.y) <= tau_thin(C, __float_as_int(r.w)))
+                       ? 1 : 0;
+            if (++col == bw) { col = 0; off += C.wm; }
+        }
     }
     const double m_max = (double)mmax;
     const double p_cov = sup == 0 ? 0.0 : (double)sup / (double)npix;
