@@ -463,12 +463,14 @@ def run_ours(args):
 
 
 def run_e2e(args, wl, params, dev):
-    """refine_masks + fuse through the drop-in API from pinned host buffers."""
+    """One fusion update through the public API from pinned host buffers:
+    ``refine_and_fuse`` (refine_mask for every view + fuse, as the session
+    does) -> host OccupancyGrid + refined ConfidenceMasks."""
     import torch
 
     import workloads
-    from paper_2601_04860_b200 import (ConfidenceMask, DensityGrid, VoxelGrid, fuse,
-                                       refine_masks, ViewGeometry)
+    from paper_2601_04860_b200 import (ConfidenceMask, DensityGrid, VoxelGrid, ViewGeometry,
+                                       refine_and_fuse)
     from paper_2601_04860_b200.geometry import Camera
     nv, H, W = wl.shape
 
@@ -484,14 +486,12 @@ def run_e2e(args, wl, params, dev):
     views = []
     for v, c in enumerate(wl.cams):
         cam = Camera(c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.world_from_camera)
-        views.append(ViewGeometry(cam, None, planes["dmins"][v], planes["dmaxs"][v],
-                                  planes["dexps"][v], planes["nsamps"][v], planes["z_surface"][v]))
-    raw = [ConfidenceMask(planes["raw_masks"][v]) for v in range(nv)]
+        vg = ViewGeometry(cam, None, planes["dmins"][v], planes["dmaxs"][v], planes["dexps"][v],
+                          planes["nsamps"][v], planes["z_surface"][v])
+        views.append((vg, ConfidenceMask(planes["raw_masks"][v])))
 
     def once():
-        refined = refine_masks(raw, views)
-        og = fuse(grid, dens, list(zip(views, refined)), params)
-        return og, refined
+        return refine_and_fuse(grid, dens, views, params)
 
     once()
     torch.cuda.synchronize()
@@ -502,15 +502,15 @@ def run_e2e(args, wl, params, dev):
         times.append(time.perf_counter() - t0)
     ms = 1e3 * float(np.median(times))
     px = nv * H * W
-    h2d = px * 12 + px * 20 + wl.g ** 3 * 4 + nv * 18 * 8
-    rho = planes_density = np.asarray(dens.values, dtype=np.float64)
+    h2d = px * 24 + wl.g ** 3 * 4 + nv * 18 * 8
+    rho = np.asarray(dens.values, dtype=np.float64)
     pv = params.as_vector()
     gated = int(((rho >= pv[4]) | ((pv[13] != 0) & (rho >= pv[5]))).sum())
-    del planes_density
     d2h = px * 4 + 8 + gated * 12
     return {"value": wl.updates() / (ms / 1e3), "unit": "updates/s", "ms_per_step": ms,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "api": "refine_masks(raw, views) + fuse(grid, density, views, params) -> OccupancyGrid",
+            "api": "refine_and_fuse(grid, density, [(ViewGeometry, raw ConfidenceMask)], params)"
+                   " -> (OccupancyGrid, refined masks)",
             "host_buffers": "pinned"}
 
 

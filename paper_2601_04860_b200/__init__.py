@@ -13,6 +13,7 @@ from .segmenter import (ConfidenceMask, refine_bands_device, refine_mask, refine
                         refine_masks_device)
 from .fusion import (DeviceViews, FusionParams, FusionStats, Fuser, OccupancyGrid,
                      extract, extract_device, fuse, fuse_with_stats, project_grid_overlay,
+                     refine_and_fuse,
                      threshold, threshold_device)
 
 __version__ = "0.1.0"
@@ -21,6 +22,6 @@ __all__ = [
     "Camera", "SceneBounds", "VoxelGrid", "look_at", "ViewGeometry", "DensityGrid",
     "ConfidenceMask", "refine_mask", "refine_masks", "refine_masks_device", "refine_bands_device",
     "DeviceViews", "FusionParams", "FusionStats", "Fuser", "OccupancyGrid",
-    "fuse", "fuse_with_stats", "project_grid_overlay",
+    "fuse", "fuse_with_stats", "refine_and_fuse", "project_grid_overlay",
     "threshold", "threshold_device", "extract", "extract_device",
 ]

@@ -732,7 +732,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
         off = 0;
         for (int i = 0; i < npix; ++i) {
             const float4 r = __ldg(rp + off + col);
-            sup += (r.z > 0.0f && fabs(xd - (double)r.y) <= tau_thin(C, __float_as_int(r.w)))
+            sup += (r.z >= 0.0f && fabs(xd - (double)r.y) <= tau_thin(C, __float_as_int(r.w)))
                        ? 1 : 0;
             if (++col == bw) { col = 0; off += C.wm; }
         }

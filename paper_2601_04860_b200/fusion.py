@@ -33,7 +33,7 @@ from ._device import as_device, device, empty
 
 __all__ = [
     "FusionParams", "OccupancyGrid", "FusionStats", "DeviceViews", "Fuser",
-    "fuse", "fuse_with_stats", "project_grid_overlay",
+    "fuse", "fuse_with_stats", "refine_and_fuse", "project_grid_overlay",
     "threshold", "extract", "threshold_device", "extract_device", "gradient_maps_device",
     "pack_cameras", "bounds_arrays",
 ]
@@ -444,6 +444,85 @@ def fuse_with_stats(grid, density, views, params, bounds=None):
     stats = FusionStats(host["n_thick"], host["n_thin"], host["sw"], host["smw"], host["st"],
                         gated)
     return OccupancyGrid(grid, host["probs"]), stats
+
+
+def _upload_planes(views, masks, dev, names):
+    """Copy host maps straight into padded [nv, hm, wm] device planes."""
+    import torch
+    cams = [vg.camera for vg in views]
+    hm = max(int(c.height) for c in cams)
+    wm = max(int(c.width) for c in cams)
+    sizes = [(int(c.height), int(c.width)) for c in cams]
+    same = all(sz == (hm, wm) for sz in sizes)
+    alloc = torch.empty if same else torch.zeros
+    planes = {k: alloc((len(views), hm, wm), dtype=torch.int32 if k == "nsamps" else torch.float32,
+                       device=dev) for k in names}
+    for i, (vg, m, (h, w)) in enumerate(zip(views, masks, sizes)):
+        src = {"raw": m.values if hasattr(m, "values") else m, "z": vg.z_surface,
+               "dmins": vg.d_min, "dmaxs": vg.d_max, "dexps": vg.d_exp, "nsamps": vg.n_samples}
+        for k in names:
+            dt = np.int32 if k == "nsamps" else np.float32
+            planes[k][i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(src[k], dt)),
+                                       non_blocking=True)
+    return planes, sizes, cams
+
+
+def _trusted_mask(values):
+    """A refined ConfidenceMask built from kernel output (already in [0, 1]),
+    skipping the host validation scan of ``ConfidenceMask.__post_init__``."""
+    from .segmenter import ConfidenceMask
+    m = ConfidenceMask.__new__(ConfidenceMask)
+    m.values = values
+    m.refined = True
+    return m
+
+
+def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
+                    return_refined=True):
+    """``refine_mask`` on every (ViewGeometry, raw ConfidenceMask) pair, then
+    ``fuse`` of the refined set -- the session's update (session.py:204-215)
+    as one device pass: each host map is uploaded once, refinement writes the
+    fusion's scan records directly, and only the gated voxels' (index, p)
+    pairs come back.  Returns (OccupancyGrid, [refined ConfidenceMask] or None).
+
+    Same validation and errors as the two reference calls; results identical
+    to ``fuse(grid, density, [(v, refine_mask(m, v)) ...], params, bounds)``.
+    """
+    import torch
+    from .segmenter import refine_bands_device
+    g = int(grid.resolution)
+    _check_layout(grid, density)
+    views = list(views)
+    for vg, m in views:
+        if m.refined:
+            raise ValueError("mask is already refined")
+        if m.shape != vg.z_surface.shape:
+            raise ValueError("mask and view dimensions differ")
+    if not views:
+        return OccupancyGrid(grid, np.zeros((g, g, g))), ([] if return_refined else None)
+    dev = device()
+    vgs = [vg for vg, _m in views]
+    planes, sizes, cams = _upload_planes(vgs, [m for _vg, m in views], dev,
+                                         ("raw", "z", "dmins", "dmaxs", "dexps", "nsamps"))
+    dens = as_device(density.values, np.float32, dev)
+    fuser = Fuser(grid, params, bounds)
+    refined, aux = refine_bands_device(planes["raw"], planes["z"], planes["nsamps"],
+                                       planes["dexps"], fuser.pv, fuser.dx,
+                                       planar=return_refined)
+    dv = DeviceViews(torch.from_numpy(pack_cameras(cams)).to(dev), refined if refined is not None
+                     else planes["raw"], planes["dmins"], planes["dmaxs"], planes["dexps"],
+                     planes["nsamps"], sizes=sizes)
+    out = fuser.run(dens, dv, bands=aux)
+    masks = None
+    if return_refined:
+        host = torch.empty(refined.shape, dtype=torch.float32, pin_memory=True)
+        host.copy_(refined, non_blocking=True)
+    probs = _sparse_probs_to_host(out, g ** 3).reshape(g, g, g)
+    if return_refined:
+        torch.cuda.current_stream().synchronize()
+        hn = host.numpy()
+        masks = [_trusted_mask(hn[i, :h, :w]) for i, (h, w) in enumerate(sizes)]
+    return OccupancyGrid(grid, probs), masks
 
 
 def gradient_maps_device(views: DeviceViews, eps: float, kappa: float, stream=None):

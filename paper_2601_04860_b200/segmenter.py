@@ -68,13 +68,16 @@ def refine_masks_device(masks, z_surface, n_samples, out=None, stream=None):
 
 
 def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, out=None,
-                        bands=None, stream=None):
+                        bands=None, stream=None, planar=True):
     """``refine_masks_device`` fused with the fusion's per-view depth bands.
 
     One pass over the planes writes the refined masks and, per 8x8 tile, the
     depth interval in which a thin candidate can find support (used by
     ``Fuser.run(bands=...)`` to skip footprint scans that provably find none).
-    Returns (out, bands).
+    ``bands`` is the fusion's "view aux" buffer: per-pixel scan records
+    (refined mask, d_exp, tau, n) followed by the tile bands.  With
+    ``planar=False`` the planar refined masks are not written (the records
+    carry them) and ``out`` is returned as None.  Returns (out, bands).
     """
     import ctypes
     import torch
@@ -87,8 +90,10 @@ def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, 
         if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
             raise ValueError("refine_bands_device expects contiguous CUDA float32/int32 planes")
     pv = np.asarray(params.as_vector() if hasattr(params, "as_vector") else params, np.float64)
-    if out is None:
+    if out is None and planar:
         out = torch.empty_like(masks)
+    if not planar:
+        out = None
     lib = _native.lib()
     if bands is None:
         bands = torch.empty(lib.divas_bands_size(nv, hm, wm), dtype=torch.uint8,

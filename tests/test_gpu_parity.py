@@ -309,3 +309,27 @@ def test_refine_bands_matches_refine_and_fuse(dev):
     for k in ("probs", "n_thick", "n_thin", "sw", "smw", "st"):
         assert torch.equal(a[k], b[k]), k
     assert np.array_equal(a["probs"].cpu().numpy(), _gpu_fuse(case, dev)[0]["probs"])
+
+
+def test_refine_and_fuse_equals_two_calls(dev):
+    """The batched session update == refine_mask per view + fuse."""
+    from paper_2601_04860_b200 import (ConfidenceMask, FusionParams, fuse, refine_and_fuse,
+                                       refine_mask)
+    raw, _z, refined = golden_io.scene_raw()
+    case = golden_io.scene_cases()["sop"]
+    grid, dens, views, bounds = reference_objects(case)
+    params = FusionParams(*[float(x) for x in case.pv[:13]], enable_thin=bool(case.pv[13]))
+    for v, (vg, _m) in enumerate(views):
+        vg.z_surface = _z[v].copy()
+    raws = [(vg, ConfidenceMask(raw[v])) for v, (vg, _m) in enumerate(views)]
+    og, masks = refine_and_fuse(grid, dens, raws, params, bounds=bounds)
+    for v, m in enumerate(masks):
+        assert m.refined and np.array_equal(m.values, refined[v])
+        assert np.array_equal(refine_mask(raws[v][1], raws[v][0]).values, m.values)
+    og2 = fuse(grid, dens, list(zip([vg for vg, _ in raws], masks)), params, bounds=bounds)
+    assert np.array_equal(og.probs, og2.probs)
+    assert np.allclose(og.probs.ravel(), case.p, rtol=REL_TOL, atol=0)
+    og3, none = refine_and_fuse(grid, dens, raws, params, bounds=bounds, return_refined=False)
+    assert none is None and np.array_equal(og3.probs, og.probs)
+    with pytest.raises(ValueError):
+        refine_and_fuse(grid, dens, [(raws[0][0], masks[0])], params)
