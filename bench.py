@@ -338,11 +338,11 @@ def run_ours(args):
         if ev is not None:
             ev[0].record(stream)
         _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps, params,
-                                        wl.dx, out=dv.masks, bands=bands)
+                                        wl.dx, aux=bands, planar=False)
         if ev is not None:
             ev[1].record(stream)
         out = fuser.run(wl.density, dv, probs=probs, occ=True, vox_range=(lo, hi), workspace=ws,
-                        bands=bands, max_gated=cap)
+                        aux=bands, max_gated=cap)
         ws = out["workspace"]
         if ev is not None:
             ev[2].record(stream)
@@ -413,6 +413,8 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         h = host_copy(wl)
+        from paper_2601_04860_b200.segmenter import refine_masks_device
+        refine_masks_device(dv.raw_masks, dv.z_surface, dv.nsamps, out=dv.masks)
         out = fuser.run(wl.density, dv, stats=True, occ=True)
         torch.cuda.synchronize()
         full_s, det = oracle_sample(wl, h, pv, args.cpu_budget_s)
@@ -432,6 +434,9 @@ def run_ours(args):
     e2e = None
     if rank == 0:
         e2e = run_e2e(args, wl, params, dev)
+        if world == 1:
+            extra["incremental"] = run_incremental(args, wl, params, dev, probs)
+            extra["incremental"]["full_recompute_ms_for_comparison"] = ms
 
     launches_per_step = 3 + 3          # refine: init, minmax, band_pass; fuse: gate, pairs, reduce
     line = {
@@ -512,6 +517,47 @@ def run_e2e(args, wl, params, dev):
             "api": "refine_and_fuse(grid, density, [(ViewGeometry, raw ConfidenceMask)], params)"
                    " -> (OccupancyGrid, refined masks)",
             "host_buffers": "pinned"}
+
+
+def run_incremental(args, wl, params, dev, full_probs, updates=200):
+    """BASELINE C4: re-refine + re-fuse one view of the fused C3 state, cycling
+    over the views; per-update device latency (CUDA events) p50 / p99, and a
+    bit-exactness check of the final state against the full fusion."""
+    import torch
+
+    import workloads
+    from paper_2601_04860_b200 import DensityGrid, FusionSession, VoxelGrid
+    from paper_2601_04860_b200.fusion import pack_cameras
+    nv, H, W = wl.shape
+    grid = VoxelGrid(wl.g, workloads.GRID_HALF, wl.origin)
+    dens = DensityGrid(grid, wl.density.cpu().numpy().reshape(wl.g, wl.g, wl.g))
+    s = FusionSession(grid, dens, params, (H, W), max_views=nv + 1, dev=dev)
+    for name, src in (("raw", wl.raw_masks), ("z", wl.z_surface), ("dmins", wl.dmins),
+                      ("dmaxs", wl.dmaxs), ("dexps", wl.dexps), ("nsamps", wl.nsamps)):
+        getattr(s, name)[:nv].copy_(src)
+    s.cams[:nv].copy_(torch.from_numpy(pack_cameras(wl.cams)))
+    s.sizes = [(H, W)] * nv
+    s.nv = nv
+    s._refine(0, nv)
+    s._fuse(0, nv)
+    torch.cuda.synchronize()
+    lat = []
+    for k in range(updates + 5):
+        i = k % nv
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s.replace_mask_device(i, wl.raw_masks[i])
+        e1.record()
+        e1.synchronize()
+        if k >= 5:
+            lat.append(e0.elapsed_time(e1))
+    exact = bool(torch.equal(s.probs, full_probs))
+    lat = np.asarray(lat)
+    return {"config": "C4: re-refine + re-fuse 1 of 32 views of the fused C3 state, "
+                      f"{updates} updates cycling over the views",
+            "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+            "mean_ms": float(lat.mean()), "bit_exact_vs_full": exact,
+            "full_recompute_ms_for_comparison": None}
 
 
 def main():

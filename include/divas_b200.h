@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define DIVAS_ABI_VERSION 3
+#define DIVAS_ABI_VERSION 4
 
 /* error codes */
 #define DIVAS_OK          0
@@ -64,20 +64,35 @@ int divas_refine(int32_t nv, int64_t hm, int64_t wm,
                  const float *mask, const float *z_surface, const int32_t *n_samples,
                  float *out, void *workspace, size_t workspace_bytes, void *stream);
 
-/* Refinement fused with the fusion's per-view depth bands: same `out` as
- * divas_refine, plus `bands` (divas_bands_size bytes, device) summarising,
- * per 8x8 pixel tile, the depth interval in which a thin candidate can find
- * support (pv = FusionParams.as_vector(), dx_vox = voxel size).  Pass the
- * bands to divas_fuse to skip its own band pass.  Needs dexp [nv][hm][wm]. */
+/* Refinement fused with the fusion's per-view "aux" data, in one pass:
+ *   out      [nv][hm][wm] f32 refined masks as divas_refine (may be NULL);
+ *   records  [nv][hm][wm] 16-byte scan records {refined mask, d_exp,
+ *            tau_d(n) as f32 or -1e30 when the pixel cannot support a thin
+ *            candidate, n_samples} (divas_records_size bytes);
+ *   bands    [nv][ceil(hm/8)][ceil(wm/8)] {lo, hi} f64 per 8x8 tile: the depth
+ *            interval in which a thin candidate can find support
+ *            (divas_bands_size bytes).
+ * pv = FusionParams.as_vector() and dx_vox (the tolerances depend on them).
+ * Views are independent: view k's slices start at k*hm*wm / k*nty*ntx, so a
+ * single view can be (re)built in place with nv = 1 and offset pointers. */
+size_t divas_records_size(int32_t nv, int64_t hm, int64_t wm);
 size_t divas_bands_size(int32_t nv, int64_t hm, int64_t wm);
 int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm,
                        const float *mask, const float *z_surface, const int32_t *n_samples,
                        const float *dexp, float *out, const double *pv, double dx_vox,
-                       void *bands, void *workspace, size_t workspace_bytes, void *stream);
+                       void *records, void *bands, void *workspace, size_t workspace_bytes,
+                       void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Fusion                                                                   */
 /* ---------------------------------------------------------------------- */
+#define DIVAS_FUSE_FULL        0  /* gate + all views + reduce                  */
+#define DIVAS_FUSE_INCREMENTAL 1  /* views [view_lo, view_hi) only, then reduce
+                                     over all nv views.  Requires a previous
+                                     FULL call on the same workspace, density,
+                                     range, params and output buffers; the
+                                     other views' contributions are reused.    */
+
 typedef struct divas_fuse_args {
     int64_t g;                   /* grid resolution G (voxels per axis)       */
     double origin[3];            /* grid min corner (VoxelGrid.origin)        */
@@ -86,7 +101,8 @@ typedef struct divas_fuse_args {
     int32_t nv;                  /* number of views (>= 1)                    */
     int32_t hm, wm;              /* padded plane height / width               */
     const double *cams;          /* [nv][DIVAS_CAM_STRIDE]                    */
-    const float *masks;          /* [nv][hm][wm] refined confidences          */
+    const float *masks;          /* [nv][hm][wm] refined confidences (read only
+                                    when records == NULL)                     */
     const float *dmins, *dmaxs, *dexps;   /* [nv][hm][wm]                     */
     const int32_t *nsamps;       /* [nv][hm][wm]                              */
     double pv[DIVAS_NPARAM];     /* FusionParams.as_vector()                  */
@@ -102,15 +118,19 @@ typedef struct divas_fuse_args {
                                     the density gate in [lo, hi); <= 0 means
                                     hi - lo (always safe).  divas_gate_count
                                     gives the exact figure for a density grid. */
-    const void *bands;           /* depth bands from divas_refine_bands for these
-                                    views and pv / dx_vox, or NULL (divas_fuse
-                                    then builds them in its workspace) */
+    const void *records;         /* scan records / bands of divas_refine_bands   */
+    const void *bands;           /* for these views, pv and dx_vox; NULL: built
+                                    in the workspace from masks/n/d_exp         */
+    int32_t nv_cap;              /* views the workspace holds (>= nv; <= 0: nv) */
+    int32_t mode;                /* DIVAS_FUSE_FULL / DIVAS_FUSE_INCREMENTAL    */
+    int32_t view_lo, view_hi;    /* INCREMENTAL: views to (re)evaluate          */
 } divas_fuse_args;
 
-/* Workspace bytes for divas_fuse with slot capacity `max_gated` and `nv` views
- * of padded size hm x wm (~ max_gated * (4 + nv * 24.25) bytes for the
- * [view][slot] contributions, plus the depth bands). */
-size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv, int32_t hm, int32_t wm);
+/* Workspace bytes for divas_fuse with slot capacity `max_gated`, `nv_cap`
+ * views of padded size hm x wm (~ max_gated * (4 + nv_cap * 24.25) bytes for
+ * the [view][slot] contributions, plus records and bands when the caller does
+ * not supply them). */
+size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv_cap, int32_t hm, int32_t wm);
 int divas_fuse(const divas_fuse_args *args, void *workspace, size_t workspace_bytes,
                void *stream);
 

@@ -9,19 +9,21 @@ entry points on top.  See DESIGN.md.
 from .geometry import Camera, SceneBounds, VoxelGrid, look_at
 from .render import ViewGeometry
 from .scene import DensityGrid
-from .segmenter import (ConfidenceMask, refine_bands_device, refine_mask, refine_masks,
+from .segmenter import (ConfidenceMask, ViewAux, refine_bands_device, refine_mask, refine_masks,
                         refine_masks_device)
 from .fusion import (DeviceViews, FusionParams, FusionStats, Fuser, OccupancyGrid,
                      extract, extract_device, fuse, fuse_with_stats, project_grid_overlay,
                      refine_and_fuse,
                      threshold, threshold_device)
 
+from .incremental import FusionSession
+
 __version__ = "0.1.0"
 
 __all__ = [
     "Camera", "SceneBounds", "VoxelGrid", "look_at", "ViewGeometry", "DensityGrid",
-    "ConfidenceMask", "refine_mask", "refine_masks", "refine_masks_device", "refine_bands_device",
+    "ConfidenceMask", "ViewAux", "refine_mask", "refine_masks", "refine_masks_device", "refine_bands_device",
     "DeviceViews", "FusionParams", "FusionStats", "Fuser", "OccupancyGrid",
     "fuse", "fuse_with_stats", "refine_and_fuse", "project_grid_overlay",
-    "threshold", "threshold_device", "extract", "extract_device",
+    "threshold", "threshold_device", "extract", "extract_device", "FusionSession",
 ]

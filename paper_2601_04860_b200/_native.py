@@ -19,7 +19,8 @@ NPARAM = 14
 
 # every symbol include/divas_b200.h declares
 EXPORTS = (
-    "divas_refine_workspace_size", "divas_refine", "divas_bands_size", "divas_refine_bands",
+    "divas_refine_workspace_size", "divas_refine", "divas_records_size", "divas_bands_size",
+    "divas_refine_bands",
     "divas_fuse_workspace_size", "divas_fuse", "divas_gate_count", "divas_fuse_gated_count",
     "divas_fuse_overflow",
     "divas_gradient_maps",
@@ -44,8 +45,12 @@ class FuseArgs(ctypes.Structure):
         ("unbounded", ctypes.c_int32), ("vox_lo", ctypes.c_int64), ("vox_hi", ctypes.c_int64),
         ("probs", _VP), ("n_thick", _VP), ("n_thin", _VP), ("sw", _VP), ("smw", _VP),
         ("st", _VP), ("occ", _VP), ("occ_thr", ctypes.c_double), ("max_gated", ctypes.c_int64),
-        ("bands", _VP),
+        ("records", _VP), ("bands", _VP), ("nv_cap", ctypes.c_int32), ("mode", ctypes.c_int32),
+        ("view_lo", ctypes.c_int32), ("view_hi", ctypes.c_int32),
     ]
+
+FUSE_FULL = 0
+FUSE_INCREMENTAL = 1
 
 
 _lib = None
@@ -57,9 +62,10 @@ def _declare(lib):
     sig = {
         "divas_refine_workspace_size": (S, [I32]),
         "divas_refine": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP, S, _VP]),
+        "divas_records_size": (S, [I32, I64, I64]),
         "divas_bands_size": (S, [I32, I64, I64]),
         "divas_refine_bands": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP,
-                                              ctypes.POINTER(D), D, _VP, _VP, S, _VP]),
+                                              ctypes.POINTER(D), D, _VP, _VP, _VP, S, _VP]),
         "divas_fuse_workspace_size": (S, [I64, I32, I32, I32]),
         "divas_fuse": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, S, _VP]),
         "divas_gate_count": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, _VP]),

@@ -130,12 +130,6 @@ inline size_t band_bytes(int nv, int hm, int wm) {
            sizeof(double2);
 }
 
-// "view aux" buffer: scan records [nv][hm][wm] float4, then the tile bands.
-inline size_t aux_records_bytes(int nv, int hm, int wm) {
-    return ((size_t)nv * hm * wm * sizeof(float4) + 255) & ~(size_t)255;
-}
-inline size_t aux_bytes(int nv, int hm, int wm) {
-    return aux_records_bytes(nv, hm, wm) + band_bytes(nv, hm, wm);
-}
+inline size_t record_bytes(int nv, int hm, int wm) { return (size_t)nv * hm * wm * sizeof(float4); }
 
 }  // namespace divas

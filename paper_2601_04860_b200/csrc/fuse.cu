@@ -45,6 +45,7 @@ struct FuseConst {
     double origin0, origin1, origin2, dx;
     int nv, hm, wm, w32;
     int64_t cap;   // slot capacity of the workspace (max gated voxels)
+    int view0;     // first view of the pair launch (incremental updates)
     double gamma, beta, bmax, lam, rho_thr, rho_thin, thin_pct, alpha1, thin_accept, eps,
         mask_thr, thin_floor, kappa;
     int enable_thin;
@@ -761,7 +762,7 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     const long long block0 = (long long)blockIdx.x * blockDim.x;
     if (block0 >= n) return;                                   // whole CTA idle
     const long long slot = block0 + threadIdx.x;
-    const int view = blockIdx.y;
+    const int view = C.view0 + (int)blockIdx.y;
     Cam k;
     load_cam(cams + (int64_t)view * kCamStride, k);
     // phase A: route every pair; queue the thin candidates that need a scan
@@ -864,27 +865,44 @@ __global__ void gradient_maps_kernel(int nv, int hm, int wm, const float *__rest
     }
 }
 
+// Incremental updates: drop the contribution bits of views [lo, hi) before
+// they are re-evaluated.
+__global__ void clear_view_bits(Contrib K, int64_t cap, int view_lo, int view_hi,
+                                const WsHeader *__restrict__ hdr) {
+    const long long n = min((long long)hdr->count, (long long)cap);
+    for (long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x; slot < n;
+         slot += (long long)gridDim.x * blockDim.x) {
+        for (int wd = view_lo >> 5; wd <= (view_hi - 1) >> 5; ++wd) {
+            const int a = max(view_lo - wd * 32, 0), b = min(view_hi - wd * 32, 32);
+            const uint32_t keep = ~(((b >= 32) ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << a) - 1u));
+            K.bits_thick[(int64_t)wd * cap + slot] &= keep;
+            K.bits_thin[(int64_t)wd * cap + slot] &= keep;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // workspace layout
 // ---------------------------------------------------------------------------
 struct WsLayout {
-    size_t work, bits_thick, bits_thin, w, mw, t, bands, total;
+    size_t work, bits_thick, bits_thin, w, mw, t, rec, bands, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static WsLayout ws_layout(int64_t cap, int32_t nv, int32_t hm, int32_t wm) {
+static WsLayout ws_layout(int64_t cap, int32_t nv_cap, int32_t hm, int32_t wm) {
     const size_t c = (size_t)(cap > 0 ? cap : 1);
-    const size_t w32 = (size_t)((nv + 31) / 32);
+    const size_t w32 = (size_t)((nv_cap + 31) / 32);
     WsLayout L;
     size_t off = 256;
     L.work = off;       off = align256(off + c * 4);
     L.bits_thick = off; off = align256(off + w32 * c * 4);
     L.bits_thin = off;  off = align256(off + w32 * c * 4);
-    L.w = off;          off = align256(off + (size_t)nv * c * 8);
-    L.mw = off;         off = align256(off + (size_t)nv * c * 8);
-    L.t = off;          off = align256(off + (size_t)nv * c * 8);
-    L.bands = off;      off = align256(off + aux_bytes(nv, hm, wm));
+    L.w = off;          off = align256(off + (size_t)nv_cap * c * 8);
+    L.mw = off;         off = align256(off + (size_t)nv_cap * c * 8);
+    L.t = off;          off = align256(off + (size_t)nv_cap * c * 8);
+    L.rec = off;        off = align256(off + record_bytes(nv_cap, hm, wm));
+    L.bands = off;      off = align256(off + band_bytes(nv_cap, hm, wm));
     L.total = off;
     return L;
 }
@@ -905,6 +923,7 @@ static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     C.dx = a->dx_vox;
     C.nv = a->nv; C.hm = a->hm; C.wm = a->wm; C.w32 = (a->nv + 31) / 32;
     C.cap = cap;
+    C.view0 = 0;
     const double *pv = a->pv;
     C.gamma = pv[0]; C.beta = pv[1]; C.bmax = pv[2]; C.lam = pv[3]; C.rho_thr = pv[4];
     C.rho_thin = pv[5]; C.thin_pct = pv[6]; C.alpha1 = pv[7]; C.thin_accept = pv[8];
@@ -931,13 +950,34 @@ static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O,
                                                                              hdr, count_only);
 }
 
+// records + bands of views [v0, v0 + cnt) from planar refined masks
+static void launch_aux(const divas_fuse_args *a, int v0, int cnt, float4 *rec, double2 *bands,
+                       cudaStream_t s) {
+    const BandParams B = band_params(a->pv, a->dx_vox, a->hm, a->wm);
+    const int64_t plane = (int64_t)a->hm * a->wm;
+    const float *m = a->masks + v0 * plane;
+    const int32_t *n = a->nsamps + v0 * plane;
+    const float *d = a->dexps + v0 * plane;
+    float4 *r = rec + v0 * plane;
+    double2 *b = bands + (int64_t)v0 * B.nty * B.ntx;
+    const bool vec = (a->wm % 4 == 0) &&
+                     ((((uintptr_t)m) | ((uintptr_t)n) | ((uintptr_t)d)) & 15) == 0;
+    if (vec) {
+        dim3 bg((unsigned)((a->wm / 4 + 255) / 256), (unsigned)B.nty, (unsigned)cnt);
+        band_pass<4, false><<<bg, 256, 0, s>>>(B, m, nullptr, n, d, nullptr, nullptr, b, r, cnt);
+    } else {
+        dim3 bg((unsigned)((a->wm + 255) / 256), (unsigned)B.nty, (unsigned)cnt);
+        band_pass<1, false><<<bg, 256, 0, s>>>(B, m, nullptr, n, d, nullptr, nullptr, b, r, cnt);
+    }
+}
+
 }  // namespace divas
 
 using namespace divas;
 
-extern "C" size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv, int32_t hm,
+extern "C" size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv_cap, int32_t hm,
                                             int32_t wm) {
-    return ws_layout(max_gated, nv > 0 ? nv : 1, hm > 0 ? hm : 1, wm > 0 ? wm : 1).total;
+    return ws_layout(max_gated, nv_cap > 0 ? nv_cap : 1, hm > 0 ? hm : 1, wm > 0 ? wm : 1).total;
 }
 
 extern "C" const int64_t *divas_fuse_gated_count(const void *workspace) {
@@ -983,16 +1023,33 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
                           void *stream) {
     int rc = validate(a, "divas_fuse");
     if (rc) return rc;
-    if (a->nv < 1 || a->nv > 1024) { set_error("divas_fuse: view count %d outside [1, 1024]", a->nv); return DIVAS_EINVAL; }
-    if (a->nv > 65535) { set_error("divas_fuse: too many views"); return DIVAS_EINVAL; }
+    const int nv_cap = a->nv_cap > 0 ? a->nv_cap : a->nv;
+    if (a->nv < 1 || a->nv > 1024 || nv_cap < a->nv || nv_cap > 1024) {
+        set_error("divas_fuse: view count %d / capacity %d outside [1, 1024]", a->nv, nv_cap);
+        return DIVAS_EINVAL;
+    }
     if (a->hm < 1 || a->wm < 1) { set_error("divas_fuse: empty planes"); return DIVAS_EINVAL; }
-    if (!a->cams || !a->masks || !a->dmins || !a->dmaxs || !a->dexps || !a->nsamps ||
-        !a->probs || !workspace) {
+    if (!a->cams || !a->dmins || !a->dmaxs || !a->dexps || !a->nsamps || !a->probs || !workspace ||
+        (!a->records && !a->masks)) {
         set_error("divas_fuse: null pointer");
         return DIVAS_EINVAL;
     }
+    if ((a->records == nullptr) != (a->bands == nullptr)) {
+        set_error("divas_fuse: records and bands come together");
+        return DIVAS_EINVAL;
+    }
+    const bool incr = a->mode == DIVAS_FUSE_INCREMENTAL;
+    if (a->mode != DIVAS_FUSE_FULL && !incr) { set_error("divas_fuse: bad mode"); return DIVAS_EINVAL; }
+    int v0 = 0, v1 = a->nv;
+    if (incr) {
+        v0 = a->view_lo; v1 = a->view_hi;
+        if (v0 < 0 || v1 > a->nv || v0 >= v1) {
+            set_error("divas_fuse: incremental views [%d, %d) outside [0, %d)", v0, v1, a->nv);
+            return DIVAS_EINVAL;
+        }
+    }
     const int64_t cap = a->max_gated > 0 ? a->max_gated : (a->vox_hi - a->vox_lo);
-    const WsLayout L = ws_layout(cap, a->nv, a->hm, a->wm);
+    const WsLayout L = ws_layout(cap, nv_cap, a->hm, a->wm);
     if (workspace_bytes < L.total) {
         set_error("divas_fuse: workspace too small (%zu < %zu)", workspace_bytes, L.total);
         return DIVAS_EWORKSPACE;
@@ -1001,46 +1058,38 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     FuseConst C;
     fill_const(C, a, cap);
     FuseOut O{a->probs, a->n_thick, a->n_thin, a->sw, a->smw, a->st, a->occ};
-    FuseMaps M{a->masks, a->dmins, a->dmaxs, a->dexps, a->nsamps, nullptr, nullptr};
-    if (a->bands) {
-        M.rec = (const float4 *)a->bands;
-        M.bands = (const double2 *)((const char *)a->bands + aux_records_bytes(a->nv, a->hm, a->wm));
-    }
+    FuseMaps M{a->masks, a->dmins, a->dmaxs, a->dexps, a->nsamps,
+               (const double2 *)a->bands, (const float4 *)a->records};
     char *ws = (char *)workspace;
     WsHeader *hdr = (WsHeader *)ws;
     uint32_t *work = (uint32_t *)(ws + L.work);
     Contrib K{(uint32_t *)(ws + L.bits_thick), (uint32_t *)(ws + L.bits_thin),
               (double *)(ws + L.w), (double *)(ws + L.mw), (double *)(ws + L.t)};
-    if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess ||
-        cudaMemsetAsync(ws + L.bits_thick, 0, L.w - L.bits_thick, s) != cudaSuccess)
-        return check_launch("divas_fuse(memset)");
     if (a->vox_hi == a->vox_lo) return DIVAS_OK;
-    if (!M.rec) {   // scan records + depth bands of the views (bands.cuh)
-        char *aux = ws + L.bands;
-        float4 *rec = (float4 *)aux;
-        double2 *bands = (double2 *)(aux + aux_records_bytes(a->nv, a->hm, a->wm));
-        const BandParams B = band_params(a->pv, a->dx_vox, a->hm, a->wm);
-        const bool vec = (a->wm % 4 == 0) &&
-                         ((((uintptr_t)a->masks) | ((uintptr_t)a->nsamps) | ((uintptr_t)a->dexps)) & 15) == 0;
-        if (vec) {
-            dim3 bg((unsigned)((a->wm / 4 + 255) / 256), (unsigned)B.nty, (unsigned)a->nv);
-            band_pass<4, false><<<bg, 256, 0, s>>>(B, a->masks, nullptr, a->nsamps, a->dexps,
-                                                   nullptr, nullptr, bands, rec, a->nv);
-        } else {
-            dim3 bg((unsigned)((a->wm + 255) / 256), (unsigned)B.nty, (unsigned)a->nv);
-            band_pass<1, false><<<bg, 256, 0, s>>>(B, a->masks, nullptr, a->nsamps, a->dexps,
-                                                   nullptr, nullptr, bands, rec, a->nv);
-        }
+    if (!M.rec) {   // scan records + depth bands of the evaluated views (bands.cuh)
+        float4 *rec = (float4 *)(ws + L.rec);
+        double2 *bands = (double2 *)(ws + L.bands);
+        launch_aux(a, v0, v1 - v0, rec, bands, s);
         if ((rc = check_launch("divas_fuse(aux)"))) return rc;
         M.rec = rec;
         M.bands = bands;
     }
-    launch_gate(C, a->density, O, work, hdr, 0, s);
-    if ((rc = check_launch("divas_fuse(gate)"))) return rc;
+    if (!incr) {
+        if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess ||
+            cudaMemsetAsync(ws + L.bits_thick, 0, L.w - L.bits_thick, s) != cudaSuccess)
+            return check_launch("divas_fuse(memset)");
+        launch_gate(C, a->density, O, work, hdr, 0, s);
+        if ((rc = check_launch("divas_fuse(gate)"))) return rc;
+    } else {
+        const int64_t blocks = std::min<int64_t>((cap + 255) / 256, (int64_t)sm_count() * 8);
+        clear_view_bits<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(K, cap, v0, v1, hdr);
+        if ((rc = check_launch("divas_fuse(clear)"))) return rc;
+    }
     const int64_t cap_blocks = (cap + kPairThreads - 1) / kPairThreads;
     if (cap_blocks > 0x7fffffffLL) { set_error("divas_fuse: too many slots"); return DIVAS_EINVAL; }
-    fuse_pairs<<<dim3((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)a->nv), kPairThreads, 0,
-                 s>>>(C, a->cams, a->density, M, K, work, hdr);
+    C.view0 = v0;
+    fuse_pairs<<<dim3((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)(v1 - v0)),
+                 kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr);
     if ((rc = check_launch("divas_fuse(pairs)"))) return rc;
     const unsigned rblocks = (unsigned)std::max<int64_t>((cap + kReduceThreads - 1) / kReduceThreads, 1);
     if (a->nv <= 32) fuse_reduce<32><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);

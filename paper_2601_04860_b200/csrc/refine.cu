@@ -159,14 +159,14 @@ extern "C" int divas_refine(int32_t nv, int64_t hm, int64_t wm, const float *mas
 extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const float *mask,
                                   const float *z_surface, const int32_t *n_samples,
                                   const float *dexp, float *out, const double *pv, double dx_vox,
-                                  void *bands, void *workspace, size_t workspace_bytes,
-                                  void *stream) {
+                                  void *records, void *bands, void *workspace,
+                                  size_t workspace_bytes, void *stream) {
     if (nv <= 0 || hm <= 0 || wm <= 0) { set_error("divas_refine_bands: empty view set"); return DIVAS_EINVAL; }
     if (nv > 65535 || hm > 0x7fffffff / 2 || wm > 0x7fffffff / 2) {
         set_error("divas_refine_bands: plane too large");
         return DIVAS_EINVAL;
     }
-    if (!mask || !z_surface || !n_samples || !dexp || !pv || !bands || !workspace) {
+    if (!mask || !z_surface || !n_samples || !dexp || !pv || !records || !bands || !workspace) {
         set_error("divas_refine_bands: null pointer");
         return DIVAS_EINVAL;
     }
@@ -179,27 +179,29 @@ extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const floa
     const int64_t plane = hm * wm;
     const bool vec = (wm % 4 == 0) &&
                      ((((uintptr_t)mask) | ((uintptr_t)z_surface) | ((uintptr_t)n_samples) |
-                       ((uintptr_t)out) | ((uintptr_t)dexp)) & 15) == 0;
+                       ((uintptr_t)out) | ((uintptr_t)dexp) | ((uintptr_t)records)) & 15) == 0;
     refine_init<<<(nv + 255) / 256, 256, 0, s>>>(ws, nv);
     dim3 grid(blocks_per_view(plane, nv), nv);
-    auto bands_of = [](void *aux, int nv_, int64_t hm_, int64_t wm_) {
-        return (double2 *)((char *)aux + aux_records_bytes(nv_, (int)hm_, (int)wm_));
-    };
     const BandParams B = band_params(pv, dx_vox, (int)hm, (int)wm);
     if (vec) {
         refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((wm / 4 + 255) / 256), (unsigned)B.nty, (unsigned)nv);
         band_pass<4, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
-                                              bands_of(bands, nv, hm, wm), (float4 *)bands, nv);
+                                              (double2 *)bands, (float4 *)records, nv);
     } else {
         refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((wm + 255) / 256), (unsigned)B.nty, (unsigned)nv);
         band_pass<1, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
-                                              bands_of(bands, nv, hm, wm), (float4 *)bands, nv);
+                                              (double2 *)bands, (float4 *)records, nv);
     }
     return check_launch("divas_refine_bands");
 }
 
+extern "C" size_t divas_records_size(int32_t nv, int64_t hm, int64_t wm) {
+    return (size_t)(nv > 0 ? nv : 0) * (size_t)(hm > 0 ? hm : 0) * (size_t)(wm > 0 ? wm : 0) *
+           sizeof(float4);
+}
+
 extern "C" size_t divas_bands_size(int32_t nv, int64_t hm, int64_t wm) {
-    return aux_bytes(nv, (int)hm, (int)wm);
+    return band_bytes(nv, (int)hm, (int)wm);
 }

@@ -320,7 +320,12 @@ class Fuser:
 
     def run(self, density, views: DeviceViews, probs=None, stats=False, occ=False,
             occ_thr=0.5, vox_range=None, workspace=None, stream=None, max_gated=None,
-            bands=None):
+            aux=None, nv_cap=None, incremental=None):
+        """Enqueue ``divas_fuse``.  ``aux``: ViewAux from ``refine_bands_device``
+        (else built in the workspace).  ``incremental=(v0, v1)``: re-evaluate
+        only views [v0, v1) against the state a previous full ``run`` left in
+        ``workspace`` (same density, range, params and output buffers) --
+        ``nv_cap`` sizes that workspace for views added later."""
         import ctypes
         import torch
         g = self.g
@@ -345,7 +350,8 @@ class Fuser:
         elif occ is not False and occ is not None:
             out["occ"] = occ
         lib = _native.lib()
-        wsb = lib.divas_fuse_workspace_size(cap, views.nv, views.hm, views.wm)
+        nvc = max(int(nv_cap or views.nv), views.nv)
+        wsb = lib.divas_fuse_workspace_size(cap, nvc, views.hm, views.wm)
         if workspace is None or workspace.numel() < wsb:
             workspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
         out["workspace"] = workspace
@@ -362,7 +368,12 @@ class Fuser:
         a.occ = _native.ptr(out.get("occ"))
         a.occ_thr = float(occ_thr)
         a.max_gated = cap
-        a.bands = _native.ptr(bands)
+        if aux is not None:
+            a.records, a.bands = _native.ptr(aux.records), _native.ptr(aux.bands)
+        a.nv_cap = nvc
+        if incremental is not None:
+            a.mode = _native.FUSE_INCREMENTAL
+            a.view_lo, a.view_hi = int(incremental[0]), int(incremental[1])
         _native.check(lib.divas_fuse(ctypes.byref(a), _native.ptr(workspace), wsb,
                                      _native.stream_handle(stream)), "divas_fuse")
         return out
@@ -509,10 +520,11 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     refined, aux = refine_bands_device(planes["raw"], planes["z"], planes["nsamps"],
                                        planes["dexps"], fuser.pv, fuser.dx,
                                        planar=return_refined)
+    # the fusion reads the refined masks from aux.records, never from dv.masks
     dv = DeviceViews(torch.from_numpy(pack_cameras(cams)).to(dev), refined if refined is not None
                      else planes["raw"], planes["dmins"], planes["dmaxs"], planes["dexps"],
                      planes["nsamps"], sizes=sizes)
-    out = fuser.run(dens, dv, bands=aux)
+    out = fuser.run(dens, dv, aux=aux)
     masks = None
     if return_refined:
         host = torch.empty(refined.shape, dtype=torch.float32, pin_memory=True)

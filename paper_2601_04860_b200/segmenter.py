@@ -15,7 +15,7 @@ import numpy as np
 from . import _native
 from ._device import as_device, device, empty
 
-__all__ = ["ConfidenceMask", "refine_mask", "refine_masks", "refine_masks_device",
+__all__ = ["ConfidenceMask", "ViewAux", "refine_mask", "refine_masks", "refine_masks_device",
            "refine_bands_device"]
 
 
@@ -67,17 +67,40 @@ def refine_masks_device(masks, z_surface, n_samples, out=None, stream=None):
     return out
 
 
-def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, out=None,
-                        bands=None, stream=None, planar=True):
-    """``refine_masks_device`` fused with the fusion's per-view depth bands.
+class ViewAux:
+    """The fusion's per-view auxiliary data (csrc/bands.cuh), device-resident:
+    ``records`` [nv, hm, wm] 16-byte scan records {refined mask, d_exp, tau,
+    n_samples} and ``bands`` [nv, ceil(hm/8), ceil(wm/8)] tile depth bands.
+    Built by ``refine_bands_device`` for given FusionParams / voxel size."""
 
-    One pass over the planes writes the refined masks and, per 8x8 tile, the
-    depth interval in which a thin candidate can find support (used by
-    ``Fuser.run(bands=...)`` to skip footprint scans that provably find none).
-    ``bands`` is the fusion's "view aux" buffer: per-pixel scan records
-    (refined mask, d_exp, tau, n) followed by the tile bands.  With
-    ``planar=False`` the planar refined masks are not written (the records
-    carry them) and ``out`` is returned as None.  Returns (out, bands).
+    def __init__(self, records, bands):
+        self.records = records
+        self.bands = bands
+
+    @classmethod
+    def empty(cls, nv, hm, wm, dev):
+        import torch
+        lib = _native.lib()
+        return cls(torch.empty(lib.divas_records_size(nv, hm, wm), dtype=torch.uint8, device=dev),
+                   torch.empty(lib.divas_bands_size(nv, hm, wm), dtype=torch.uint8, device=dev))
+
+    def view_slices(self, v0, v1, nv, hm, wm):
+        """(records, bands) byte views of views [v0, v1)."""
+        lib = _native.lib()
+        r1 = lib.divas_records_size(1, hm, wm)
+        b1 = lib.divas_bands_size(1, hm, wm)
+        return self.records[v0 * r1: v1 * r1], self.bands[v0 * b1: v1 * b1]
+
+
+def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, out=None,
+                        aux=None, stream=None, planar=True):
+    """``refine_masks_device`` fused with the fusion's per-view aux data.
+
+    One pass over the planes writes the refined masks (``planar=True``) and
+    the ``ViewAux`` (scan records + tile depth bands) that ``Fuser.run(aux=)``
+    consumes, so the fusion never re-reads the planar masks.  ``aux`` may be
+    a preallocated ViewAux or a pair of byte tensors (records, bands) for a
+    slice of a larger set.  Returns (out or None, aux).
     """
     import ctypes
     import torch
@@ -95,18 +118,21 @@ def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, 
     if not planar:
         out = None
     lib = _native.lib()
-    if bands is None:
-        bands = torch.empty(lib.divas_bands_size(nv, hm, wm), dtype=torch.uint8,
-                            device=masks.device)
+    if aux is None:
+        aux = ViewAux.empty(nv, hm, wm, masks.device)
+    rec, bands = (aux.records, aux.bands) if isinstance(aux, ViewAux) else aux
+    if rec.numel() < lib.divas_records_size(nv, hm, wm) or \
+            bands.numel() < lib.divas_bands_size(nv, hm, wm):
+        raise ValueError("view aux buffers too small")
     wsb = lib.divas_refine_workspace_size(nv)
     ws = torch.empty(wsb, dtype=torch.uint8, device=masks.device)
     pvc = (ctypes.c_double * 14)(*pv.tolist())
     _native.check(lib.divas_refine_bands(nv, hm, wm, _native.ptr(masks), _native.ptr(z_surface),
                                          _native.ptr(n_samples), _native.ptr(d_exp),
                                          _native.ptr(out), pvc, float(voxel_size),
-                                         _native.ptr(bands), _native.ptr(ws), wsb,
+                                         _native.ptr(rec), _native.ptr(bands), _native.ptr(ws), wsb,
                                          _native.stream_handle(stream)), "divas_refine_bands")
-    return out, bands
+    return out, aux
 
 
 def refine_mask(mask: ConfidenceMask, view) -> ConfidenceMask:

@@ -304,7 +304,7 @@ def test_refine_bands_matches_refine_and_fuse(dev):
     fuser = Fuser(grid_ns(case), case.pv, bounds_ns(case))
     dens = torch.from_numpy(case.density.reshape(-1)).to(dev)
     a = fuser.run(dens, dv, stats=True)
-    b = fuser.run(dens, dv, stats=True, bands=bands)
+    b = fuser.run(dens, dv, stats=True, aux=bands)
     torch.cuda.synchronize()
     for k in ("probs", "n_thick", "n_thin", "sw", "smw", "st"):
         assert torch.equal(a[k], b[k]), k

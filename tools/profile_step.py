@@ -28,8 +28,8 @@ def main():
     params = FusionParams()
     for _ in range(args.steps):      # the bench step: refine+bands, fuse with those bands
         _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps, params,
-                                        wl.dx, out=dv.masks, bands=bands)
-        out = fuser.run(wl.density, dv, probs=probs, occ=True, workspace=ws, bands=bands)
+                                        wl.dx, out=dv.masks, aux=bands)
+        out = fuser.run(wl.density, dv, probs=probs, occ=True, workspace=ws, aux=bands)
         ws = out["workspace"]
     torch.cuda.synchronize()
     print("gated", int(Fuser.gated_count(out).item()))

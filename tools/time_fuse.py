@@ -39,12 +39,12 @@ def main():
         e[0].record()
         if args.bands:
             _o, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps,
-                                            FusionParams(), wl.dx, out=dv.masks, bands=bands)
+                                            FusionParams(), wl.dx, out=dv.masks, aux=bands)
         else:
             refine_masks_device(dv.raw_masks, dv.z_surface, dv.nsamps, out=dv.masks)
         e[1].record()
         out = fuser.run(wl.density, dv, probs=probs, occ=True, workspace=ws,
-                        bands=bands if args.bands else None)
+                        aux=bands if args.bands else None)
         ws = out["workspace"]
         e[2].record()
         torch.cuda.synchronize()
