@@ -678,10 +678,9 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
 }
 
 // Corner projections + footprint scan of one queued thin candidate.
-// Footprint box of a queued thin candidate (fusion.py:315-351): corner
-// projections (certified), reject / clip.  Returns false when no box.
-__device__ __forceinline__ bool thin_box(const FuseConst &C, const Cam &k, const QItem &q,
-                                         int &xs, int &ys, int &bw, int &bh) {
+__device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, const FuseMaps &M,
+                                          const Contrib &K, int view,
+                                          const QItem &q) {
     const uint32_t g = (uint32_t)C.g, gg = g * g;
     const uint32_t ix = q.vi / gg;
     const uint32_t rem = q.vi - ix * gg;
@@ -690,37 +689,62 @@ __device__ __forceinline__ bool thin_box(const FuseConst &C, const Cam &k, const
     const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
     const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
     const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
-    long long lxs, lxe, lys, lye;
-    if (!thin_bounds(C, k, xc0, xc1, xc2, q.x_d, q.xcam, q.ycam, lxs, lxe, lys, lye)) return false;
+    long long xs, xe, ys, ye;
+    if (!thin_bounds(C, k, xc0, xc1, xc2, q.x_d, q.xcam, q.ycam, xs, xe, ys, ye)) return;
     const long long wi = (long long)k.w, hi = (long long)k.h;
-    if (lxe < 0 || lxs > wi - 1 || lye < 0 || lys > hi - 1) return false;
-    if (lxs < 0) lxs = 0;
-    if (lys < 0) lys = 0;
-    if (lxe > wi - 1) lxe = wi - 1;
-    if (lye > hi - 1) lye = hi - 1;
-    xs = (int)lxs;
-    ys = (int)lys;
-    bw = (int)(lxe - lxs) + 1;
-    bh = (int)(lye - lys) + 1;
-    return true;
-}
-
-// Margin of the certified f32 support test (see the scan in fuse_pairs).
-__device__ __forceinline__ float support_margin(const FuseConst &C, double xd) {
-    return (float)(9.5367431640625e-07 * (fabs(xd) + C.tau_max));   // 2^-20
-}
-
-// The reference's exact support count of one box (fusion.py:355-367).
-__device__ __forceinline__ int exact_support(const FuseConst &C, const float4 *rp, int bw, int bh,
-                                             double xd) {
+    if (xe < 0 || xs > wi - 1 || ye < 0 || ys > hi - 1) return;
+    if (xs < 0) xs = 0;
+    if (ys < 0) ys = 0;
+    if (xe > wi - 1) xe = wi - 1;
+    if (ye > hi - 1) ye = hi - 1;
+#if defined(DIVAS_ABL) && DIVAS_ABL >= 1
+    K.t[(int64_t)view * C.cap + q.slot] = q.x_d + (double)(xe - xs);
+    return;
+#endif
+    // Footprint scan over the 16-byte records {m, D, tau32, n}.  m_max: f32
+    // widening is exact and monotone, so fmaxf in f32 equals the reference's
+    // f64 `if mv > m_max` (NaN never wins).  Support: the f32 margin test
+    // e = |f32(x_d) - D| - tau32 has |error| < 2^-22 (|x_d| + tau_max); beyond
+    // M = 2^-20 (|x_d| + tau_max) from 0 it decides the reference's f64 test
+    // |x_d - f64(D)| <= tau(n) exactly, inside M the f64 test runs.  Ineligible
+    // pixels (mask <= 0.5 or n == 0) carry tau32 = -1e30: never counted.
+    const float4 *__restrict__ rp = M.rec + (int64_t)view * C.hm * C.wm + ys * (int64_t)C.wm + xs;
+    const double xd = q.x_d;
+    const float xd32 = (float)xd;
+    const float Mg = (float)(9.5367431640625e-07 * (fabs(xd) + C.tau_max));   // 2^-20
+    const int bw = (int)(xe - xs) + 1;
+    const int npix = bw * ((int)(ye - ys) + 1);
     int sup = 0;
-    for (int r = 0; r < bh; ++r)
-        for (int c = 0; c < bw; ++c) {
-            const float4 v = __ldg(rp + (int64_t)r * C.wm + c);
-            sup += (v.z >= 0.0f && fabs(xd - (double)v.y) <= tau_thin(C, __float_as_int(v.w)))
+    float mmax = 0.0f;
+    bool unsure = false;
+    int col = 0, off = 0;
+#pragma unroll 4
+    for (int i = 0; i < npix; ++i) {
+        const float4 r = __ldg(rp + off + col);
+        mmax = fmaxf(mmax, r.x);
+        const float e = fabsf(xd32 - r.y) - r.z;
+        sup += (e <= -Mg) ? 1 : 0;
+        unsure |= fabsf(e) < Mg;
+        if (++col == bw) { col = 0; off += C.wm; }
+    }
+    if (unsure) {   // some pixel within the margin: recount with the reference's f64 test
+        sup = 0;
+        col = 0;
+        off = 0;
+        for (int i = 0; i < npix; ++i) {
+            const float4 r = __ldg(rp + off + col);
+            sup += (r.z >= 0.0f && fabs(xd - (double)r.y) <= tau_thin(C, __float_as_int(r.w)))
                        ? 1 : 0;
+            if (++col == bw) { col = 0; off += C.wm; }
         }
-    return sup;
+    }
+    const double m_max = (double)mmax;
+    const double p_cov = sup == 0 ? 0.0 : (double)sup / (double)npix;
+    const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
+    if (npix > 0 && t >= C.thin_accept) {
+        K.t[(int64_t)view * C.cap + q.slot] = t;
+        atomicOr(K.bits_thin + (int64_t)(view >> 5) * C.cap + q.slot, 1u << (view & 31));
+    }
 }
 
 #ifndef DIVAS_PAIR_MINB
@@ -731,11 +755,6 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
            FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
            const WsHeader *__restrict__ hdr) {
     __shared__ QItem s_q[kQueue];
-    __shared__ int4 s_box[kQueue];
-    __shared__ int s_rows[kQueue + 1];
-    __shared__ int s_sup[kQueue];
-    __shared__ unsigned s_mmax[kQueue];
-    __shared__ int s_unsure[kQueue];
     __shared__ int s_nq;
     if (threadIdx.x == 0) s_nq = 0;
     __syncthreads();
@@ -763,95 +782,9 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     base = __shfl_sync(0xffffffffu, base, 0);
     if (has) s_q[base + __popc(ball & ((1u << lane) - 1u))] = q;
     __syncthreads();
-    // phase B1: footprint boxes of the queued candidates, one thread each
+    // phase B: the queued candidates, densely packed onto the first warps
     const int nq = s_nq;
-    if (nq == 0) return;
-    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
-        int xs = 0, ys = 0, bw = 0, bh = 0;
-        if (!thin_box(C, k, s_q[i], xs, ys, bw, bh)) bw = bh = 0;
-        s_box[i] = make_int4(xs, ys, bw, bh);
-        s_rows[i] = bh;
-        s_sup[i] = 0;
-        s_mmax[i] = 0u;
-        s_unsure[i] = 0;
-    }
-    __syncthreads();
-    // B2: exclusive prefix sum of the row counts (one warp)
-    if (threadIdx.x < 32) {
-        int carry = 0;
-        for (int b0 = 0; b0 < nq; b0 += 32) {
-            const int i = b0 + lane;
-            const int v = i < nq ? s_rows[i] : 0;
-            int incl = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (i < nq) s_rows[i] = carry + incl - v;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (lane == 0) s_rows[nq] = carry;
-    }
-    __syncthreads();
-    // B3: every thread scans whole rows of the CTA's boxes.  Support (an
-    // integer count) and m_max (a maximum of non-negative f32 values, whose
-    // bit patterns order like the values) combine with shared-memory
-    // atomics: the result does not depend on the split.  m_max: f32 widening
-    // is exact and monotone, so fmaxf in f32 equals the reference's f64
-    // `if mv > m_max` (NaN never wins).  Support: the f32 margin test
-    // e = |f32(x_d) - D| - tau32 has |error| < 2^-22 (|x_d| + tau_max); beyond
-    // M = 2^-20 (|x_d| + tau_max) from 0 it decides the reference's f64 test
-    // |x_d - f64(D)| <= tau(n) exactly; an item with any pixel inside M is
-    // recounted exactly in B4.  Ineligible pixels (mask <= 0.5 or n == 0)
-    // carry tau32 = -1e30 and never count.
-    const int total_rows = s_rows[nq];
-    const float4 *__restrict__ vrec = M.rec + (int64_t)view * C.hm * C.wm;
-    for (int r = threadIdx.x; r < total_rows; r += blockDim.x) {
-        int lo = 0, hi = nq - 1;                      // item: last with s_rows[item] <= r
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_rows[mid] <= r) lo = mid; else hi = mid - 1;
-        }
-        const int item = lo;
-        const int4 b = s_box[item];
-        const double xd = s_q[item].x_d;
-        const float xd32 = (float)xd;
-        const float Mg = support_margin(C, xd);
-        const float4 *__restrict__ row =
-            vrec + (int64_t)(b.y + (r - s_rows[item])) * C.wm + b.x;
-        int sup = 0;
-        float mmax = 0.0f;
-        bool unsure = false;
-#pragma unroll 4
-        for (int c = 0; c < b.z; ++c) {
-            const float4 v = __ldg(row + c);
-            mmax = fmaxf(mmax, v.x);
-            const float e = fabsf(xd32 - v.y) - v.z;
-            sup += (e <= -Mg) ? 1 : 0;
-            unsure |= fabsf(e) < Mg;
-        }
-        if (sup) atomicAdd(&s_sup[item], sup);
-        if (mmax > 0.0f) atomicMax(&s_mmax[item], __float_as_uint(mmax));
-        if (unsure) s_unsure[item] = 1;
-    }
-    __syncthreads();
-    // B4: finalize each item (fusion.py:368-370, :482-484)
-    for (int i = threadIdx.x; i < nq; i += blockDim.x) {
-        const int4 b = s_box[i];
-        if (b.z == 0) continue;
-        const QItem &q = s_q[i];
-        int sup = s_sup[i];
-        if (s_unsure[i])
-            sup = exact_support(C, vrec + (int64_t)b.y * C.wm + b.x, b.z, b.w, q.x_d);
-        const int npix = b.z * b.w;
-        const double m_max = (double)__uint_as_float(s_mmax[i]);
-        const double p_cov = sup == 0 ? 0.0 : (double)sup / (double)npix;
-        const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
-        if (t >= C.thin_accept) {
-            K.t[(int64_t)view * C.cap + q.slot] = t;
-            atomicOr(K.bits_thin + (int64_t)(view >> 5) * C.cap + q.slot, 1u << (view & 31));
-        }
-    }
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) thin_item(C, k, M, K, view, s_q[i]);
 }
 
 // ---------------------------------------------------------------------------
