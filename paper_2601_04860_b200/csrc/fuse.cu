@@ -753,7 +753,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
 #define DIVAS_PAIR_MINB 4
 #endif
 #ifndef DIVAS_SPLIT
-#define DIVAS_SPLIT 1
+#define DIVAS_SPLIT 0
 #endif
 __global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
 fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
