@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define DIVAS_ABI_VERSION 4
+#define DIVAS_ABI_VERSION 5
 
 /* error codes */
 #define DIVAS_OK          0
@@ -147,10 +147,55 @@ const int64_t *divas_fuse_gated_count(const void *workspace);
 const int32_t *divas_fuse_overflow(const void *workspace);
 
 /* The f64 depth-gradient maps of fusion._gradient_maps on the padded planes
- * (divas_fuse computes g on the fly; this export is for parity tests). */
+ * (divas_fuse computes g on the fly; this export is for parity tests and for
+ * fusion.depth_gradient).  valid_only != 0: invalid pixels get 0 as in
+ * _gradient_map (fusion.py:232-240); 0: _grad_at at every pixel. */
 int divas_gradient_maps(int32_t nv, int32_t hm, int32_t wm, const float *dexps,
                         const float *dmins, const float *dmaxs, const int32_t *nsamps,
-                        double eps, double kappa, double *out, void *stream);
+                        double eps, double kappa, int32_t valid_only, double *out, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Per-pair decision trace: the reference's public per-pair operations      */
+/* thick_check / thin_check (fusion.py:549-646), which _fuse_traced          */
+/* (fusion.py:727-764) and fuse(trace_path=...) are built on.  Their        */
+/* arithmetic differs from the fused kernel's exactly where the reference's */
+/* does: _thick_pair receives Python floats (f64 at the d_min/d_max sites)  */
+/* and the gradient uses each view's true-size neighbourhood.  One record   */
+/* per query (point, rho, view), evaluated on the device.                   */
+/* ---------------------------------------------------------------------- */
+#define DIVAS_STAGE_FRUSTUM      0
+#define DIVAS_STAGE_NO_SURFACE   1
+#define DIVAS_STAGE_MASK_GATE    2
+#define DIVAS_STAGE_DENSITY_GATE 3
+#define DIVAS_STAGE_SPATIAL      4
+#define DIVAS_STAGE_DEPTH        5
+#define DIVAS_STAGE_PASSED       6
+
+typedef struct divas_pair_record {
+    int32_t stage;               /* thick_check stage (DIVAS_STAGE_*)         */
+    int32_t thin_candidate;      /* thin_check candidate flag                 */
+    double m, delta, g, tau_spatial, tau_depth, t_proj, t_clamped, x_d, mu_d, h_d, r, w_depth;
+    int64_t x_start, x_end, y_start, y_end, support_count, n_pixels;
+    double p_covered, m_max, t;
+} divas_pair_record;
+
+typedef struct divas_trace_args {
+    int32_t nv, hm, wm;          /* padded planes; true sizes from cams      */
+    const double *cams;          /* [nv][DIVAS_CAM_STRIDE]                    */
+    const float *masks, *dmins, *dmaxs, *dexps;
+    const int32_t *nsamps;       /* [nv][hm][wm]                              */
+    double pv[DIVAS_NPARAM];
+    double bc[3], bh[3];
+    int32_t unbounded;
+    double dx_vox;               /* voxel_size (the cube edge of thin_check)  */
+    int64_t n;                   /* queries                                   */
+    const double *points;        /* [n][3] voxel centres (world)              */
+    const double *rho;           /* [n] densities                             */
+    const int32_t *views;        /* [n] view index per query                  */
+    divas_pair_record *out;      /* [n]                                       */
+} divas_trace_args;
+
+int divas_pair_trace(const divas_trace_args *args, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Threshold / extract: occ[i] = p[i] >= thr;  idx = C-order indices of the */

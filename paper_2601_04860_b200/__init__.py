@@ -17,6 +17,8 @@ from .fusion import (DeviceViews, FusionParams, FusionStats, Fuser, OccupancyGri
                      threshold, threshold_device)
 
 from .incremental import FusionSession
+from .trace import (ThickPathDecision, ThinPathDecision, depth_gradient, depth_weight,
+                    thick_check, thin_check)
 
 __version__ = "0.1.0"
 
@@ -26,4 +28,6 @@ __all__ = [
     "DeviceViews", "FusionParams", "FusionStats", "Fuser", "OccupancyGrid",
     "fuse", "fuse_with_stats", "refine_and_fuse", "project_grid_overlay",
     "threshold", "threshold_device", "extract", "extract_device", "FusionSession",
+    "ThickPathDecision", "ThinPathDecision", "depth_gradient", "depth_weight", "thick_check",
+    "thin_check",
 ]

@@ -23,7 +23,7 @@ EXPORTS = (
     "divas_refine_bands",
     "divas_fuse_workspace_size", "divas_fuse", "divas_gate_count", "divas_fuse_gated_count",
     "divas_fuse_overflow",
-    "divas_gradient_maps",
+    "divas_gradient_maps", "divas_pair_trace",
     "divas_threshold_workspace_size", "divas_threshold",
     "divas_overlay",
     "divas_last_error", "divas_abi_version",
@@ -71,7 +71,9 @@ def _declare(lib):
         "divas_gate_count": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, _VP]),
         "divas_fuse_gated_count": (_VP, [_VP]),
         "divas_fuse_overflow": (_VP, [_VP]),
-        "divas_gradient_maps": (ctypes.c_int, [I32, I32, I32, _VP, _VP, _VP, _VP, D, D, _VP, _VP]),
+        "divas_gradient_maps": (ctypes.c_int, [I32, I32, I32, _VP, _VP, _VP, _VP, D, D, I32, _VP,
+                                               _VP]),
+        "divas_pair_trace": (ctypes.c_int, [_VP, _VP]),
         "divas_threshold_workspace_size": (S, [I64]),
         "divas_threshold": (ctypes.c_int, [_VP, I64, D, I64, _VP, _VP, _VP, _VP, S, _VP]),
         "divas_overlay": (ctypes.c_int, [_VP, I32, I32, _VP, _VP, _VP, _VP, I64,

@@ -35,6 +35,7 @@
 // (the TU is compiled with -fmad=false; explicit fma() appears only inside the
 // certified approximations), binary32 exactly at the 8 numba f32 sites.
 #include <algorithm>
+#include <cstring>
 
 #include "bands.cuh"
 
@@ -909,7 +910,7 @@ __global__ void gradient_maps_kernel(int nv, int hm, int wm, const float *__rest
                                      const float *__restrict__ dmins,
                                      const float *__restrict__ dmaxs,
                                      const int32_t *__restrict__ nsamps, double eps, double kappa,
-                                     double *__restrict__ out) {
+                                     int valid_only, double *__restrict__ out) {
     const int64_t plane = (int64_t)hm * wm;
     const int64_t total = plane * nv;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
@@ -917,9 +918,169 @@ __global__ void gradient_maps_kernel(int nv, int hm, int wm, const float *__rest
         const int64_t v = i / plane;
         const int64_t r = i - v * plane;
         const int iy = (int)(r / wm), ix = (int)(r - (int64_t)iy * wm);
-        out[i] = nsamps[i] > 0 ? grad_at(dexps + v * plane, dmins + v * plane, dmaxs + v * plane,
-                                         hm, wm, ix, iy, eps, kappa)
-                               : 0.0;
+        out[i] = (!valid_only || nsamps[i] > 0)
+                     ? grad_at(dexps + v * plane, dmins + v * plane, dmaxs + v * plane, hm, wm, ix,
+                               iy, eps, kappa)
+                     : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// per-pair decision trace (thick_check / thin_check, fusion.py:549-646)
+// ---------------------------------------------------------------------------
+__global__ void pair_trace_kernel(divas_trace_args A, FuseConst C) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        divas_pair_record R;
+        memset(&R, 0, sizeof(R));
+        R.x_end = -1;
+        R.y_end = -1;
+        const int view = A.views[i];
+        Cam k;
+        load_cam(A.cams + (int64_t)view * kCamStride, k);
+        const double xc0 = A.points[3 * i], xc1 = A.points[3 * i + 1], xc2 = A.points[3 * i + 2];
+        const double rho = A.rho[i];
+        const int64_t plane = (int64_t)A.hm * A.wm;
+        const float *mk = A.masks + view * plane;
+        const float *dmn = A.dmins + view * plane;
+        const float *dmx = A.dmaxs + view * plane;
+        const float *dex = A.dexps + view * plane;
+        const int32_t *nsp = A.nsamps + view * plane;
+        const int W = (int)k.w, H = (int)k.h;
+        double u, v, x_d;
+        R.stage = DIVAS_STAGE_FRUSTUM;
+        const bool front = project_px(k, xc0, xc1, xc2, u, v, x_d);
+        bool pix_ok = front && !(u < 0.0 || u >= 1.0 || v < 0.0 || v >= 1.0);
+        long long px = 0, py = 0;
+        int32_t ns = 0;
+        double m = 0.0;
+        if (pix_ok) {
+            px = pixel_index(u, (long long)W);
+            py = pixel_index(v, (long long)H);
+            ns = nsp[py * A.wm + px];
+            if (ns <= 0) {
+                R.stage = DIVAS_STAGE_NO_SURFACE;
+                pix_ok = false;
+            } else {
+                m = (double)mk[py * A.wm + px];
+                R.m = m;
+                R.x_d = x_d;
+            }
+        }
+        if (pix_ok) {        // thick_check (fusion.py:571-603)
+            if (m < C.mask_thr) R.stage = DIVAS_STAGE_MASK_GATE;
+            else if (rho < C.rho_thr) R.stage = DIVAS_STAGE_DENSITY_GATE;
+            else {
+                // _grad_at on the view's own (true-size) arrays
+                const int64_t c = py * A.wm + px;
+                const float center = dex[c];
+                const float r32 = dmx[c] - dmn[c];                       // f32 site
+                const double rng = (double)r32 + C.eps;
+                double gmax = 0.0, sg;
+                if (px > 0) { sg = (double)fabsf(dex[c - 1] - center) / rng; if (sg > gmax) gmax = sg; }
+                if (px < W - 1) { sg = (double)fabsf(dex[c + 1] - center) / rng; if (sg > gmax) gmax = sg; }
+                if (py > 0) { sg = (double)fabsf(dex[c - A.wm] - center) / rng; if (sg > gmax) gmax = sg; }
+                if (py < H - 1) { sg = (double)fabsf(dex[c + A.wm] - center) / rng; if (sg > gmax) gmax = sg; }
+                double g = 1.0 / (1.0 + C.kappa * gmax);
+                if (g > 1.0 - C.eps) g = 1.0 - C.eps;
+                if (g < 0.0) g = 0.0;
+                // _thick_pair with Python floats: f64 at every site
+                const double dmin = (double)dmn[c], dmax = (double)dmx[c], dexp = (double)dex[c];
+                const double *Rm = k.r;
+                const double rx = (u * k.w - k.cx) / k.fx;
+                const double ry = (k.cy - v * k.h) / k.fy;
+                double ddx = Rm[0] * rx + Rm[1] * ry - Rm[2];
+                double ddy = Rm[3] * rx + Rm[4] * ry - Rm[5];
+                double ddz = Rm[6] * rx + Rm[7] * ry - Rm[8];
+                const double norm = sqrt(ddx * ddx + ddy * ddy + ddz * ddz);
+                ddx /= norm; ddy /= norm; ddz /= norm;
+                const double t_proj = ((xc0 - k.p0) * ddx + (xc1 - k.p1) * ddy + (xc2 - k.p2) * ddz);
+                double t_c = t_proj;
+                if (t_c < dmin) t_c = dmin;
+                else if (t_c > dmax) t_c = dmax;
+                double pcx = k.p0 + ddx * t_c, pcy = k.p1 + ddy * t_c, pcz = k.p2 + ddz * t_c;
+                if (C.unbounded != 0) {
+                    const double nx = (pcx - C.bc0) / C.bh0, ny = (pcy - C.bc1) / C.bh1,
+                                 nz = (pcz - C.bc2) / C.bh2;
+                    const double rr = sqrt(nx * nx + ny * ny + nz * nz);
+                    if (rr > 1.0) {
+                        const double sc = (2.0 - 1.0 / rr) / rr;
+                        pcx = C.bc0 + nx * sc * C.bh0;
+                        pcy = C.bc1 + ny * sc * C.bh1;
+                        pcz = C.bc2 + nz * sc * C.bh2;
+                    }
+                }
+                const double ex = xc0 - pcx, ey = xc1 - pcy, ez = xc2 - pcz;
+                const double delta = sqrt(ex * ex + ey * ey + ez * ez);
+                const double tau_sp = A.dx_vox * g + C.lam * (dmax - dmin);
+                double b = C.beta * (double)ns;
+                if (b > C.bmax) b = C.bmax;
+                const double tau_dp = (C.gamma + b) * A.dx_vox;
+                const bool ok = delta <= tau_sp && fabs(x_d - dexp) <= tau_dp;
+                const double mu = 0.5 * (dmin + dmax);
+                double hd = 0.5 * (dmax - dmin);
+                if (hd < C.eps) hd = C.eps;
+                const double r = fabs(t_c - mu) / hd;
+                R.delta = delta; R.g = g; R.tau_spatial = tau_sp; R.tau_depth = tau_dp;
+                R.t_proj = t_proj; R.t_clamped = t_c; R.mu_d = mu; R.h_d = hd; R.r = r;
+                R.w_depth = exp(-C.alpha1 * r * r);
+                R.stage = ok ? DIVAS_STAGE_PASSED
+                             : (delta > tau_sp ? DIVAS_STAGE_SPATIAL : DIVAS_STAGE_DEPTH);
+            }
+            // thin_check (fusion.py:618-646)
+            const double fmax = k.fx > k.fy ? k.fx : k.fy;
+            if (m > C.thin_floor && rho >= C.rho_thin && x_d > 0.0 && A.dx_vox * fmax / x_d >= 1.0) {
+                const double half = 0.5 * A.dx_vox;
+                double umn = 1e30, umx = -1e30, vmn = 1e30, vmx = -1e30;
+                bool okc = true;
+                for (int j = 0; j < 8 && okc; ++j) {
+                    const double sx = ((j & 1) == 0) ? -1.0 : 1.0;
+                    const double sy = ((j & 2) == 0) ? -1.0 : 1.0;
+                    const double sz = ((j & 4) == 0) ? -1.0 : 1.0;
+                    double cu, cv, cd;
+                    if (!project_px(k, xc0 + sx * half, xc1 + sy * half, xc2 + sz * half, cu, cv, cd)) {
+                        okc = false;
+                        break;
+                    }
+                    if (cu < umn) umn = cu;
+                    if (cu > umx) umx = cu;
+                    if (cv < vmn) vmn = cv;
+                    if (cv > vmx) vmx = cv;
+                }
+                if (okc) {
+                    long long xs = nb_floor_int(umn * k.w), xe = nb_floor_int(umx * k.w);
+                    long long ys = nb_floor_int(vmn * k.h), ye = nb_floor_int(vmx * k.h);
+                    if (!(xe < 0 || xs > W - 1 || ye < 0 || ys > H - 1)) {
+                        if (xs < 0) xs = 0;
+                        if (ys < 0) ys = 0;
+                        if (xe > W - 1) xe = W - 1;
+                        if (ye > H - 1) ye = H - 1;
+                        long long support = 0, npix = 0;
+                        double m_max = 0.0;
+                        for (long long yy = ys; yy <= ye; ++yy)
+                            for (long long xx = xs; xx <= xe; ++xx) {
+                                ++npix;
+                                const double mv = (double)mk[yy * A.wm + xx];
+                                if (mv > m_max) m_max = mv;
+                                const int32_t nn = nsp[yy * A.wm + xx];
+                                if (mv > 0.5 && nn > 0) {
+                                    double bb = C.beta * (double)nn;
+                                    if (bb > C.bmax) bb = C.bmax;
+                                    const double tau_d = (2.0 * C.gamma + bb) * A.dx_vox;
+                                    if (fabs(x_d - (double)dex[yy * A.wm + xx]) <= tau_d) ++support;
+                                }
+                            }
+                        const double p_cov = (double)support / (double)npix;
+                        R.thin_candidate = 1;
+                        R.x_start = xs; R.x_end = xe; R.y_start = ys; R.y_end = ye;
+                        R.support_count = support; R.n_pixels = npix;
+                        R.p_covered = p_cov; R.m_max = m_max;
+                        R.t = (p_cov >= C.thin_pct) ? m_max : p_cov;
+                    }
+                }
+            }
+        }
+        A.out[i] = R;
     }
 }
 
@@ -1168,7 +1329,8 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
 
 extern "C" int divas_gradient_maps(int32_t nv, int32_t hm, int32_t wm, const float *dexps,
                                    const float *dmins, const float *dmaxs, const int32_t *nsamps,
-                                   double eps, double kappa, double *out, void *stream) {
+                                   double eps, double kappa, int32_t valid_only, double *out,
+                                   void *stream) {
     if (nv < 1 || hm < 1 || wm < 1) { set_error("divas_gradient_maps: empty"); return DIVAS_EINVAL; }
     if (!dexps || !dmins || !dmaxs || !nsamps || !out) {
         set_error("divas_gradient_maps: null pointer");
@@ -1177,6 +1339,31 @@ extern "C" int divas_gradient_maps(int32_t nv, int32_t hm, int32_t wm, const flo
     const int64_t total = (int64_t)nv * hm * wm;
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
     gradient_maps_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
-        nv, hm, wm, dexps, dmins, dmaxs, nsamps, eps, kappa, out);
+        nv, hm, wm, dexps, dmins, dmaxs, nsamps, eps, kappa, valid_only, out);
     return check_launch("divas_gradient_maps");
+}
+
+extern "C" int divas_pair_trace(const divas_trace_args *a, void *stream) {
+    if (!a || a->nv < 1 || a->hm < 1 || a->wm < 1 || a->n < 0) {
+        set_error("divas_pair_trace: bad arguments");
+        return DIVAS_EINVAL;
+    }
+    if (a->n == 0) return DIVAS_OK;
+    if (!a->cams || !a->masks || !a->dmins || !a->dmaxs || !a->dexps || !a->nsamps ||
+        !a->points || !a->rho || !a->views || !a->out) {
+        set_error("divas_pair_trace: null pointer");
+        return DIVAS_EINVAL;
+    }
+    divas_fuse_args fa;
+    memset(&fa, 0, sizeof(fa));
+    for (int i = 0; i < DIVAS_NPARAM; ++i) fa.pv[i] = a->pv[i];
+    for (int i = 0; i < 3; ++i) { fa.bc[i] = a->bc[i]; fa.bh[i] = a->bh[i]; }
+    fa.unbounded = a->unbounded;
+    fa.dx_vox = a->dx_vox;
+    fa.nv = a->nv; fa.hm = a->hm; fa.wm = a->wm;
+    FuseConst C;
+    fill_const(C, &fa, 0);
+    const int64_t blocks = std::min<int64_t>((a->n + 127) / 128, (int64_t)sm_count() * 32);
+    pair_trace_kernel<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(*a, C);
+    return check_launch("divas_pair_trace");
 }

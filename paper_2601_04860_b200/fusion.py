@@ -30,12 +30,16 @@ import numpy as np
 
 from . import _native
 from ._device import as_device, device, empty
+from .trace import (ThickPathDecision, ThinPathDecision, depth_gradient, depth_weight,
+                    thick_check, thin_check)
 
 __all__ = [
     "FusionParams", "OccupancyGrid", "FusionStats", "DeviceViews", "Fuser",
     "fuse", "fuse_with_stats", "refine_and_fuse", "project_grid_overlay",
     "threshold", "extract", "threshold_device", "extract_device", "gradient_maps_device",
     "pack_cameras", "bounds_arrays",
+    "ThickPathDecision", "ThinPathDecision", "depth_gradient", "depth_weight", "thick_check",
+    "thin_check",
 ]
 
 
@@ -545,7 +549,7 @@ def gradient_maps_device(views: DeviceViews, eps: float, kappa: float, stream=No
     _native.check(lib.divas_gradient_maps(views.nv, views.hm, views.wm,
                                           _native.ptr(views.dexps), _native.ptr(views.dmins),
                                           _native.ptr(views.dmaxs), _native.ptr(views.nsamps),
-                                          float(eps), float(kappa), _native.ptr(out),
+                                          float(eps), float(kappa), 1, _native.ptr(out),
                                           _native.stream_handle(stream)), "divas_gradient_maps")
     return out
 

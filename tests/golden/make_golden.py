@@ -223,10 +223,116 @@ def make_scene():
     np.savez_compressed(os.path.join(OUT, "scene.npz"), **store)
 
 
+def _store_views(store, prefix, views):
+    store[f"{prefix}_nv"] = np.int64(len(views))
+    for i, (vg, m) in enumerate(views):
+        c = vg.camera
+        store[f"{prefix}_v{i}_intr"] = np.array([c.fx, c.fy, c.cx, c.cy, c.width, c.height],
+                                                dtype=np.float64)
+        store[f"{prefix}_v{i}_w2c"] = np.asarray(c.world_from_camera, dtype=np.float64)
+        for k in ("d_min", "d_max", "d_exp", "n_samples", "z_surface"):
+            store[f"{prefix}_v{i}_{k}"] = np.asarray(getattr(vg, k))
+        store[f"{prefix}_v{i}_mask"] = np.asarray(m.values, dtype=np.float32)
+
+
+def make_trace():
+    """thick_check / thin_check / depth_gradient / fuse(trace_path) of the
+    reference (test_fusion.py fixtures)."""
+    import json
+    import tempfile
+    from dataclasses import asdict
+    from divas.fusion import (FusionParams, depth_gradient, fuse, thick_check, thin_check)
+    from divas.geometry import Camera, SceneBounds, VoxelGrid, look_at
+    from divas.render import RenderConfig, ViewGeometry, render_view
+    from divas.scene import SceneModel, ScenePrimitive, bake_density_grid
+    from divas.segmenter import ConfidenceMask
+    bounds = SceneBounds((-4, -4, -4), (4, 4, 4))
+    INTR = dict(fx=96.0, fy=96.0, cx=32.0, cy=32.0, width=64, height=64)
+    CFG = RenderConfig(samples_per_ray=192, near=0.5, far=7.0)
+    store = {}
+
+    def small(sigma, g):
+        sphere = ScenePrimitive("sphere", {"center": (0, 0, -3.0), "radius": 0.8},
+                                density=sigma, color=(0.8, 0.2, 0.2), object_id=1)
+        scene = SceneModel((sphere,), bounds)
+        cams = [Camera(world_from_camera=np.eye(4), **INTR),
+                Camera(world_from_camera=look_at((3.0, 0.3, -3.0), (0, 0, -3.0)), **INTR)]
+        views = []
+        for c in cams:
+            vg = render_view(scene, c, CFG)
+            views.append((vg, ConfidenceMask(np.where(vg.valid, 0.9, 0.0).astype(np.float32),
+                                             refined=True)))
+        grid = VoxelGrid(g, 1.2, origin=(-1.2, -1.2, -4.2))
+        return scene, grid, bake_density_grid(scene, grid), views
+
+    # traced fuse (test_fusion.py:269-278)
+    scene, grid, dens, views = small(2.5, 8)
+    p = FusionParams()
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "t.jsonl")
+        og = fuse(grid, dens, views, p, bounds=scene.bounds, trace_path=path)
+        store["traced_lines"] = np.array(open(path).read().splitlines())
+    store["traced_probs"] = og.probs
+    store["traced_g"] = np.int64(8)
+    store["traced_density"] = np.asarray(dens.values, np.float32)
+    _store_views(store, "traced", views)
+    # thick_check cases (test_fusion.py:99-142) on small_instance(300, 16) view 0
+    scene, grid, dens, views = small(300.0, 16)
+    vg, mask = views[0]
+    dx = grid.voxel_size()
+    tau = (p.base_tolerance_multiplier + p.max_bonus) * dx
+    cases = [((0.0, 0.0, -2.2 - dx / 2), 300.0, p), ((0.0, 0.0, -2.2 - 10 * tau), 300.0, p),
+             ((0, 0, -2.25), 0.1, p), ((0, 0, -3.0), 2.0, FusionParams(per_sample_bonus=100.0,
+                                                                       max_bonus=3.0)),
+             ((0.05, -0.02, -2.21), 300.0, FusionParams(depth_range_factor=0.3)),
+             ((0.0, 0.0, 5.0), 300.0, p)]
+    recs = []
+    for i, (c, rho, pp) in enumerate(cases):
+        ok, dec = thick_check(np.asarray(c, float), dx, rho, vg, mask, pp, scene.bounds,
+                              voxel_index=(i, 0, 0), view_index=0)
+        tdec = thin_check(np.asarray(c, float), dx, rho, vg, mask, pp, voxel_index=(i, 0, 0))
+        recs.append(json.dumps({"ok": ok, "thick": asdict(dec), "thin": asdict(tdec),
+                                "center": list(map(float, c)), "rho": rho,
+                                "pv": pp.as_vector().tolist()}))
+    store["checks"] = np.array(recs)
+    store["checks_dx"] = np.float64(dx)
+    _store_views(store, "checks", [(vg, mask)])
+    # thin_check on the rod (test_fusion.py:145-167)
+    rod = ScenePrimitive("capsule", {"p0": (0, -1, -3.0), "p1": (0, 1, -3.0), "radius": 0.02},
+                         density=8.0, color=(0.9, 0.3, 0.1), object_id=1)
+    rvg = render_view(SceneModel((rod,), bounds), Camera(world_from_camera=np.eye(4), **INTR), CFG)
+    rmask = ConfidenceMask(np.where(rvg.valid, 0.95, 0.0).astype(np.float32), refined=True)
+    rrecs = []
+    for c, vox, rho in (((0, 0, -3.0), 0.04, 8.0), ((0.01, 0.3, -3.0), 0.04, 8.0),
+                        ((0, 0, -3.0), 0.04, 0.5), ((0.0, 0.0, -2.0), 0.2, 8.0)):
+        tdec = thin_check(np.asarray(c, float), vox, rho, rvg, rmask, p)
+        rrecs.append(json.dumps({"thin": asdict(tdec), "center": list(map(float, c)),
+                                 "voxel": vox, "rho": rho}))
+    store["rod"] = np.array(rrecs)
+    _store_views(store, "rod", [(rvg, rmask)])
+    # depth_gradient (test_fusion.py:34-58) on hand-built views
+    grads = []
+    for i, pix in enumerate(((4, 4), (0, 0), (7, 7), (5, 4), (2, 6))):
+        cam = Camera(fx=10.0, fy=10.0, cx=4.0, cy=4.0, width=8, height=8,
+                     world_from_camera=np.eye(4))
+        rng = np.random.default_rng(i)
+        dexp = (2.0 + rng.random((8, 8))).astype(np.float32)
+        dexp[:, 5:] = 200.0 if i == 0 else dexp[:, 5:]
+        n = np.full((8, 8), 20, np.int32)
+        n[0, 0] = 0
+        gv = ViewGeometry(cam, np.zeros((8, 8, 3), np.float32), np.full((8, 8), 1.0, np.float32),
+                          np.full((8, 8), 3.0, np.float32), dexp, n, dexp)
+        grads.append(depth_gradient(gv, pix))
+        store[f"grad{i}_dexp"] = dexp
+        store[f"grad{i}_n"] = n
+    store["grads"] = np.array(grads)
+    np.savez_compressed(os.path.join(OUT, "trace.npz"), **store)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", default="/root/reference/pkg")
-    ap.add_argument("--only", default="fuzz,refine,scene")
+    ap.add_argument("--only", default="fuzz,refine,scene,trace")
     args = ap.parse_args()
     ta = _import_reference(args.ref)
     todo = args.only.split(",")
@@ -234,6 +340,8 @@ def main():
         make_refine()
     if "scene" in todo:
         make_scene()
+    if "trace" in todo:
+        make_trace()
     if "fuzz" in todo:
         make_fuzz(ta)
 
