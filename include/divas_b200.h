@@ -22,6 +22,8 @@
  *   divas_threshold      <- `ogrid.probs >= threshold` + np.argwhere
  *                                                           ablation.py:109
  *   divas_overlay        <- fusion._overlay_kernel           fusion.py:771-843
+ *   divas_vgrid_payload  <- io.write_vgrid's transpose        io.py:59-69
+ *   divas_pair_trace     <- fusion.thick_check / thin_check   fusion.py:549-646
  */
 #ifndef DIVAS_B200_H
 #define DIVAS_B200_H
@@ -207,6 +209,10 @@ size_t divas_threshold_workspace_size(int64_t n);
 int divas_threshold(const double *p, int64_t n, double thr, int64_t g,
                     uint8_t *occ, int64_t *idx, int64_t *count,
                     void *workspace, size_t workspace_bytes, void *stream);
+
+/* .vgrid payload (io.write_vgrid, io.py:59-69): out[iz][iy][ix] =       */
+/* (float)p[ix][iy][iz] -- the file's x-fastest float32 order.              */
+int divas_vgrid_payload(const double *p, int64_t g, float *out, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Overlay: binary mask of pixels whose ray meets a voxel with p >= thr     */

@@ -25,7 +25,7 @@ EXPORTS = (
     "divas_fuse_overflow",
     "divas_gradient_maps", "divas_pair_trace",
     "divas_threshold_workspace_size", "divas_threshold",
-    "divas_overlay",
+    "divas_overlay", "divas_vgrid_payload",
     "divas_last_error", "divas_abi_version",
 )
 
@@ -79,6 +79,7 @@ def _declare(lib):
         "divas_overlay": (ctypes.c_int, [_VP, I32, I32, _VP, _VP, _VP, _VP, I64,
                                          ctypes.POINTER(D), D, ctypes.POINTER(D),
                                          ctypes.POINTER(D), I32, D, _VP, _VP]),
+        "divas_vgrid_payload": (ctypes.c_int, [_VP, I64, _VP, _VP]),
         "divas_last_error": (ctypes.c_char_p, []),
         "divas_abi_version": (ctypes.c_int, []),
     }

@@ -175,3 +175,32 @@ extern "C" int divas_threshold(const double *p, int64_t n, double thr, int64_t g
     thr_emit<<<(unsigned)nt, kThrThreads, 0, s>>>(occ_buf, n, g, tiles, idx);
     return check_launch("divas_threshold(emit)");
 }
+
+// ---------------------------------------------------------------------------
+// .vgrid payload: p [ix][iy][iz] f64 -> f32 in x-fastest order [iz][iy][ix]
+// (io.write_vgrid, /root/reference/pkg/src/divas/io.py:59-69).  32x32 tiles of
+// the (ix, iz) plane of one iy through shared memory: coalesced both ways.
+// ---------------------------------------------------------------------------
+namespace divas {
+__global__ void vgrid_transpose(const double *__restrict__ p, float *__restrict__ out, int64_t g) {
+    __shared__ float tile[32][33];
+    const int64_t iy = blockIdx.z;
+    const int64_t ix0 = (int64_t)blockIdx.y * 32, iz0 = (int64_t)blockIdx.x * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {      // read rows ix, columns iz
+        const int64_t ix = ix0 + r, iz = iz0 + threadIdx.x;
+        if (ix < g && iz < g) tile[r][threadIdx.x] = (float)p[(ix * g + iy) * g + iz];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {      // write rows iz, columns ix
+        const int64_t iz = iz0 + r, ix = ix0 + threadIdx.x;
+        if (ix < g && iz < g) out[(iz * g + iy) * g + ix] = tile[threadIdx.x][r];
+    }
+}
+}  // namespace divas
+
+extern "C" int divas_vgrid_payload(const double *p, int64_t g, float *out, void *stream) {
+    if (!p || !out || g < 1 || g > 65535) { set_error("divas_vgrid_payload: bad arguments"); return DIVAS_EINVAL; }
+    dim3 grid((unsigned)((g + 31) / 32), (unsigned)((g + 31) / 32), (unsigned)g);
+    divas::vgrid_transpose<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(p, out, g);
+    return check_launch("divas_vgrid_payload");
+}

@@ -169,6 +169,15 @@ def make_scene():
     dens = bake_density_grid(prof.scene, grid)
     probs = fuse(grid, dens, views, prof.fusion, bounds=prof.scene.bounds).probs
     _record(store, "sop", grid, dens, views, prof.fusion, prof.scene.bounds, probs)
+    import io as _io
+    from divas.io import write_fmap, write_vgrid
+    from divas.fusion import OccupancyGrid as _OG
+    buf = _io.BytesIO()
+    write_vgrid(buf, _OG(grid, probs), unbounded=prof.scene.bounds.unbounded)
+    store["sop_vgrid_bytes"] = np.frombuffer(buf.getvalue(), dtype=np.uint8)
+    buf = _io.BytesIO()
+    write_fmap(buf, views[0][0].d_exp)
+    store["sop_fmap_bytes"] = np.frombuffer(buf.getvalue(), dtype=np.uint8)
     store["sop_raw_masks"] = np.stack([r[0] for r in raw])
     store["sop_z"] = np.stack([r[1] for r in raw])
     store["sop_refined"] = np.stack([r[3] for r in raw])

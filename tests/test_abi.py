@@ -49,23 +49,38 @@ def test_sm100a_code_only(lib):
     assert "sm_100a" in out
 
 
-def test_struct_layout_matches_header(tmp_path):
-    prog = tmp_path / "layout.c"
-    fields = [f[0] for f in _native.FuseArgs._fields_]
-    body = "\n".join(f'printf("%zu\\n", offsetof(divas_fuse_args, {f}));' for f in fields)
+def _c_layout(tmp_path, cname, fields):
+    prog = tmp_path / f"layout_{cname}.c"
+    body = "\n".join(f'printf("%zu\\n", offsetof({cname}, {f}));' for f in fields)
     prog.write_text(f"""
 #include <stdio.h>
 #include <stddef.h>
 #include "divas_b200.h"
-int main(void) {{ printf("%zu\\n", sizeof(divas_fuse_args)); {body} return 0; }}
+int main(void) {{ printf("%zu\\n", sizeof({cname})); {body} return 0; }}
 """)
-    exe = tmp_path / "layout"
+    exe = tmp_path / f"layout_{cname}"
     subprocess.run(["gcc", "-I", os.path.dirname(HEADER), str(prog), "-o", str(exe)], check=True)
-    vals = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+    return [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
                                            check=True).stdout.split()]
-    assert vals[0] == ctypes.sizeof(_native.FuseArgs)
+
+
+@pytest.mark.parametrize("which", ["fuse", "trace", "record"])
+def test_struct_layout_matches_header(tmp_path, which):
+    from paper_2601_04860_b200 import trace
+    if which == "record":
+        names = list(trace.RECORD_DTYPE.names)
+        vals = _c_layout(tmp_path, "divas_pair_record", names)
+        assert vals[0] == trace.RECORD_DTYPE.itemsize
+        for f, off in zip(names, vals[1:]):
+            assert trace.RECORD_DTYPE.fields[f][1] == off, f
+        return
+    st, cname = ((_native.FuseArgs, "divas_fuse_args") if which == "fuse"
+                 else (trace._TraceArgs, "divas_trace_args"))
+    fields = [f[0] for f in st._fields_]
+    vals = _c_layout(tmp_path, cname, fields)
+    assert vals[0] == ctypes.sizeof(st)
     for f, off in zip(fields, vals[1:]):
-        assert getattr(_native.FuseArgs, f).offset == off, f
+        assert getattr(st, f).offset == off, f
 
 
 def test_invalid_arguments_rejected_without_gpu(lib):
