@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define DIVAS_ABI_VERSION 5
+#define DIVAS_ABI_VERSION 6
 
 /* error codes */
 #define DIVAS_OK          0
@@ -88,12 +88,20 @@ int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm,
 /* ---------------------------------------------------------------------- */
 /* Fusion                                                                   */
 /* ---------------------------------------------------------------------- */
-#define DIVAS_FUSE_FULL        0  /* gate + all views + reduce                  */
-#define DIVAS_FUSE_INCREMENTAL 1  /* views [view_lo, view_hi) only, then reduce
-                                     over all nv views.  Requires a previous
-                                     FULL call on the same workspace, density,
-                                     range, params and output buffers; the
-                                     other views' contributions are reused.    */
+/* `mode` of divas_fuse_args: 0 (DIVAS_FUSE_FULL) or an OR of steps.        */
+#define DIVAS_STEP_GATE        1  /* zero the outputs on [lo, hi), build the
+                                     gated-voxel list                          */
+#define DIVAS_STEP_CLEAR_ALL   2  /* zero every contribution bit              */
+#define DIVAS_STEP_CLEAR_VIEWS 4  /* zero the bits of views [view_lo, view_hi) */
+#define DIVAS_STEP_PAIRS       8  /* evaluate views [view_lo, view_hi)          */
+#define DIVAS_STEP_REDUCE     16  /* value-sorted sums over all nv views -> p  */
+#define DIVAS_FUSE_FULL        0  /* = GATE | CLEAR_ALL | PAIRS(all) | REDUCE  */
+#define DIVAS_FUSE_INCREMENTAL (DIVAS_STEP_CLEAR_VIEWS | DIVAS_STEP_PAIRS | DIVAS_STEP_REDUCE)
+/* Steps without GATE reuse the gated list, and steps without PAIRS the
+ * contributions, that earlier calls left in the same workspace (same density,
+ * range, params and output buffers).  Between calls the caller may edit the
+ * workspace regions (divas_fuse_ws_regions), e.g. to exchange contributions
+ * between ranks that evaluated different views (views-sharding). */
 
 typedef struct divas_fuse_args {
     int64_t g;                   /* grid resolution G (voxels per axis)       */
@@ -124,8 +132,9 @@ typedef struct divas_fuse_args {
     const void *bands;           /* for these views, pv and dx_vox; NULL: built
                                     in the workspace from masks/n/d_exp         */
     int32_t nv_cap;              /* views the workspace holds (>= nv; <= 0: nv) */
-    int32_t mode;                /* DIVAS_FUSE_FULL / DIVAS_FUSE_INCREMENTAL    */
-    int32_t view_lo, view_hi;    /* INCREMENTAL: views to (re)evaluate          */
+    int32_t mode;                /* DIVAS_FUSE_FULL or DIVAS_STEP_* flags       */
+    int32_t view_lo, view_hi;    /* views evaluated by PAIRS / cleared by
+                                    CLEAR_VIEWS (ignored by FULL)              */
 } divas_fuse_args;
 
 /* Workspace bytes for divas_fuse with slot capacity `max_gated`, `nv_cap`
@@ -147,6 +156,13 @@ int divas_gate_count(const divas_fuse_args *args, void *workspace, void *stream)
  * exceeded max_gated -- voxels past the capacity were then left at p = 0). */
 const int64_t *divas_fuse_gated_count(const void *workspace);
 const int32_t *divas_fuse_overflow(const void *workspace);
+
+/* Byte offsets of the workspace regions for (max_gated, nv_cap, hm, wm):
+ * out[0] gated-voxel list (u32 [cap]), out[1] thick bits, out[2] thin bits
+ * (u32 [ceil(nv_cap/32)][cap] each), out[3] w, out[4] m*w, out[5] t
+ * (f64 [nv_cap][cap] each), out[6] total size. */
+void divas_fuse_ws_regions(int64_t max_gated, int32_t nv_cap, int32_t hm, int32_t wm,
+                           size_t out[7]);
 
 /* The f64 depth-gradient maps of fusion._gradient_maps on the padded planes
  * (divas_fuse computes g on the fly; this export is for parity tests and for

@@ -22,7 +22,7 @@ EXPORTS = (
     "divas_refine_workspace_size", "divas_refine", "divas_records_size", "divas_bands_size",
     "divas_refine_bands",
     "divas_fuse_workspace_size", "divas_fuse", "divas_gate_count", "divas_fuse_gated_count",
-    "divas_fuse_overflow",
+    "divas_fuse_overflow", "divas_fuse_ws_regions",
     "divas_gradient_maps", "divas_pair_trace",
     "divas_threshold_workspace_size", "divas_threshold",
     "divas_overlay", "divas_vgrid_payload",
@@ -50,7 +50,8 @@ class FuseArgs(ctypes.Structure):
     ]
 
 FUSE_FULL = 0
-FUSE_INCREMENTAL = 1
+STEP_GATE, STEP_CLEAR_ALL, STEP_CLEAR_VIEWS, STEP_PAIRS, STEP_REDUCE = 1, 2, 4, 8, 16
+FUSE_INCREMENTAL = STEP_CLEAR_VIEWS | STEP_PAIRS | STEP_REDUCE
 
 
 _lib = None
@@ -71,6 +72,7 @@ def _declare(lib):
         "divas_gate_count": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, _VP]),
         "divas_fuse_gated_count": (_VP, [_VP]),
         "divas_fuse_overflow": (_VP, [_VP]),
+        "divas_fuse_ws_regions": (None, [I64, I32, I32, I32, ctypes.POINTER(S)]),
         "divas_gradient_maps": (ctypes.c_int, [I32, I32, I32, _VP, _VP, _VP, _VP, D, D, I32, _VP,
                                                _VP]),
         "divas_pair_trace": (ctypes.c_int, [_VP, _VP]),
@@ -102,6 +104,13 @@ def lib():
             _declare(handle)
             _lib = handle
     return _lib
+
+
+def ws_regions(cap, nv_cap, hm, wm):
+    """Byte offsets {work, bits_thick, bits_thin, w, mw, t, total} of a fuse workspace."""
+    out = (ctypes.c_size_t * 7)()
+    lib().divas_fuse_ws_regions(int(cap), int(nv_cap), int(hm), int(wm), out)
+    return dict(zip(("work", "bits_thick", "bits_thin", "w", "mw", "t", "total"), list(out)))
 
 
 def check(rc: int, what: str):

@@ -1258,13 +1258,15 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         set_error("divas_fuse: records and bands come together");
         return DIVAS_EINVAL;
     }
-    const bool incr = a->mode == DIVAS_FUSE_INCREMENTAL;
-    if (a->mode != DIVAS_FUSE_FULL && !incr) { set_error("divas_fuse: bad mode"); return DIVAS_EINVAL; }
+    const int steps = a->mode == DIVAS_FUSE_FULL
+                          ? (DIVAS_STEP_GATE | DIVAS_STEP_CLEAR_ALL | DIVAS_STEP_PAIRS | DIVAS_STEP_REDUCE)
+                          : a->mode;
+    if (steps & ~31) { set_error("divas_fuse: bad mode %d", a->mode); return DIVAS_EINVAL; }
     int v0 = 0, v1 = a->nv;
-    if (incr) {
+    if (a->mode != DIVAS_FUSE_FULL && (steps & (DIVAS_STEP_PAIRS | DIVAS_STEP_CLEAR_VIEWS))) {
         v0 = a->view_lo; v1 = a->view_hi;
         if (v0 < 0 || v1 > a->nv || v0 >= v1) {
-            set_error("divas_fuse: incremental views [%d, %d) outside [0, %d)", v0, v1, a->nv);
+            set_error("divas_fuse: views [%d, %d) outside [0, %d)", v0, v1, a->nv);
             return DIVAS_EINVAL;
         }
     }
@@ -1286,7 +1288,7 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     Contrib K{(uint32_t *)(ws + L.bits_thick), (uint32_t *)(ws + L.bits_thin),
               (double *)(ws + L.w), (double *)(ws + L.mw), (double *)(ws + L.t)};
     if (a->vox_hi == a->vox_lo) return DIVAS_OK;
-    if (!M.rec) {   // scan records + depth bands of the evaluated views (bands.cuh)
+    if (!M.rec && (steps & DIVAS_STEP_PAIRS)) {   // records + bands of the evaluated views
         float4 *rec = (float4 *)(ws + L.rec);
         double2 *bands = (double2 *)(ws + L.bands);
         launch_aux(a, v0, v1 - v0, rec, bands, s);
@@ -1294,37 +1296,55 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         M.rec = rec;
         M.bands = bands;
     }
-    if (!incr) {
-        if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess ||
-            cudaMemsetAsync(ws + L.bits_thick, 0, L.w - L.bits_thick, s) != cudaSuccess)
+    if (steps & DIVAS_STEP_GATE) {
+        if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess)
             return check_launch("divas_fuse(memset)");
         launch_gate(C, a->density, O, work, hdr, 0, s);
         if ((rc = check_launch("divas_fuse(gate)"))) return rc;
-    } else {
+    }
+    if (steps & DIVAS_STEP_CLEAR_ALL) {
+        if (cudaMemsetAsync(ws + L.bits_thick, 0, L.w - L.bits_thick, s) != cudaSuccess)
+            return check_launch("divas_fuse(memset bits)");
+    }
+    if (steps & DIVAS_STEP_CLEAR_VIEWS) {
         const int64_t blocks = std::min<int64_t>((cap + 255) / 256, (int64_t)sm_count() * 8);
         clear_view_bits<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(K, cap, v0, v1, hdr);
         if ((rc = check_launch("divas_fuse(clear)"))) return rc;
     }
-    const int64_t cap_blocks = (cap + kPairThreads - 1) / kPairThreads;
-    if (cap_blocks > 0x7fffffffLL) { set_error("divas_fuse: too many slots"); return DIVAS_EINVAL; }
-    C.view0 = v0;
-    uint4 *tq = (uint4 *)(ws + L.tq);
-    if (cudaMemsetAsync(&hdr->nthin, 0, sizeof(unsigned long long), s) != cudaSuccess)
-        return check_launch("divas_fuse(memset queue)");
-    fuse_pairs<<<dim3((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)(v1 - v0)),
-                 kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr, hdr, tq);
-    if ((rc = check_launch("divas_fuse(pairs)"))) return rc;
+    if (steps & DIVAS_STEP_PAIRS) {
+        const int64_t cap_blocks = (cap + kPairThreads - 1) / kPairThreads;
+        if (cap_blocks > 0x7fffffffLL) { set_error("divas_fuse: too many slots"); return DIVAS_EINVAL; }
+        C.view0 = v0;
+        uint4 *tq = (uint4 *)(ws + L.tq);
+        if (cudaMemsetAsync(&hdr->nthin, 0, sizeof(unsigned long long), s) != cudaSuccess)
+            return check_launch("divas_fuse(memset queue)");
+        fuse_pairs<<<dim3((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)(v1 - v0)),
+                     kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr, hdr, tq);
+        if ((rc = check_launch("divas_fuse(pairs)"))) return rc;
 #if DIVAS_SPLIT
-    fuse_thin<<<(unsigned)(sm_count() * 16), kThinThreads, 0, s>>>(C, a->cams, M, K, tq, hdr);
-    if ((rc = check_launch("divas_fuse(thin)"))) return rc;
+        fuse_thin<<<(unsigned)(sm_count() * 16), kThinThreads, 0, s>>>(C, a->cams, M, K, tq, hdr);
+        if ((rc = check_launch("divas_fuse(thin)"))) return rc;
 #endif
-    const unsigned rblocks = (unsigned)std::max<int64_t>((cap + kReduceThreads - 1) / kReduceThreads, 1);
-    if (a->nv <= 32) fuse_reduce<32><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
-    else if (a->nv <= 64) fuse_reduce<64><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
-    else if (a->nv <= 128) fuse_reduce<128><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
-    else if (a->nv <= 256) fuse_reduce<256><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
-    else fuse_reduce<1024><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
-    return check_launch("divas_fuse(reduce)");
+    }
+    if (steps & DIVAS_STEP_REDUCE) {
+        const unsigned rblocks =
+            (unsigned)std::max<int64_t>((cap + kReduceThreads - 1) / kReduceThreads, 1);
+        if (a->nv <= 32) fuse_reduce<32><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+        else if (a->nv <= 64) fuse_reduce<64><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+        else if (a->nv <= 128) fuse_reduce<128><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+        else if (a->nv <= 256) fuse_reduce<256><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+        else fuse_reduce<1024><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+        if ((rc = check_launch("divas_fuse(reduce)"))) return rc;
+    }
+    return DIVAS_OK;
+}
+
+extern "C" void divas_fuse_ws_regions(int64_t max_gated, int32_t nv_cap, int32_t hm, int32_t wm,
+                                      size_t out[7]) {
+    const WsLayout L = ws_layout(max_gated, nv_cap > 0 ? nv_cap : 1, hm > 0 ? hm : 1,
+                                 wm > 0 ? wm : 1);
+    out[0] = L.work; out[1] = L.bits_thick; out[2] = L.bits_thin;
+    out[3] = L.w; out[4] = L.mw; out[5] = L.t; out[6] = L.total;
 }
 
 extern "C" int divas_gradient_maps(int32_t nv, int32_t hm, int32_t wm, const float *dexps,

@@ -324,12 +324,13 @@ class Fuser:
 
     def run(self, density, views: DeviceViews, probs=None, stats=False, occ=False,
             occ_thr=0.5, vox_range=None, workspace=None, stream=None, max_gated=None,
-            aux=None, nv_cap=None, incremental=None):
+            aux=None, nv_cap=None, incremental=None, steps=None, view_range=None):
         """Enqueue ``divas_fuse``.  ``aux``: ViewAux from ``refine_bands_device``
         (else built in the workspace).  ``incremental=(v0, v1)``: re-evaluate
         only views [v0, v1) against the state a previous full ``run`` left in
         ``workspace`` (same density, range, params and output buffers) --
-        ``nv_cap`` sizes that workspace for views added later."""
+        ``nv_cap`` sizes that workspace for views added later.  ``steps``:
+        explicit ``_native.STEP_*`` flags with ``view_range`` (views-sharding)."""
         import ctypes
         import torch
         g = self.g
@@ -378,6 +379,11 @@ class Fuser:
         if incremental is not None:
             a.mode = _native.FUSE_INCREMENTAL
             a.view_lo, a.view_hi = int(incremental[0]), int(incremental[1])
+        elif steps is not None:
+            a.mode = int(steps)
+            v0, v1 = view_range if view_range is not None else (0, views.nv)
+            a.view_lo, a.view_hi = int(v0), int(v1)
+        out["cap"], out["nv_cap"] = cap, nvc
         _native.check(lib.divas_fuse(ctypes.byref(a), _native.ptr(workspace), wsb,
                                      _native.stream_handle(stream)), "divas_fuse")
         return out

@@ -26,7 +26,8 @@ from __future__ import annotations
 import numpy as np
 
 __all__ = ["slice_weights", "balanced_slabs", "equal_slabs", "slab_voxel_range",
-           "broadcast_views", "gather_occupancy", "gather_slab_values"]
+           "broadcast_views", "gather_occupancy", "gather_slab_values",
+           "view_blocks", "ViewShardPlan"]
 
 # relative cost of one voxel in the dense gate pass vs one gated voxel-view pair
 STREAM_WEIGHT = 0.02
@@ -127,3 +128,52 @@ def gather_occupancy(occ_slab, slabs, g: int, rank: int, group=None):
 def gather_slab_values(vals_slab, slabs, g: int, rank: int, group=None):
     """Full (G^3,) grid of any dtype from per-rank slabs (e.g. f64 probs, on demand)."""
     return _gather_padded(vals_slab, slabs, g, rank, group)
+
+
+# ---------------------------------------------------------------------------
+# views-sharding (the north star's measured alternative to slabs)
+# ---------------------------------------------------------------------------
+
+def view_blocks(nv: int, n: int):
+    """Rank r evaluates views [r*R, min((r+1)*R, nv)), R = ceil(nv / n)."""
+    rr = -(-nv // n)
+    return [(min(r * rr, nv), min((r + 1) * rr, nv)) for r in range(n)], rr
+
+
+class ViewShardPlan:
+    """Exchange plan for views-sharding over a fuse workspace.
+
+    Every rank fuses the WHOLE grid for its block of views.  Exactness needs
+    the same slot order everywhere, so rank 0's gated-voxel list is
+    broadcast after the GATE step.  After the PAIRS step each rank's
+    contribution rows ([view][slot] f64 arrays w, m*w, t) are all-gathered in
+    place -- rank r's rows are the r-th block of R rows -- and the presence
+    bits are summed: ranks set disjoint bits, so the sum is their OR.  Every
+    rank then runs the REDUCE step and holds the full p.
+    Bytes exchanged: 3 * 8 * R * N * cap + 8 * ceil(nv/32) * cap.
+    """
+
+    def __init__(self, nv, world, cap, hm, wm):
+        from . import _native
+        self.blocks, self.rows = view_blocks(nv, world)
+        self.nv_cap = self.rows * world
+        self.cap = int(cap)
+        self.reg = _native.ws_regions(self.cap, self.nv_cap, hm, wm)
+
+    def broadcast_gated(self, workspace, src=0, group=None):
+        import torch.distributed as dist
+        dist.broadcast(workspace[:8], src=src, group=group)              # gated count
+        w0 = self.reg["work"]
+        dist.broadcast(workspace[w0: w0 + 4 * self.cap], src=src, group=group)
+
+    def exchange(self, workspace, rank, group=None):
+        import torch
+        import torch.distributed as dist
+        rb = self.rows * self.cap * 8                                    # bytes per rank block
+        for k in ("w", "mw", "t"):
+            o = self.reg[k]
+            full = workspace[o: o + rb * len(self.blocks)]
+            dist.all_gather_into_tensor(full, full[rank * rb:(rank + 1) * rb], group=group)
+        b0, b1 = self.reg["bits_thick"], self.reg["w"]
+        bits = workspace[b0:b1].view(torch.int32)
+        dist.all_reduce(bits, op=dist.ReduceOp.SUM, group=group)
