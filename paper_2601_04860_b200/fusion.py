@@ -383,7 +383,6 @@ class Fuser:
             a.mode = int(steps)
             v0, v1 = view_range if view_range is not None else (0, views.nv)
             a.view_lo, a.view_hi = int(v0), int(v1)
-        out["cap"], out["nv_cap"] = cap, nvc
         _native.check(lib.divas_fuse(ctypes.byref(a), _native.ptr(workspace), wsb,
                                      _native.stream_handle(stream)), "divas_fuse")
         return out
