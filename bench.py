@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--slabs", default="balanced", choices=["balanced", "equal"])
+    ap.add_argument("--shard", default="slabs", choices=["slabs", "views"],
+                    help="N>1 decomposition: voxel slabs (default) or view blocks")
     return ap.parse_args()
 
 
@@ -319,35 +321,64 @@ def run_ours(args):
     grid = type("G", (), {"resolution": g, "origin": wl.origin, "voxel_size": lambda s=None: wl.dx})()
     fuser = Fuser(grid, params)
 
-    # --- slabs ------------------------------------------------------------------
+    # --- decomposition ----------------------------------------------------------
+    from paper_2601_04860_b200 import _native
+    from paper_2601_04860_b200.segmenter import ViewAux
     if args.slabs == "balanced":
         slabs = sharding.balanced_slabs(sharding.slice_weights(wl.density.reshape(g, g, g), pv, nv),
                                         world)
     else:
         slabs = sharding.equal_slabs(g, world)
+    views_mode = args.shard == "views" and world > 1
+    if views_mode:
+        slabs = [(0, g)] * world
     lo, hi = sharding.slab_voxel_range(slabs[rank], g)
     probs = torch.empty(g ** 3, dtype=torch.float64, device=dev)
+    occ_buf = torch.empty(g ** 3, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     ws = None
     bands = None
     cap = fuser.capacity(wl.density, lo, hi)      # one counting pass + sync, outside the loop
     stream = torch.cuda.current_stream()
+    H, W = wl.shape[1], wl.shape[2]
+    if views_mode:
+        plan = sharding.ViewShardPlan(nv, world, cap, H, W)
+        v0, v1 = plan.blocks[rank]
+        bands = ViewAux.empty(nv, H, W, dev)
+        ws = torch.empty(_native.ws_regions(cap, plan.nv_cap, H, W)["total"], dtype=torch.uint8,
+                         device=dev)
 
     def step(ev=None):
         nonlocal ws, bands
         if ev is not None:
             ev[0].record(stream)
-        _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps, params,
-                                        wl.dx, aux=bands, planar=False)
+        if views_mode:
+            if v1 > v0:
+                refine_bands_device(dv.raw_masks[v0:v1], dv.z_surface[v0:v1], dv.nsamps[v0:v1],
+                                    dv.dexps[v0:v1], params, wl.dx,
+                                    aux=bands.view_slices(v0, v1, nv, H, W), planar=False)
+        else:
+            _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps,
+                                            params, wl.dx, aux=bands, planar=False)
         if ev is not None:
             ev[1].record(stream)
-        out = fuser.run(wl.density, dv, probs=probs, occ=True, vox_range=(lo, hi), workspace=ws,
-                        aux=bands, max_gated=cap)
+        if views_mode:
+            kw = dict(probs=probs, occ=occ_buf, workspace=ws, max_gated=cap, aux=bands,
+                      nv_cap=plan.nv_cap)
+            out = fuser.run(wl.density, dv, steps=_native.STEP_GATE, **kw)
+            plan.broadcast_gated(ws)
+            pairs = _native.STEP_CLEAR_ALL | (_native.STEP_PAIRS if v1 > v0 else 0)
+            fuser.run(wl.density, dv, steps=pairs, view_range=(v0, max(v1, v0 + 1)), **kw)
+            plan.exchange(ws, rank)
+            out = fuser.run(wl.density, dv, steps=_native.STEP_REDUCE, **kw)
+        else:
+            out = fuser.run(wl.density, dv, probs=probs, occ=occ_buf, vox_range=(lo, hi),
+                            workspace=ws, aux=bands, max_gated=cap)
         ws = out["workspace"]
         if ev is not None:
             ev[2].record(stream)
         occ_full = None
-        if world > 1:
+        if world > 1 and not views_mode:
             occ_full = sharding.gather_occupancy(out["occ"][lo:hi], slabs, g, rank)
         if ev is not None:
             ev[3].record(stream)
@@ -445,10 +476,13 @@ def run_ours(args):
         "latency_ms": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIG_DESC[args.config], "grid": g, "views": nv,
-                   "width": W, "height": H, "parallelism": f"slab x{world}" if world > 1 else "1 GPU",
+                   "width": W, "height": H,
+                   "parallelism": (f"{args.shard} x{world}" if world > 1 else "1 GPU"),
                    "slabs": slabs, "slab_policy": args.slabs,
-                   "step": "refine+bands(all views) + fuse(slab, threshold fused)"
-                           + (" + all-gather(occupancy)" if world > 1 else ""),
+                   "step": ("refine+aux(own views) + gate + bcast(gated list) + pairs(own views)"
+                            " + all-gather(contributions) + reduce" if views_mode else
+                            "refine+aux(all views) + fuse(slab, threshold fused)"
+                            + (" + all-gather(occupancy)" if world > 1 else "")),
                    "l2": "flushed (256 MiB write) between steps, outside the events",
                    "params": "FusionParams() defaults"},
         "breakdown_ms": {"refine": refine_ms, "fuse": fuse_ms, "gather": float(np.mean(t_gath)),
