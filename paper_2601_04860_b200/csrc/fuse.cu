@@ -459,12 +459,19 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     const double Rv = k.fy * rho * (x_d + fabs(ycam)) * inv + 2.0;
     const double fx0 = floor((Uc - Ru) * (1.0 / kBandTile)), fx1 = floor((Uc + Ru) * (1.0 / kBandTile));
     const double fy0 = floor((Vc - Rv) * (1.0 / kBandTile)), fy1 = floor((Vc + Rv) * (1.0 / kBandTile));
+    if (Ru <= (double)kBandTile && Rv <= (double)kBandTile && Uc >= 0.0 && Vc >= 0.0 &&
+        Uc < (double)C.wm && Vc < (double)C.hm) {
+        // the box lies in the 3x3 tile neighbourhood of the centre pixel's tile
+        const int cx = (int)(Uc * (1.0 / kBandTile)), cy = (int)(Vc * (1.0 / kBandTile));
+        const double2 d = M.bands[((int64_t)(2 * view + 1) * C.nty + cy) * C.ntx + cx];
+        if (!(x_d >= d.x && x_d <= d.y)) return true;
+    }
     const int tx0 = (int)fmax(fx0, 0.0), tx1 = (int)fmin(fx1, (double)(C.ntx - 1));
     const int ty0 = (int)fmax(fy0, 0.0), ty1 = (int)fmin(fy1, (double)(C.nty - 1));
     if (tx1 < tx0 || ty1 < ty0) return false;
     if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16) return false;
     double lo = 1e300, hi = -1e300;
-    const double2 *bv = M.bands + (int64_t)view * C.nty * C.ntx;
+    const double2 *bv = M.bands + (int64_t)view * 2 * C.nty * C.ntx;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
             const double2 b = bv[ty * C.ntx + tx];
@@ -1179,7 +1186,7 @@ static void launch_aux(const divas_fuse_args *a, int v0, int cnt, float4 *rec, d
     const int32_t *n = a->nsamps + v0 * plane;
     const float *d = a->dexps + v0 * plane;
     float4 *r = rec + v0 * plane;
-    double2 *b = bands + (int64_t)v0 * B.nty * B.ntx;
+    double2 *b = bands + (int64_t)v0 * 2 * B.nty * B.ntx;
     const bool vec = (a->wm % 4 == 0) &&
                      ((((uintptr_t)m) | ((uintptr_t)n) | ((uintptr_t)d)) & 15) == 0;
     if (vec) {
@@ -1189,6 +1196,7 @@ static void launch_aux(const divas_fuse_args *a, int v0, int cnt, float4 *rec, d
         dim3 bg((unsigned)((a->wm + 255) / 256), (unsigned)B.nty, (unsigned)cnt);
         band_pass<1, false><<<bg, 256, 0, s>>>(B, m, nullptr, n, d, nullptr, nullptr, b, r, cnt);
     }
+    launch_dilate(b, cnt, a->hm, a->wm, s);
 }
 
 }  // namespace divas
