@@ -39,8 +39,8 @@ def nvcc() -> str:
 
 
 def _deps(src):
-    return [os.path.join(CSRC, src), os.path.join(CSRC, "common.cuh"),
-            os.path.join(INCLUDE, "divas_b200.h")]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    return [os.path.join(CSRC, src), os.path.join(INCLUDE, "divas_b200.h"), *headers]
 
 
 def _stale(target, deps):
