@@ -4,10 +4,11 @@
 //   mask_p > 0.5 && n_p > 0 && |fl(x_d - D_p)| <= tau(n_p)          (fusion.py:361-367)
 // which implies  D_p - tau(1 + 2^-52) <= x_d <= D_p + tau(1 + 2^-52).  A tile's
 // band is the hull of those intervals over its eligible pixels, widened by a
-// 1e-12 relative margin that dominates every rounding involved.  If x_d lies
-// outside the bands of all tiles that can contain the footprint box, support
-// is exactly 0, so p_cov = 0 and (for thin_percent_cover > 0) t = 0 < thin_accept:
-// the pair cannot vote and needs neither corner projections nor a scan.
+// 1e-12 relative margin that dominates every rounding involved.  A supporting
+// pixel's interval lies inside its own tile's band, so if x_d lies outside the
+// band of EVERY tile that can contain the footprint box, support is exactly 0,
+// p_cov = 0 and (for thin_percent_cover > 0) t = 0 < thin_accept: the pair
+// cannot vote and needs neither corner projections nor a scan.
 #pragma once
 
 #include "common.cuh"
@@ -112,31 +113,7 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
     }
     if (active && (threadIdx.x % TPW) == 0) {
         const int tx = x0 / kBandTile;
-        bands[((int64_t)v * 2 * B.nty + blockIdx.y) * B.ntx + tx] = make_double2(lo, hi);
-    }
-}
-
-// Dilated bands: the hull of each tile's 3x3 tile neighbourhood.  Per view the
-// band buffer holds the plain tile plane followed by the dilated one.  A
-// footprint box within 8 px of a pixel lies inside the 3x3 neighbourhood of
-// that pixel's tile, so one lookup bounds its support.
-static __global__ void band_dilate(double2 *__restrict__ bands, int nv, int nty, int ntx) {
-    const int64_t T = (int64_t)nty * ntx;
-    const int64_t total = (int64_t)nv * T;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = i / T;
-        const int r = (int)(i - v * T);
-        const int ty = r / ntx, tx = r - ty * ntx;
-        const double2 *src = bands + v * 2 * T;
-        double lo = __longlong_as_double(0x7ff0000000000000LL), hi = -lo;
-        for (int y = max(ty - 1, 0); y <= min(ty + 1, nty - 1); ++y)
-            for (int x = max(tx - 1, 0); x <= min(tx + 1, ntx - 1); ++x) {
-                const double2 b = src[(int64_t)y * ntx + x];
-                lo = fmin(lo, b.x);
-                hi = fmax(hi, b.y);
-            }
-        bands[v * 2 * T + T + r] = make_double2(lo, hi);
+        bands[((int64_t)v * B.nty + blockIdx.y) * B.ntx + tx] = make_double2(lo, hi);
     }
 }
 
@@ -149,17 +126,9 @@ inline BandParams band_params(const double *pv, double dx, int hm, int wm) {
     return B;
 }
 
-// per view: plain tile bands, then the dilated ones
 inline size_t band_bytes(int nv, int hm, int wm) {
-    return (size_t)nv * 2 * ((hm + kBandTile - 1) / kBandTile) *
-           ((wm + kBandTile - 1) / kBandTile) * sizeof(double2);
-}
-
-inline void launch_dilate(double2 *bands, int nv, int hm, int wm, cudaStream_t s) {
-    const int nty = (hm + kBandTile - 1) / kBandTile, ntx = (wm + kBandTile - 1) / kBandTile;
-    const int64_t total = (int64_t)nv * nty * ntx;
-    const int64_t blocks = total < 148 * 64 * 256 ? (total + 255) / 256 : 148 * 64;
-    band_dilate<<<(unsigned)(blocks > 0 ? blocks : 1), 256, 0, s>>>(bands, nv, nty, ntx);
+    return (size_t)nv * ((hm + kBandTile - 1) / kBandTile) * ((wm + kBandTile - 1) / kBandTile) *
+           sizeof(double2);
 }
 
 inline size_t record_bytes(int nv, int hm, int wm) { return (size_t)nv * hm * wm * sizeof(float4); }

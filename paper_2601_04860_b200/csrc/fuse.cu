@@ -459,26 +459,22 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     const double Rv = k.fy * rho * (x_d + fabs(ycam)) * inv + 2.0;
     const double fx0 = floor((Uc - Ru) * (1.0 / kBandTile)), fx1 = floor((Uc + Ru) * (1.0 / kBandTile));
     const double fy0 = floor((Vc - Rv) * (1.0 / kBandTile)), fy1 = floor((Vc + Rv) * (1.0 / kBandTile));
-    if (Ru <= (double)kBandTile && Rv <= (double)kBandTile && Uc >= 0.0 && Vc >= 0.0 &&
-        Uc < (double)C.wm && Vc < (double)C.hm) {
-        // the box lies in the 3x3 tile neighbourhood of the centre pixel's tile
-        const int cx = (int)(Uc * (1.0 / kBandTile)), cy = (int)(Vc * (1.0 / kBandTile));
-        const double2 d = M.bands[((int64_t)(2 * view + 1) * C.nty + cy) * C.ntx + cx];
-        if (!(x_d >= d.x && x_d <= d.y)) return true;
-    }
     const int tx0 = (int)fmax(fx0, 0.0), tx1 = (int)fmin(fx1, (double)(C.ntx - 1));
     const int ty0 = (int)fmax(fy0, 0.0), ty1 = (int)fmin(fy1, (double)(C.nty - 1));
     if (tx1 < tx0 || ty1 < ty0) return false;
     if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16) return false;
-    double lo = 1e300, hi = -1e300;
-    const double2 *bv = M.bands + (int64_t)view * 2 * C.nty * C.ntx;
+    const double2 *bv = M.bands + (int64_t)view * C.nty * C.ntx;
+    // the centre pixel's tile first: the likeliest to contain x_d
+    const int cx = (int)fmin(fmax(floor(Uc * (1.0 / kBandTile)), (double)tx0), (double)tx1);
+    const int cy = (int)fmin(fmax(floor(Vc * (1.0 / kBandTile)), (double)ty0), (double)ty1);
+    const double2 c = bv[cy * C.ntx + cx];
+    if (x_d >= c.x && x_d <= c.y) return false;
     for (int ty = ty0; ty <= ty1; ++ty)
         for (int tx = tx0; tx <= tx1; ++tx) {
             const double2 b = bv[ty * C.ntx + tx];
-            lo = fmin(lo, b.x);
-            hi = fmax(hi, b.y);
+            if (x_d >= b.x && x_d <= b.y) return false;   // a pixel of this tile may support
         }
-    return !(x_d >= lo && x_d <= hi);
+    return true;
 }
 
 // Certified thick spatial test (fusion.py:268-296).  u, v are the projection

@@ -194,7 +194,6 @@ extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const floa
         band_pass<1, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
                                               (double2 *)bands, (float4 *)records, nv);
     }
-    launch_dilate((double2 *)bands, nv, (int)hm, (int)wm, s);
     return check_launch("divas_refine_bands");
 }
 
