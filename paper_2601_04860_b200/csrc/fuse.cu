@@ -1192,7 +1192,6 @@ static void launch_aux(const divas_fuse_args *a, int v0, int cnt, float4 *rec, d
         dim3 bg((unsigned)((a->wm + 255) / 256), (unsigned)B.nty, (unsigned)cnt);
         band_pass<1, false><<<bg, 256, 0, s>>>(B, m, nullptr, n, d, nullptr, nullptr, b, r, cnt);
     }
-    launch_dilate(b, cnt, a->hm, a->wm, s);
 }
 
 }  // namespace divas
