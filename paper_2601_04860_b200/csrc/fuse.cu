@@ -1182,7 +1182,7 @@ static void launch_aux(const divas_fuse_args *a, int v0, int cnt, float4 *rec, d
     const int32_t *n = a->nsamps + v0 * plane;
     const float *d = a->dexps + v0 * plane;
     float4 *r = rec + v0 * plane;
-    double2 *b = bands + (int64_t)v0 * 2 * B.nty * B.ntx;
+    double2 *b = bands + (int64_t)v0 * B.nty * B.ntx;
     const bool vec = (a->wm % 4 == 0) &&
                      ((((uintptr_t)m) | ((uintptr_t)n) | ((uintptr_t)d)) & 15) == 0;
     if (vec) {
