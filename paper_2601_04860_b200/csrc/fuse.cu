@@ -759,6 +759,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
 #ifndef DIVAS_SPLIT
 #define DIVAS_SPLIT 0
 #endif
+
 __global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
 fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
            FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
