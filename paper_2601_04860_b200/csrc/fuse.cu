@@ -245,26 +245,25 @@ __device__ __forceinline__ double grad_at(const float *__restrict__ dexp,
     return g;
 }
 
-// grad_at with one division: fl(a / rng) is monotone in a for rng > 0, so the
-// max over neighbours commutes with the division (NaN differences never win
-// in either form).  Falls back to the 4-division form otherwise.
-__device__ __forceinline__ double grad_at_fast(const float *__restrict__ dexp,
-                                               const float *__restrict__ dmin,
-                                               const float *__restrict__ dmax, int hm, int wm,
-                                               int ix, int iy, double eps, double kappa) {
-    const int64_t c = (int64_t)iy * wm + ix;
-    const float center = __ldg(dexp + c);
-    const float r32 = __ldg(dmax + c) - __ldg(dmin + c);            // f32 site
-    const double rng = (double)r32 + eps;
-    if (!(rng > 0.0)) return grad_at(dexp, dmin, dmax, hm, wm, ix, iy, eps, kappa);
+// _grad_at from pre-loaded centre / neighbour values with one division:
+// fl(a / rng) is monotone in a for rng > 0, so the max over neighbours
+// commutes with the division (NaN differences never win in either form);
+// the 4-division form (grad_at) otherwise.  f32 sites: fl(|nb - centre|).
+__device__ __forceinline__ double grad_from(float center, float dmin, float dmax, float nl,
+                                            float nr, float nu, float nd, const float *dexp,
+                                            const float *dmins, const float *dmaxs,
+                                            const FuseConst &C, int ix, int iy) {
+    const float r32 = dmax - dmin;                                  // f32 site
+    const double rng = (double)r32 + C.eps;
+    if (!(rng > 0.0)) return grad_at(dexp, dmins, dmaxs, C.hm, C.wm, ix, iy, C.eps, C.kappa);
     float amax = 0.0f;
-    if (ix > 0) amax = fmaxf(amax, fabsf(__ldg(dexp + c - 1) - center));    // f32 sites
-    if (ix < wm - 1) amax = fmaxf(amax, fabsf(__ldg(dexp + c + 1) - center));
-    if (iy > 0) amax = fmaxf(amax, fabsf(__ldg(dexp + c - wm) - center));
-    if (iy < hm - 1) amax = fmaxf(amax, fabsf(__ldg(dexp + c + wm) - center));
+    amax = fmaxf(amax, fabsf(nl - center));                         // f32 sites
+    amax = fmaxf(amax, fabsf(nr - center));
+    amax = fmaxf(amax, fabsf(nu - center));
+    amax = fmaxf(amax, fabsf(nd - center));
     const double gmax = amax > 0.0f ? (double)amax / rng : 0.0;
-    double g = 1.0 / (1.0 + kappa * gmax);
-    const double hi = 1.0 - eps;
+    double g = 1.0 / (1.0 + C.kappa * gmax);
+    const double hi = 1.0 - C.eps;
     if (g > hi) g = hi;
     if (g < 0.0) g = 0.0;
     return g;
@@ -464,16 +463,24 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     if (tx1 < tx0 || ty1 < ty0) return false;
     if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16) return false;
     const double2 *bv = M.bands + (int64_t)view * C.nty * C.ntx;
-    // the centre pixel's tile first: the likeliest to contain x_d
-    const int cx = (int)fmin(fmax(floor(Uc * (1.0 / kBandTile)), (double)tx0), (double)tx1);
-    const int cy = (int)fmin(fmax(floor(Vc * (1.0 / kBandTile)), (double)ty0), (double)ty1);
-    const double2 c = bv[cy * C.ntx + cx];
-    if (x_d >= c.x && x_d <= c.y) return false;
-    for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx) {
-            const double2 b = bv[ty * C.ntx + tx];
-            if (x_d >= b.x && x_d <= b.y) return false;   // a pixel of this tile may support
+    // tiles in row-major order, four loads in flight per round trip (indices
+    // past the last tile repeat it: always in range, never changes the answer)
+    const int nx = tx1 - tx0 + 1;
+    const int nt = nx * (ty1 - ty0 + 1);
+    int tx = tx0, ty = ty0;
+    for (int i0 = 0; i0 < nt; i0 += 4) {
+        double2 b[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            b[j] = __ldg(bv + ty * C.ntx + tx);
+            if (i0 + j + 1 < nt) {
+                if (++tx > tx1) { tx = tx0; ++ty; }
+            }
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (x_d >= b[j].x && x_d <= b[j].y) return false;   // this tile may support
+    }
     return true;
 }
 
@@ -634,9 +641,17 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
         if (b > C.bmax) b = C.bmax;
         const double tau_dp = (C.gamma + b) * C.dx;
         if (fabs(x_d - (double)dexp) <= tau_dp) {
+            // dmin, dmax and the four neighbour depths in one round trip; a
+            // missing neighbour reads the centre itself (|d - d| = 0 never
+            // raises the max, exactly like skipping it)
+            const float *de = M.dexps + pix;
             const float dmin = __ldg(M.dmins + pix), dmax = __ldg(M.dmaxs + pix);
-            const double gr = grad_at_fast(M.dexps + vplane, M.dmins + vplane, M.dmaxs + vplane,
-                                           C.hm, C.wm, (int)px, (int)py, C.eps, C.kappa);
+            const float nl = __ldg(de - (px > 0 ? 1 : 0));
+            const float nr = __ldg(de + (px < C.wm - 1 ? 1 : 0));
+            const float nu = __ldg(de - (py > 0 ? C.wm : 0));
+            const float nd = __ldg(de + (py < C.hm - 1 ? C.wm : 0));
+            const double gr = grad_from(dexp, dmin, dmax, nl, nr, nu, nd, M.dexps + vplane,
+                                        M.dmins + vplane, M.dmaxs + vplane, C, (int)px, (int)py);
             double t_c = 0.0;
             bool need_t = false;
             int ok = thick_certified(C, k, xc0, xc1, xc2, relx, rely, relz, dmin, dmax, gr, t_c,
@@ -767,13 +782,13 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
            uint4 *__restrict__ tq) {
     __shared__ QItem s_q[kQueue];
     __shared__ int s_nq;
+    const int view = C.view0 + (int)blockIdx.y;
     if (threadIdx.x == 0) s_nq = 0;
     __syncthreads();
     const long long n = min((long long)hdr->count, (long long)C.cap);
     const long long block0 = (long long)blockIdx.x * blockDim.x;
     if (block0 >= n) return;                                   // whole CTA idle
     const long long slot = block0 + threadIdx.x;
-    const int view = C.view0 + (int)blockIdx.y;
     Cam k;
     load_cam(cams + (int64_t)view * kCamStride, k);
     // phase A: route every pair; queue the thin candidates that need a scan
@@ -855,13 +870,25 @@ fuse_thin(FuseConst C, const double *__restrict__ cams, FuseMaps M, Contrib K,
 // ---------------------------------------------------------------------------
 constexpr int kReduceThreads = 128;
 
+__device__ __forceinline__ void reduce_store(const FuseConst &C, const FuseOut &O, uint32_t vi,
+                                             int n_thick, int n_thin, double sw, double smw,
+                                             double st) {
+    const double denom = sw + (double)n_thin;
+    const double p = (denom > C.eps) ? (smw + st) / denom : 0.0;
+    O.probs[vi] = p;
+    if (O.n_thick) O.n_thick[vi] = n_thick;
+    if (O.n_thin) O.n_thin[vi] = n_thin;
+    if (O.sw) O.sw[vi] = sw;
+    if (O.smw) O.smw[vi] = smw;
+    if (O.st) O.st[vi] = st;
+    if (O.occ) O.occ[vi] = (p >= C.occ_thr) ? 1 : 0;
+}
+
+// One voxel, lists in local memory (any count up to MAXV views).
 template <int MAXV>
-__global__ void __launch_bounds__(kReduceThreads)
-fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work,
-            const WsHeader *__restrict__ hdr) {
-    const long long n = min((long long)hdr->count, (long long)C.cap);
-    const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (slot >= n) return;
+__device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &K,
+                                             const FuseOut &O, const uint32_t *work,
+                                             long long slot) {
     double tw[MAXV], tmw[MAXV], tt[MAXV];
     int n_thick = 0, n_thin = 0;
     for (int wd = 0; wd < C.w32; ++wd) {
@@ -895,16 +922,17 @@ fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work
     double sw = 0.0, smw = 0.0, st = 0.0;
     for (int i = 0; i < n_thick; ++i) { sw += tw[i]; smw += tmw[i]; }
     for (int i = 0; i < n_thin; ++i) st += tt[i];
-    const double denom = sw + (double)n_thin;
-    const double p = (denom > C.eps) ? (smw + st) / denom : 0.0;
-    const uint32_t vi = work[slot];
-    O.probs[vi] = p;
-    if (O.n_thick) O.n_thick[vi] = n_thick;
-    if (O.n_thin) O.n_thin[vi] = n_thin;
-    if (O.sw) O.sw[vi] = sw;
-    if (O.smw) O.smw[vi] = smw;
-    if (O.st) O.st[vi] = st;
-    if (O.occ) O.occ[vi] = (p >= C.occ_thr) ? 1 : 0;
+    reduce_store(C, O, work[slot], n_thick, n_thin, sw, smw, st);
+}
+
+template <int MAXV>
+__global__ void __launch_bounds__(kReduceThreads)
+fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work,
+            const WsHeader *__restrict__ hdr) {
+    const long long n = min((long long)hdr->count, (long long)C.cap);
+    const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= n) return;
+    reduce_local<MAXV>(C, K, O, work, slot);
 }
 
 // ---------------------------------------------------------------------------
