@@ -119,7 +119,11 @@ typedef struct divas_fuse_args {
     double bc[3], bh[3];         /* SceneBounds centre / half (fusion.py:542) */
     int32_t unbounded;           /* spherical contraction on/off              */
     int64_t vox_lo, vox_hi;      /* flat voxel range [lo, hi) to fuse (a slab) */
-    double *probs;               /* [G^3] out, written on [lo, hi)            */
+    double *probs;               /* [G^3] out, written on [lo, hi); may be
+                                    page-locked host memory (unified addressing:
+                                    the kernels write it directly).  NULL is
+                                    allowed in calls without REDUCE: GATE then
+                                    leaves the (caller-zeroed) output alone.   */
     int32_t *n_thick, *n_thin;   /* [G^3] integer votes, or NULL              */
     double *sw, *smw, *st;       /* [G^3] sorted sums, or NULL                */
     uint8_t *occ;                /* [G^3] fused threshold p >= occ_thr, or NULL */

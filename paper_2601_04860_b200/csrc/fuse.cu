@@ -124,8 +124,10 @@ fuse_gate(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__re
             if (!count_only) {
                 if (aligned && k4 == 4) {
                     const double2 z2 = make_double2(0.0, 0.0);
-                    __stcs(reinterpret_cast<double2 *>(O.probs + base), z2);
-                    __stcs(reinterpret_cast<double2 *>(O.probs + base) + 1, z2);
+                    if (O.probs) {
+                        __stcs(reinterpret_cast<double2 *>(O.probs + base), z2);
+                        __stcs(reinterpret_cast<double2 *>(O.probs + base) + 1, z2);
+                    }
                     if (O.n_thick) *reinterpret_cast<int4 *>(O.n_thick + base) = make_int4(0, 0, 0, 0);
                     if (O.n_thin) *reinterpret_cast<int4 *>(O.n_thin + base) = make_int4(0, 0, 0, 0);
                     double *sums[3] = {O.sw, O.smw, O.st};
@@ -137,7 +139,7 @@ fuse_gate(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__re
                     if (O.occ) *reinterpret_cast<uchar4 *>(O.occ + base) = make_uchar4(occ0, occ0, occ0, occ0);
                 } else {
                     for (int k = 0; k < k4; ++k) {
-                        O.probs[base + k] = 0.0;
+                        if (O.probs) O.probs[base + k] = 0.0;
                         if (O.n_thick) O.n_thick[base + k] = 0;
                         if (O.n_thin) O.n_thin[base + k] = 0;
                         if (O.sw) O.sw[base + k] = 0.0;
@@ -360,6 +362,14 @@ __device__ __forceinline__ int cert_axis(double Ua, double E, double n, long lon
 // ---------------------------------------------------------------------------
 constexpr int kPairThreads = 256;
 
+#if DIVAS_STATS
+// experiment builds only: per-stage pair counters (tools/pair_stats.py)
+__device__ unsigned long long g_pair_stats[24];
+#define PSTAT(i, v) atomicAdd(&g_pair_stats[i], (unsigned long long)(v))
+#else
+#define PSTAT(i, v) ((void)0)
+#endif
+
 // (2 gamma + min(beta * n, bmax)) * dx, the reference's ops (fusion.py:362-365)
 __device__ __forceinline__ double tau_thin(const FuseConst &C, int32_t n) {
     double b = C.beta * (double)n;
@@ -423,6 +433,7 @@ __device__ __forceinline__ bool thin_bounds(const FuseConst &C, const Cam &k, do
             cert_floor(k.cy - vmax, EV, ys) && cert_floor(k.cy - vmin, EV, ye))
             return true;
     }
+    PSTAT(13, 1);
     // exact corner chain (fusion.py:315-341)
     double umn = 1e30, umx = -1e30, vmn = 1e30, vmx = -1e30;
 #pragma unroll 1
@@ -461,12 +472,13 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     const int tx0 = (int)fmax(fx0, 0.0), tx1 = (int)fmin(fx1, (double)(C.ntx - 1));
     const int ty0 = (int)fmax(fy0, 0.0), ty1 = (int)fmin(fy1, (double)(C.nty - 1));
     if (tx1 < tx0 || ty1 < ty0) return false;
-    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16) return false;
+    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16) { PSTAT(15, 1); return false; }
     const double2 *bv = M.bands + (int64_t)view * C.nty * C.ntx;
     // tiles in row-major order, four loads in flight per round trip (indices
     // past the last tile repeat it: always in range, never changes the answer)
     const int nx = tx1 - tx0 + 1;
     const int nt = nx * (ty1 - ty0 + 1);
+    PSTAT(7, nt);
     int tx = tx0, ty = ty0;
     for (int i0 = 0; i0 < nt; i0 += 4) {
         double2 b[4];
@@ -605,6 +617,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     const double relz = xc2 - k.p2;
     const double zc = k.r[2] * relx + k.r[5] * rely + k.r[8] * relz;
     const double x_d = -zc;
+    PSTAT(0, 1);
     if (!(x_d > 0.0)) return false;                            // behind the camera
     const double xcam = k.r[0] * relx + k.r[3] * rely + k.r[6] * relz;
     const double ycam = k.r[1] * relx + k.r[4] * rely + k.r[7] * relz;
@@ -624,12 +637,15 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
         px = pixel_index(u, (long long)k.w);
         py = pixel_index(v, (long long)k.h);
     }
+    PSTAT(1, 1);
+    if (cu == 2 || cv == 2) PSTAT(14, 1);
     const int64_t vplane = (int64_t)view * C.hm * C.wm;
     const int64_t pix = vplane + py * (int64_t)C.wm + px;
     const float4 rc = __ldg(M.rec + pix);                      // {m, d_exp, tau32, n}
     const int32_t ns = __float_as_int(rc.w);
     if (ns <= 0) return false;                                 // valids[view, py, px] == 0
     const float m = rc.x;
+    PSTAT(2, 1);
 #if defined(DIVAS_ABL) && DIVAS_ABL >= 3
     K.t[kidx] = (double)m;
     return false;
@@ -637,10 +653,12 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
 
     if ((double)m >= C.mask_thr && rho >= C.rho_thr) {
         const float dexp = rc.y;
+        PSTAT(3, 1);
         double b = C.beta * (double)ns;
         if (b > C.bmax) b = C.bmax;
         const double tau_dp = (C.gamma + b) * C.dx;
         if (fabs(x_d - (double)dexp) <= tau_dp) {
+            PSTAT(4, 1);
             // dmin, dmax and the four neighbour depths in one round trip; a
             // missing neighbour reads the centre itself (|d - d| = 0 never
             // raises the max, exactly like skipping it)
@@ -667,6 +685,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
                 }
                 wd = depth_weight(C, t_c, dmin, dmax);
             } else if (ok == 2) {                  // exact reference chain
+                PSTAT(12, 1);
                 const double u = (k.fx * (xcam / x_d) + k.cx) / k.w;
                 const double v = (k.cy - k.fy * (ycam / x_d)) / k.h;
                 ok = thick_spatial(C, k, xc0, xc1, xc2, u, v, dmin, dmax, gr, wd) ? 1 : 0;
@@ -675,6 +694,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
                 K.w[kidx] = wd;
                 K.mw[kidx] = (double)m * wd;
                 atomicOr(K.bits_thick + bidx, bit);
+                PSTAT(5, 1);
                 return false;                                  // routed thick
             }
         }
@@ -690,8 +710,10 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
         if (a < x_d * (1.0 - 1e-12)) return false;
         if (!(a > x_d * (1.0 + 1e-12)) && !(a / x_d >= 1.0)) return false;
     }
+    PSTAT(6, 1);
     if (C.band_ok && band_reject(C, M, k, view, x_d, xcam, ycam, A + k.cx, k.cy - B))
         return false;                                          // support is exactly 0
+    PSTAT(8, 1);
     x_d_out = x_d;
     xcam_out = xcam;
     ycam_out = ycam;
@@ -735,6 +757,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     const float Mg = (float)(9.5367431640625e-07 * (fabs(xd) + C.tau_max));   // 2^-20
     const int bw = (int)(xe - xs) + 1;
     const int npix = bw * ((int)(ye - ys) + 1);
+    PSTAT(9, npix);
     int sup = 0;
     float mmax = 0.0f;
     bool unsure = false;
@@ -748,6 +771,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
         unsure |= fabsf(e) < Mg;
         if (++col == bw) { col = 0; off += C.wm; }
     }
+    if (unsure) PSTAT(10, 1);
     if (unsure) {   // some pixel within the margin: recount with the reference's f64 test
         sup = 0;
         col = 0;
@@ -764,6 +788,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
     if (npix > 0 && t >= C.thin_accept) {
         K.t[(int64_t)view * C.cap + q.slot] = t;
+        PSTAT(11, 1);
         atomicOr(K.bits_thin + (int64_t)(view >> 5) * C.cap + q.slot, 1u << (view & 31));
     }
 }
@@ -1281,8 +1306,9 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         return DIVAS_EINVAL;
     }
     if (a->hm < 1 || a->wm < 1) { set_error("divas_fuse: empty planes"); return DIVAS_EINVAL; }
-    if (!a->cams || !a->dmins || !a->dmaxs || !a->dexps || !a->nsamps || !a->probs || !workspace ||
-        (!a->records && !a->masks)) {
+    const bool reduces = a->mode == DIVAS_FUSE_FULL || (a->mode & DIVAS_STEP_REDUCE);
+    if (!a->cams || !a->dmins || !a->dmaxs || !a->dexps || !a->nsamps || (reduces && !a->probs) ||
+        !workspace || (!a->records && !a->masks)) {
         set_error("divas_fuse: null pointer");
         return DIVAS_EINVAL;
     }
@@ -1419,3 +1445,15 @@ extern "C" int divas_pair_trace(const divas_trace_args *a, void *stream) {
     pair_trace_kernel<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(*a, C);
     return check_launch("divas_pair_trace");
 }
+
+#if DIVAS_STATS
+extern "C" int divas_debug_pair_stats(unsigned long long *out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, divas::g_pair_stats, sizeof(unsigned long long) * 24);
+    if (reset) {
+        unsigned long long z[24] = {0};
+        cudaMemcpyToSymbol(divas::g_pair_stats, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

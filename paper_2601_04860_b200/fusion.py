@@ -23,6 +23,7 @@ packs and moves data.  There is no CPU fallback.
 
 from __future__ import annotations
 
+import ctypes
 import json
 from dataclasses import asdict, dataclass, replace
 
@@ -344,6 +345,8 @@ class Fuser:
         cap = max(int(cap), 1)
         if probs is None:
             probs = torch.empty(nvox, dtype=torch.float64, device=dev)
+        elif probs is False:                  # GATE / PAIRS steps: no output grid
+            probs = None
         out = {"probs": probs}
         if stats:
             out["n_thick"] = torch.empty(nvox, dtype=torch.int32, device=dev)
@@ -409,14 +412,30 @@ class Fuser:
         return ws[256:256 + 4 * n].view(torch.int32).to(torch.int64) & 0xffffffff
 
 
-def _sparse_probs_to_host(out, nvox) -> np.ndarray:
-    """Dense host probabilities from the gated list: only ~1 % of voxels can be
-    nonzero, so copy (index, p) pairs instead of the whole G^3 f64 grid."""
+def _zeroed_host(nvox):
+    """A zero-filled page-locked f64 buffer for the dense result.  Called while
+    the device is still busy (uploads / fusion queued), so the parallel host
+    fill overlaps the device work; the block returns to torch's host cache
+    when the array built on it is released."""
+    import torch
+    host = torch.empty(nvox, dtype=torch.float64, pin_memory=True)
+    host.zero_()
+    return host
+
+
+def _sparse_probs_to_host(out, nvox, host=None) -> np.ndarray:
+    """Dense host probabilities from the gated list: only the gated voxels
+    can be nonzero (the gate pass writes 0 everywhere else), so their (index,
+    p) pairs are gathered on the device, copied, and scattered into a zeroed
+    host buffer (``host``: from ``_zeroed_host``, filled while the device
+    worked)."""
+    import torch
     idx = Fuser.gated_voxels(out)
-    vals = out["probs"][idx]
-    probs = np.zeros(nvox, dtype=np.float64)
-    probs[idx.cpu().numpy()] = vals.cpu().numpy()
-    return probs
+    vals = out["probs"].reshape(-1)[idx]
+    if host is None:
+        host = _zeroed_host(nvox)
+    host[idx.cpu()] = vals.cpu()
+    return host.numpy()
 
 
 def _device_inputs(grid, density, views, params, bounds):
@@ -445,7 +464,8 @@ def fuse(grid, density, views, params, bounds=None, workers=None,
         return OccupancyGrid(grid, fuse_traced(grid, density, views, params, bounds, trace_path))
     fuser, dens, dv = _device_inputs(grid, density, views, params, bounds)
     out = fuser.run(dens, dv)
-    return OccupancyGrid(grid, _sparse_probs_to_host(out, g ** 3).reshape(g, g, g))
+    host = _zeroed_host(g ** 3)
+    return OccupancyGrid(grid, _sparse_probs_to_host(out, g ** 3, host).reshape(g, g, g))
 
 
 def fuse_with_stats(grid, density, views, params, bounds=None):
@@ -497,20 +517,61 @@ def _trusted_mask(values):
     return m
 
 
+_STREAMS = {}
+
+
+def _adjacent_run(arrs, dt, shape):
+    """One (n, *shape) array over ``arrs`` when they are C-contiguous
+    ``shape`` planes of dtype ``dt`` laid end to end in memory (e.g. slices of
+    one stacked host buffer): one copy instead of n.  None otherwise."""
+    first = arrs[0]
+    if not isinstance(first, np.ndarray) or first.dtype != dt:
+        return None
+    nbytes = int(np.prod(shape)) * np.dtype(dt).itemsize
+    base = first.__array_interface__["data"][0]
+    for j, a in enumerate(arrs):
+        if (not isinstance(a, np.ndarray) or a.dtype != dt or a.shape != tuple(shape) or
+                not a.flags.c_contiguous or a.__array_interface__["data"][0] != base + j * nbytes):
+            return None
+    if len(arrs) == 1:
+        return first.reshape((1,) + tuple(shape))
+    buf = (ctypes.c_char * (nbytes * len(arrs))).from_address(base)
+    return np.frombuffer(buf, dtype=dt).reshape((len(arrs),) + tuple(shape))
+
+
+def _side_stream(dev, name):
+    """A per-device side stream (uploads / downloads of the pipelined update)."""
+    import torch
+    key = (str(dev), name)
+    if key not in _STREAMS:
+        _STREAMS[key] = torch.cuda.Stream(device=dev)
+    return _STREAMS[key]
+
+
 def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
-                    return_refined=True):
+                    return_refined=True, chunk_views=4):
     """``refine_mask`` on every (ViewGeometry, raw ConfidenceMask) pair, then
     ``fuse`` of the refined set -- the session's update (session.py:204-215)
     as one device pass: each host map is uploaded once, refinement writes the
-    fusion's scan records directly, and only the gated voxels' (index, p)
-    pairs come back.  Returns (OccupancyGrid, [refined ConfidenceMask] or None).
+    fusion's scan records directly.  Returns (OccupancyGrid, [refined
+    ConfidenceMask] or None).
+
+    Pipelined over chunks of ``chunk_views`` views: while chunk k+1 uploads
+    (side stream), chunk k is refined and its (view, voxel) pairs evaluated
+    (``divas_fuse`` PAIRS step for those views, current stream) and chunk
+    k-1's refined masks download (second side stream).  After the last chunk
+    only the value-sorted reduction and the (index, p) download of the gated
+    voxels remain, so an update costs about the host-link time of its inputs.
 
     Same validation and errors as the two reference calls; results identical
-    to ``fuse(grid, density, [(v, refine_mask(m, v)) ...], params, bounds)``.
+    to ``fuse(grid, density, [(v, refine_mask(m, v)) ...], params, bounds)``
+    (the pair evaluations and the order-independent reduction do not depend
+    on how the views are grouped).
     """
     import torch
-    from .segmenter import refine_bands_device
+    from .segmenter import ViewAux, refine_bands_device
     g = int(grid.resolution)
+    nvox = g ** 3
     _check_layout(grid, density)
     views = list(views)
     for vg, m in views:
@@ -521,29 +582,88 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     if not views:
         return OccupancyGrid(grid, np.zeros((g, g, g))), ([] if return_refined else None)
     dev = device()
-    vgs = [vg for vg, _m in views]
-    planes, sizes, cams = _upload_planes(vgs, [m for _vg, m in views], dev,
-                                         ("raw", "z", "dmins", "dmaxs", "dexps", "nsamps"))
-    dens = as_device(density.values, np.float32, dev)
+    cur = torch.cuda.current_stream(dev)
+    up, down = _side_stream(dev, "up"), _side_stream(dev, "down")
     fuser = Fuser(grid, params, bounds)
-    refined, aux = refine_bands_device(planes["raw"], planes["z"], planes["nsamps"],
-                                       planes["dexps"], fuser.pv, fuser.dx,
-                                       planar=return_refined)
-    # the fusion reads the refined masks from aux.records, never from dv.masks
-    dv = DeviceViews(torch.from_numpy(pack_cameras(cams)).to(dev), refined if refined is not None
-                     else planes["raw"], planes["dmins"], planes["dmaxs"], planes["dexps"],
-                     planes["nsamps"], sizes=sizes)
-    out = fuser.run(dens, dv, aux=aux)
+    cams = [vg.camera for vg, _m in views]
+    nv = len(views)
+    hm = max(int(c.height) for c in cams)
+    wm = max(int(c.width) for c in cams)
+    sizes = [(int(c.height), int(c.width)) for c in cams]
+    alloc = torch.empty if all(sz == (hm, wm) for sz in sizes) else torch.zeros
+    names = ("raw", "z", "dmins", "dmaxs", "dexps", "nsamps")
+    planes = {k: alloc((nv, hm, wm), dtype=torch.int32 if k == "nsamps" else torch.float32,
+                       device=dev) for k in names}
+    aux = ViewAux.empty(nv, hm, wm, dev)
+    refined = torch.empty((nv, hm, wm), dtype=torch.float32, device=dev) if return_refined else None
+    host = (torch.empty((nv, hm, wm), dtype=torch.float32, pin_memory=True)
+            if return_refined else None)
+    cam_t = torch.from_numpy(pack_cameras(cams)).to(dev, non_blocking=True)
+    # 1. density first (the gate count needs it), then every view upload queued
+    dens = as_device(density.values, np.float32, dev, non_blocking=True)
+    cnt = torch.zeros(256, dtype=torch.uint8, device=dev)
+    _native.check(_native.lib().divas_gate_count(ctypes.byref(fuser._args(dens, 0, nvox)),
+                                                 _native.ptr(cnt), _native.stream_handle()),
+                  "divas_gate_count")
+    up.wait_stream(cur)                       # planes allocated on the current stream
+    chunk = max(1, int(chunk_views))
+    bounds_k = [(v0, min(nv, v0 + chunk)) for v0 in range(0, nv, chunk)]
+    ready = []
+    srcs = [{"raw": m.values if hasattr(m, "values") else m, "z": vg.z_surface, "dmins": vg.d_min,
+             "dmaxs": vg.d_max, "dexps": vg.d_exp, "nsamps": vg.n_samples} for vg, m in views]
+    with torch.cuda.stream(up):
+        for v0, v1 in bounds_k:
+            for k in names:
+                dt = np.int32 if k == "nsamps" else np.float32
+                run = _adjacent_run([srcs[i][k] for i in range(v0, v1)], dt, (hm, wm))
+                if run is not None:           # the views' planes are one host block
+                    planes[k][v0:v1].copy_(torch.from_numpy(run), non_blocking=True)
+                    continue
+                for i in range(v0, v1):
+                    h, w = sizes[i]
+                    planes[k][i, :h, :w].copy_(
+                        torch.from_numpy(np.ascontiguousarray(srcs[i][k], dt)), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(up)
+            ready.append(ev)
+    # 2. exact workspace size (the count finished long before the uploads)
+    cap = max(int(cnt[:8].view(torch.int64).item()), 1)
+    dv = DeviceViews(cam_t, refined if refined is not None else planes["raw"], planes["dmins"],
+                     planes["dmaxs"], planes["dexps"], planes["nsamps"], sizes=sizes)
+    # The result grid lives in page-locked host memory: zero-filled by the
+    # host while the views upload, and the reduction writes the gated voxels'
+    # p into it directly (unified addressing) -- no gather, copy or scatter.
+    # The gate pass gets no output (probs=None) so it leaves the grid alone.
+    kw = dict(max_gated=cap, aux=aux)
+    out = fuser.run(dens, dv, steps=_native.STEP_GATE | _native.STEP_CLEAR_ALL, probs=False, **kw)
+    kw["workspace"] = out["workspace"]
+    # 3. per chunk: refine -> pairs of those views; refined masks download
+    for (v0, v1), ev in zip(bounds_k, ready):
+        cur.wait_event(ev)
+        refine_bands_device(planes["raw"][v0:v1], planes["z"][v0:v1], planes["nsamps"][v0:v1],
+                            planes["dexps"][v0:v1], fuser.pv, fuser.dx,
+                            out=refined[v0:v1] if return_refined else None,
+                            aux=aux.view_slices(v0, v1, nv, hm, wm), planar=return_refined)
+        fuser.run(dens, dv, steps=_native.STEP_PAIRS, view_range=(v0, v1), probs=False, **kw)
+        if return_refined:
+            down.wait_stream(cur)
+            with torch.cuda.stream(down):
+                host[v0:v1].copy_(refined[v0:v1], non_blocking=True)
+    # 4. reduction (p lands in hp), then the overflow flag
+    hp = _zeroed_host(nvox)                   # host fill overlaps the queued device work
+    fuser.run(dens, dv, steps=_native.STEP_REDUCE, probs=hp, **kw)
+    hdr_h = torch.empty(16, dtype=torch.uint8, pin_memory=True)
+    hdr_h.copy_(kw["workspace"][:16], non_blocking=True)
+    cur.synchronize()
+    if int(hdr_h[8:12].view(torch.int32).item()) != 0:
+        raise RuntimeError("divas_fuse: gated voxels exceeded the workspace capacity")
+    hpn = hp.numpy()
     masks = None
     if return_refined:
-        host = torch.empty(refined.shape, dtype=torch.float32, pin_memory=True)
-        host.copy_(refined, non_blocking=True)
-    probs = _sparse_probs_to_host(out, g ** 3).reshape(g, g, g)
-    if return_refined:
-        torch.cuda.current_stream().synchronize()
+        down.synchronize()
         hn = host.numpy()
         masks = [_trusted_mask(hn[i, :h, :w]) for i, (h, w) in enumerate(sizes)]
-    return OccupancyGrid(grid, probs), masks
+    return OccupancyGrid(grid, hpn.reshape(g, g, g)), masks
 
 
 def gradient_maps_device(views: DeviceViews, eps: float, kappa: float, stream=None):

@@ -333,3 +333,23 @@ def test_refine_and_fuse_equals_two_calls(dev):
     assert none is None and np.array_equal(og3.probs, og.probs)
     with pytest.raises(ValueError):
         refine_and_fuse(grid, dens, [(raws[0][0], masks[0])], params)
+
+
+@pytest.mark.parametrize("name", ["sop", "mixed"])
+def test_refine_and_fuse_chunking(dev, name):
+    """The pipelined update does not depend on how views are grouped into
+    upload/pair chunks, nor on padded (mixed-size) views: every grouping gives
+    exactly refine_mask per view + fuse."""
+    from paper_2601_04860_b200 import (ConfidenceMask, FusionParams, fuse, refine_and_fuse,
+                                       refine_mask)
+    case = golden_io.scene_cases()[name]
+    grid, dens, views, bounds = reference_objects(case)
+    params = FusionParams(*[float(x) for x in case.pv[:13]], enable_thin=bool(case.pv[13]))
+    raws = [(vg, ConfidenceMask(m.values.copy())) for vg, m in views]
+    ref = fuse(grid, dens, [(vg, refine_mask(m, vg)) for vg, m in raws], params, bounds=bounds)
+    for chunk in (1, 2, 3, 64):
+        og, masks = refine_and_fuse(grid, dens, raws, params, bounds=bounds, chunk_views=chunk)
+        assert np.array_equal(og.probs, ref.probs), chunk
+        for (vg, m), got in zip(raws, masks):
+            assert got.shape == m.shape
+            assert np.array_equal(got.values, refine_mask(m, vg).values), chunk
