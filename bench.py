@@ -536,6 +536,7 @@ def run_e2e(args, wl, params, dev):
     torch.cuda.synchronize()
     times = []
     for _ in range(max(1, args.e2e_steps)):
+        og = refined = None               # the previous update's results are released
         t0 = time.perf_counter()
         og, refined = once()
         times.append(time.perf_counter() - t0)

@@ -38,7 +38,9 @@ def report(path, sass=False):
                          text=True).stdout
     for line in out.splitlines():
         s = line.strip()
-        if any(s.startswith(k) for k in KEYS):
+        if ", Context " in s:                       # a kernel's section header
+            print("== " + re.sub(r"\(.*?\)\s*\(", "(", s.split(", Context ")[0], count=1))
+        elif any(s.startswith(k) for k in KEYS):
             print(s)
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
