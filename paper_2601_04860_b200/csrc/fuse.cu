@@ -761,26 +761,31 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     int sup = 0;
     float mmax = 0.0f;
     bool unsure = false;
-    int col = 0, off = 0;
+    // a running record pointer: +1 per pixel, + (wm - bw) at the end of a row
+    const int64_t skip = (int64_t)C.wm - bw;
+    const float4 *__restrict__ pp = rp;
+    int left = bw;
 #pragma unroll 4
     for (int i = 0; i < npix; ++i) {
-        const float4 r = __ldg(rp + off + col);
+        const float4 r = __ldg(pp);
         mmax = fmaxf(mmax, r.x);
         const float e = fabsf(xd32 - r.y) - r.z;
         sup += (e <= -Mg) ? 1 : 0;
         unsure |= fabsf(e) < Mg;
-        if (++col == bw) { col = 0; off += C.wm; }
+        ++pp;
+        if (--left == 0) { left = bw; pp += skip; }
     }
     if (unsure) PSTAT(10, 1);
     if (unsure) {   // some pixel within the margin: recount with the reference's f64 test
         sup = 0;
-        col = 0;
-        off = 0;
+        pp = rp;
+        left = bw;
         for (int i = 0; i < npix; ++i) {
-            const float4 r = __ldg(rp + off + col);
+            const float4 r = __ldg(pp);
             sup += (r.z >= 0.0f && fabs(xd - (double)r.y) <= tau_thin(C, __float_as_int(r.w)))
                        ? 1 : 0;
-            if (++col == bw) { col = 0; off += C.wm; }
+            ++pp;
+            if (--left == 0) { left = bw; pp += skip; }
         }
     }
     const double m_max = (double)mmax;
