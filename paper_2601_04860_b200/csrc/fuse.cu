@@ -479,14 +479,17 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     const int nx = tx1 - tx0 + 1;
     const int nt = nx * (ty1 - ty0 + 1);
     PSTAT(7, nt);
-    int tx = tx0, ty = ty0;
+    const int skip = C.ntx - nx;
+    const double2 *__restrict__ bp = bv + ty0 * C.ntx + tx0;
+    int left = nx;
     for (int i0 = 0; i0 < nt; i0 += 4) {
         double2 b[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            b[j] = __ldg(bv + ty * C.ntx + tx);
+            b[j] = __ldg(bp);
             if (i0 + j + 1 < nt) {
-                if (++tx > tx1) { tx = tx0; ++ty; }
+                ++bp;
+                if (--left == 0) { left = nx; bp += skip; }
             }
         }
 #pragma unroll
