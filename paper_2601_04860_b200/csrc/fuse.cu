@@ -57,7 +57,25 @@ struct FuseConst {
     double bc0, bc1, bc2, bh0, bh1, bh2;
     int unbounded;
     double occ_thr;
+    int gshift;          // log2(g) when g is a power of two, else -1
 };
+
+// (ix, iy, iz) of a flat voxel index: shifts for power-of-two grids
+__device__ __forceinline__ void voxel_coords(const FuseConst &C, uint32_t vi, uint32_t &ix,
+                                             uint32_t &iy, uint32_t &iz) {
+    if (C.gshift >= 0) {
+        const uint32_t m = (1u << C.gshift) - 1u;
+        ix = vi >> (2 * C.gshift);
+        iy = (vi >> C.gshift) & m;
+        iz = vi & m;
+    } else {
+        const uint32_t g = (uint32_t)C.g, gg = g * g;
+        ix = vi / gg;
+        const uint32_t rem = vi - ix * gg;
+        iy = rem / g;
+        iz = rem - iy * g;
+    }
+}
 
 struct FuseOut {
     double *probs;
@@ -604,11 +622,8 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
                                            const FuseMaps &M, const Contrib &K, uint32_t vi,
                                            int view, int64_t kidx, int64_t bidx, uint32_t bit,
                                            double &x_d_out, double &xcam_out, double &ycam_out) {
-    const uint32_t g = (uint32_t)C.g, gg = g * g;
-    const uint32_t ix = vi / gg;
-    const uint32_t rem = vi - ix * gg;
-    const uint32_t iy = rem / g;
-    const uint32_t iz = rem - iy * g;
+    uint32_t ix, iy, iz;
+    voxel_coords(C, vi, ix, iy, iz);
     const double rho = (double)__ldg(dens + vi);
     const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
     const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
@@ -727,11 +742,8 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
 __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, const FuseMaps &M,
                                           const Contrib &K, int view,
                                           const QItem &q) {
-    const uint32_t g = (uint32_t)C.g, gg = g * g;
-    const uint32_t ix = q.vi / gg;
-    const uint32_t rem = q.vi - ix * gg;
-    const uint32_t iy = rem / g;
-    const uint32_t iz = rem - iy * g;
+    uint32_t ix, iy, iz;
+    voxel_coords(C, q.vi, ix, iy, iz);
     const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
     const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
     const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
@@ -876,11 +888,8 @@ fuse_thin(FuseConst C, const double *__restrict__ cams, FuseMaps M, Contrib K,
         const int view = (int)e.z;
         Cam k;
         load_cam(cams + (int64_t)view * kCamStride, k);
-        const uint32_t g = (uint32_t)C.g, gg = g * g;
-        const uint32_t ix = e.y / gg;
-        const uint32_t rem = e.y - ix * gg;
-        const uint32_t iy = rem / g;
-        const uint32_t iz = rem - iy * g;
+        uint32_t ix, iy, iz;
+        voxel_coords(C, e.y, ix, iy, iz);
         const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
         const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
         const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
@@ -1204,6 +1213,10 @@ static int sm_count() {
 
 static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     C.g = a->g; C.lo = a->vox_lo; C.hi = a->vox_hi;
+    C.gshift = -1;
+    if (a->g > 0 && (a->g & (a->g - 1)) == 0)
+        for (int b = 0; b < 31; ++b)
+            if ((int64_t(1) << b) == a->g) { C.gshift = b; break; }
     C.origin0 = a->origin[0]; C.origin1 = a->origin[1]; C.origin2 = a->origin[2];
     C.dx = a->dx_vox;
     C.nv = a->nv; C.hm = a->hm; C.wm = a->wm; C.w32 = (a->nv + 31) / 32;
