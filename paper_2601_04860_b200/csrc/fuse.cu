@@ -100,7 +100,7 @@ struct WsHeader {
     unsigned long long count;    // gated voxels found
     unsigned int overflow;       // count > cap
     unsigned int pad;
-    unsigned long long nthin;    // thin candidates queued for fuse_thin
+    unsigned long long reserved;
 };
 
 // ---------------------------------------------------------------------------
@@ -816,27 +816,15 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
 #ifndef DIVAS_PAIR_MINB
 #define DIVAS_PAIR_MINB 4
 #endif
-#ifndef DIVAS_SPLIT
-#define DIVAS_SPLIT 0
-#endif
-
-__global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
-fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
-           FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
-           const WsHeader *__restrict__ hdr, WsHeader *__restrict__ hdr_mut,
-           uint4 *__restrict__ tq) {
-    __shared__ QItem s_q[kQueue];
-    __shared__ int s_nq;
-    const int view = C.view0 + (int)blockIdx.y;
-    if (threadIdx.x == 0) s_nq = 0;
-    __syncthreads();
-    const long long n = min((long long)hdr->count, (long long)C.cap);
-    const long long block0 = (long long)blockIdx.x * blockDim.x;
-    if (block0 >= n) return;                                   // whole CTA idle
+// One tile = one view x 256 consecutive gated voxels.  Phase A routes every
+// pair of the tile and compacts the thin candidates that need a footprint
+// scan into a shared-memory queue; phase B runs them on densely packed warps.
+__device__ __forceinline__ void pair_tile(const FuseConst &C, const Cam &k,
+                                          const float *__restrict__ dens, const FuseMaps &M,
+                                          const Contrib &K, const uint32_t *__restrict__ work,
+                                          long long n, long long block0, int view, QItem *s_q,
+                                          int *s_nq) {
     const long long slot = block0 + threadIdx.x;
-    Cam k;
-    load_cam(cams + (int64_t)view * kCamStride, k);
-    // phase A: route every pair; queue the thin candidates that need a scan
     bool has = false;
     QItem q;
     if (slot < n) {
@@ -848,64 +836,31 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
     }
     const unsigned ball = __ballot_sync(0xffffffffu, has);
     const int lane = threadIdx.x & 31;
-#if DIVAS_SPLIT
-    // queue the candidates for fuse_thin (warp-aggregated append)
-    if (ball) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(&hdr_mut->nthin, (unsigned long long)__popc(ball));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (has)
-            tq[base + __popc(ball & ((1u << lane) - 1u))] =
-                make_uint4((uint32_t)slot, q.vi, (uint32_t)view, 0u);
-    }
-#else
     int base = 0;
-    if (lane == 0 && ball) base = atomicAdd(&s_nq, __popc(ball));
+    if (lane == 0 && ball) base = atomicAdd(s_nq, __popc(ball));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (has) s_q[base + __popc(ball & ((1u << lane) - 1u))] = q;
     __syncthreads();
-    // phase B: the queued candidates, densely packed onto the first warps
-    const int nq = s_nq;
+    const int nq = *s_nq;
     for (int i = threadIdx.x; i < nq; i += blockDim.x) thin_item(C, k, M, K, view, s_q[i]);
-#endif
 }
 
-#if DIVAS_SPLIT
-// Phase B as its own kernel: one thread per queued thin candidate, densely
-// packed (grid-stride over the device-side queue count).  The centre's camera
-// coordinates are recomputed exactly (the reference's chain, no division).
-constexpr int kThinThreads = 128;
-#ifndef DIVAS_THIN_MINB
-#define DIVAS_THIN_MINB 8
-#endif
-__global__ void __launch_bounds__(kThinThreads, DIVAS_THIN_MINB)
-fuse_thin(FuseConst C, const double *__restrict__ cams, FuseMaps M, Contrib K,
-          const uint4 *__restrict__ tq, const WsHeader *__restrict__ hdr) {
-    const unsigned long long n = hdr->nthin;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-        const uint4 e = tq[i];
-        const int view = (int)e.z;
-        Cam k;
-        load_cam(cams + (int64_t)view * kCamStride, k);
-        uint32_t ix, iy, iz;
-        voxel_coords(C, e.y, ix, iy, iz);
-        const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
-        const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
-        const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
-        const double relx = xc0 - k.p0;
-        const double rely = xc1 - k.p1;
-        const double relz = xc2 - k.p2;
-        QItem q;
-        q.slot = e.x;
-        q.vi = e.y;
-        q.x_d = -(k.r[2] * relx + k.r[5] * rely + k.r[8] * relz);
-        q.xcam = k.r[0] * relx + k.r[3] * rely + k.r[6] * relz;
-        q.ycam = k.r[1] * relx + k.r[4] * rely + k.r[7] * relz;
-        thin_item(C, k, M, K, view, q);
-    }
+__global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
+fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
+           FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
+           const WsHeader *__restrict__ hdr, int nviews) {
+    __shared__ QItem s_q[kQueue];
+    __shared__ int s_nq;
+    const long long n = min((long long)hdr->count, (long long)C.cap);
+    const int view = C.view0 + (int)blockIdx.y;
+    if (threadIdx.x == 0) s_nq = 0;
+    __syncthreads();
+    const long long block0 = (long long)blockIdx.x * blockDim.x;
+    if (block0 >= n) return;                                   // whole CTA idle
+    Cam k;
+    load_cam(cams + (int64_t)view * kCamStride, k);
+    pair_tile(C, k, dens, M, K, work, n, block0, view, s_q, &s_nq);
 }
-#endif
 
 // ---------------------------------------------------------------------------
 // reduction: value-sorted sums per voxel
@@ -1178,7 +1133,7 @@ __global__ void clear_view_bits(Contrib K, int64_t cap, int view_lo, int view_hi
 // workspace layout
 // ---------------------------------------------------------------------------
 struct WsLayout {
-    size_t work, bits_thick, bits_thin, w, mw, t, rec, bands, tq, total;
+    size_t work, bits_thick, bits_thin, w, mw, t, rec, bands, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1196,7 +1151,6 @@ static WsLayout ws_layout(int64_t cap, int32_t nv_cap, int32_t hm, int32_t wm) {
     L.t = off;          off = align256(off + (size_t)nv_cap * c * 8);
     L.rec = off;        off = align256(off + record_bytes(nv_cap, hm, wm));
     L.bands = off;      off = align256(off + band_bytes(nv_cap, hm, wm));
-    L.tq = off;         off = align256(off + (size_t)nv_cap * c * 16);
     L.total = off;
     return L;
 }
@@ -1394,16 +1348,9 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         const int64_t cap_blocks = (cap + kPairThreads - 1) / kPairThreads;
         if (cap_blocks > 0x7fffffffLL) { set_error("divas_fuse: too many slots"); return DIVAS_EINVAL; }
         C.view0 = v0;
-        uint4 *tq = (uint4 *)(ws + L.tq);
-        if (cudaMemsetAsync(&hdr->nthin, 0, sizeof(unsigned long long), s) != cudaSuccess)
-            return check_launch("divas_fuse(memset queue)");
         fuse_pairs<<<dim3((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)(v1 - v0)),
-                     kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr, hdr, tq);
+                     kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr, v1 - v0);
         if ((rc = check_launch("divas_fuse(pairs)"))) return rc;
-#if DIVAS_SPLIT
-        fuse_thin<<<(unsigned)(sm_count() * 16), kThinThreads, 0, s>>>(C, a->cams, M, K, tq, hdr);
-        if ((rc = check_launch("divas_fuse(thin)"))) return rc;
-#endif
     }
     if (steps & DIVAS_STEP_REDUCE) {
         const unsigned rblocks =
