@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--slabs", default="balanced", choices=["balanced", "equal"])
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="slab mode, N>1: occupancy all-gather fused into the fusion's stores "
+                         "over NVLink (symmetric memory), or a separate NCCL all_gather")
     ap.add_argument("--shard", default="slabs", choices=["slabs", "views"],
                     help="N>1 decomposition: voxel slabs (default) or view blocks")
     return ap.parse_args()
@@ -348,7 +351,19 @@ def run_ours(args):
         ws = torch.empty(_native.ws_regions(cap, plan.nv_cap, H, W)["total"], dtype=torch.uint8,
                          device=dev)
 
-    def step(ev=None):
+    peer = None
+    gather_mode = None
+    if world > 1 and not views_mode:
+        gather_mode = "nccl all_gather of the slab occupancy bytes"
+        if args.gather == "p2p":
+            try:
+                peer = sharding.PeerOccupancy(g ** 3, dev)
+                gather_mode = ("fused: gate/reduce store occupancy into every rank's "
+                               "symmetric-memory buffer over NVLink, device barrier")
+            except Exception as e:  # noqa: BLE001
+                gather_mode = f"nccl all_gather (symmetric memory unavailable: {type(e).__name__})"
+
+    def step(ev=None, check=False):
         nonlocal ws, bands
         if ev is not None:
             ev[0].record(stream)
@@ -372,14 +387,20 @@ def run_ours(args):
             plan.exchange(ws, rank)
             out = fuser.run(wl.density, dv, steps=_native.STEP_REDUCE, **kw)
         else:
-            out = fuser.run(wl.density, dv, probs=probs, occ=occ_buf, vox_range=(lo, hi),
-                            workspace=ws, aux=bands, max_gated=cap)
+            out = fuser.run(wl.density, dv, probs=probs,
+                            occ=occ_buf if (peer is None or check) else None,
+                            vox_range=(lo, hi), workspace=ws, aux=bands, max_gated=cap,
+                            occ_peers=peer.peers if peer is not None else None)
         ws = out["workspace"]
         if ev is not None:
             ev[2].record(stream)
         occ_full = None
         if world > 1 and not views_mode:
-            occ_full = sharding.gather_occupancy(out["occ"][lo:hi], slabs, g, rank)
+            if peer is not None:
+                peer.barrier()
+                occ_full = peer.buf
+            else:
+                occ_full = sharding.gather_occupancy(out["occ"][lo:hi], slabs, g, rank)
         if ev is not None:
             ev[3].record(stream)
         return out, occ_full
@@ -389,6 +410,17 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     if world > 1:
+        dist.barrier()
+    if peer is not None:
+        # the fused gather must equal the NCCL one bit for bit, or it is not used
+        out_c, occ_p = step(check=True)
+        ref = sharding.gather_occupancy(out_c["occ"][lo:hi], slabs, g, rank)
+        bad = torch.tensor([0 if torch.equal(occ_p, ref) else 1], device=dev)
+        dist.all_reduce(bad)
+        if int(bad.item()):
+            peer = None
+            gather_mode = "nccl all_gather (fused peer stores failed the bit-exact check)"
+        torch.cuda.synchronize()
         dist.barrier()
 
     K = args.steps
@@ -483,6 +515,7 @@ def run_ours(args):
                             " + all-gather(contributions) + reduce" if views_mode else
                             "refine+aux(all views) + fuse(slab, threshold fused)"
                             + (" + all-gather(occupancy)" if world > 1 else "")),
+                   "gather": gather_mode,
                    "l2": "flushed (256 MiB write) between steps, outside the events",
                    "params": "FusionParams() defaults"},
         "breakdown_ms": {"refine": refine_ms, "fuse": fuse_ms, "gather": float(np.mean(t_gath)),

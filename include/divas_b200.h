@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define DIVAS_ABI_VERSION 6
+#define DIVAS_ABI_VERSION 7
 
 /* error codes */
 #define DIVAS_OK          0
@@ -139,6 +139,15 @@ typedef struct divas_fuse_args {
     int32_t mode;                /* DIVAS_FUSE_FULL or DIVAS_STEP_* flags       */
     int32_t view_lo, view_hi;    /* views evaluated by PAIRS / cleared by
                                     CLEAR_VIEWS (ignored by FULL)              */
+    uint8_t *const *occ_peers;   /* device array of n_peers device pointers, or
+                                    NULL: [G^3] occupancy buffers (one per rank,
+                                    e.g. NVLink peer mappings of symmetric
+                                    memory).  The fused occupancy of [lo, hi)
+                                    is stored into EVERY listed buffer at the
+                                    same offsets -- the slab all-gather fused
+                                    into the gate (zeros) and reduce (p >=
+                                    occ_thr) stores.  Independent of `occ`.    */
+    int32_t n_peers;
 } divas_fuse_args;
 
 /* Workspace bytes for divas_fuse with slot capacity `max_gated`, `nv_cap`

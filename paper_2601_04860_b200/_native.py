@@ -47,6 +47,7 @@ class FuseArgs(ctypes.Structure):
         ("st", _VP), ("occ", _VP), ("occ_thr", ctypes.c_double), ("max_gated", ctypes.c_int64),
         ("records", _VP), ("bands", _VP), ("nv_cap", ctypes.c_int32), ("mode", ctypes.c_int32),
         ("view_lo", ctypes.c_int32), ("view_hi", ctypes.c_int32),
+        ("occ_peers", _VP), ("n_peers", ctypes.c_int32),
     ]
 
 FUSE_FULL = 0

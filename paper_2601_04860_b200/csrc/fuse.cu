@@ -82,6 +82,8 @@ struct FuseOut {
     int32_t *n_thick, *n_thin;
     double *sw, *smw, *st;
     uint8_t *occ;
+    uint8_t *const *occ_peers;   // fused slab all-gather: every rank's buffer
+    int n_peers;
 };
 
 struct FuseMaps {
@@ -155,6 +157,9 @@ fuse_gate(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__re
                             reinterpret_cast<double2 *>(sums[s] + base)[1] = z2;
                         }
                     if (O.occ) *reinterpret_cast<uchar4 *>(O.occ + base) = make_uchar4(occ0, occ0, occ0, occ0);
+                    for (int r = 0; r < O.n_peers; ++r)       // NVLink stores to every rank
+                        *reinterpret_cast<uchar4 *>(O.occ_peers[r] + base) =
+                            make_uchar4(occ0, occ0, occ0, occ0);
                 } else {
                     for (int k = 0; k < k4; ++k) {
                         if (O.probs) O.probs[base + k] = 0.0;
@@ -164,6 +169,7 @@ fuse_gate(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__re
                         if (O.smw) O.smw[base + k] = 0.0;
                         if (O.st) O.st[base + k] = 0.0;
                         if (O.occ) O.occ[base + k] = occ0;
+                        for (int r = 0; r < O.n_peers; ++r) O.occ_peers[r][base + k] = occ0;
                     }
                 }
             }
@@ -878,7 +884,9 @@ __device__ __forceinline__ void reduce_store(const FuseConst &C, const FuseOut &
     if (O.sw) O.sw[vi] = sw;
     if (O.smw) O.smw[vi] = smw;
     if (O.st) O.st[vi] = st;
-    if (O.occ) O.occ[vi] = (p >= C.occ_thr) ? 1 : 0;
+    const uint8_t oc = (p >= C.occ_thr) ? 1 : 0;
+    if (O.occ) O.occ[vi] = oc;
+    for (int r = 0; r < O.n_peers; ++r) O.occ_peers[r][vi] = oc;
 }
 
 // One voxel, lists in local memory (any count up to MAXV views).
@@ -1291,6 +1299,10 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         set_error("divas_fuse: records and bands come together");
         return DIVAS_EINVAL;
     }
+    if (a->occ_peers && (a->n_peers < 1 || a->n_peers > 1024)) {
+        set_error("divas_fuse: n_peers %d outside [1, 1024]", a->n_peers);
+        return DIVAS_EINVAL;
+    }
     const int steps = a->mode == DIVAS_FUSE_FULL
                           ? (DIVAS_STEP_GATE | DIVAS_STEP_CLEAR_ALL | DIVAS_STEP_PAIRS | DIVAS_STEP_REDUCE)
                           : a->mode;
@@ -1312,7 +1324,8 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     cudaStream_t s = (cudaStream_t)stream;
     FuseConst C;
     fill_const(C, a, cap);
-    FuseOut O{a->probs, a->n_thick, a->n_thin, a->sw, a->smw, a->st, a->occ};
+    FuseOut O{a->probs, a->n_thick, a->n_thin, a->sw, a->smw, a->st, a->occ,
+              a->occ_peers, a->occ_peers ? a->n_peers : 0};
     FuseMaps M{a->masks, a->dmins, a->dmaxs, a->dexps, a->nsamps,
                (const double2 *)a->bands, (const float4 *)a->records};
     char *ws = (char *)workspace;

@@ -325,13 +325,18 @@ class Fuser:
 
     def run(self, density, views: DeviceViews, probs=None, stats=False, occ=False,
             occ_thr=0.5, vox_range=None, workspace=None, stream=None, max_gated=None,
-            aux=None, nv_cap=None, incremental=None, steps=None, view_range=None):
+            aux=None, nv_cap=None, incremental=None, steps=None, view_range=None,
+            occ_peers=None):
         """Enqueue ``divas_fuse``.  ``aux``: ViewAux from ``refine_bands_device``
         (else built in the workspace).  ``incremental=(v0, v1)``: re-evaluate
         only views [v0, v1) against the state a previous full ``run`` left in
         ``workspace`` (same density, range, params and output buffers) --
         ``nv_cap`` sizes that workspace for views added later.  ``steps``:
-        explicit ``_native.STEP_*`` flags with ``view_range`` (views-sharding)."""
+        explicit ``_native.STEP_*`` flags with ``view_range`` (views-sharding).
+        ``occ_peers``: (device pointer of an array of n buffer pointers, n) --
+        the occupancy of the range is also stored into every listed [G^3]
+        buffer (``sharding.PeerOccupancy``: the slab all-gather fused into the
+        fusion's own stores over NVLink)."""
         import ctypes
         import torch
         g = self.g
@@ -379,6 +384,8 @@ class Fuser:
         if aux is not None:
             a.records, a.bands = _native.ptr(aux.records), _native.ptr(aux.bands)
         a.nv_cap = nvc
+        if occ_peers is not None:
+            a.occ_peers, a.n_peers = int(occ_peers[0]), int(occ_peers[1])
         if incremental is not None:
             a.mode = _native.FUSE_INCREMENTAL
             a.view_lo, a.view_hi = int(incremental[0]), int(incremental[1])

@@ -27,7 +27,7 @@ import numpy as np
 
 __all__ = ["slice_weights", "balanced_slabs", "equal_slabs", "slab_voxel_range",
            "broadcast_views", "gather_occupancy", "gather_slab_values",
-           "view_blocks", "ViewShardPlan"]
+           "view_blocks", "ViewShardPlan", "PeerOccupancy"]
 
 # relative cost of one voxel in the dense gate pass vs one gated voxel-view pair
 STREAM_WEIGHT = 0.02
@@ -123,6 +123,37 @@ def _gather_padded(chunk, slabs, g, rank, group, dtype_fill=0):
 def gather_occupancy(occ_slab, slabs, g: int, rank: int, group=None):
     """Full (G^3,) uint8 occupancy on every rank from each rank's slab bytes."""
     return _gather_padded(occ_slab, slabs, g, rank, group)
+
+
+class PeerOccupancy:
+    """The slab all-gather fused into the fusion's stores.
+
+    A [G^3] uint8 occupancy buffer in symmetric memory on every rank
+    (``torch.distributed._symmetric_memory``: NVLink peer mappings of each
+    rank's allocation).  ``Fuser.run(occ_peers=self.peers)`` makes the gate and
+    reduce kernels store each voxel's occupancy byte into EVERY rank's buffer
+    (zeros of the slab as coalesced 4-byte stores, the gated voxels' p >= thr
+    bytes as they are reduced), so after ``barrier()`` each rank holds the
+    full grid without a separate collective.  Raises if symmetric memory is
+    unavailable (the caller falls back to ``gather_occupancy``).
+    """
+
+    def __init__(self, nvox: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        group = group or dist.group.WORLD
+        self.buf = symm.empty(nvox, dtype=torch.uint8, device=device)
+        self.hdl = symm.rendezvous(self.buf, group)
+        self.world = int(self.hdl.world_size)
+        ptrs = [int(p) for p in self.hdl.buffer_ptrs]
+        self.ptr_table = torch.tensor(ptrs, dtype=torch.int64, device=device)
+        self.peers = (int(self.ptr_table.data_ptr()), self.world)
+
+    def barrier(self):
+        """Device-side barrier on the current stream: every rank's stores of
+        this step have landed in every buffer after it."""
+        self.hdl.barrier(channel=0)
 
 
 def gather_slab_values(vals_slab, slabs, g: int, rank: int, group=None):
