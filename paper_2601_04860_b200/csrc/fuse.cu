@@ -896,32 +896,60 @@ __device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &
                                              long long slot) {
     double tw[MAXV], tmw[MAXV], tt[MAXV];
     int n_thick = 0, n_thin = 0;
+    // contributions are fetched in groups of 4 (all loads in flight before
+    // the first insertion), then inserted in view order as before
     for (int wd = 0; wd < C.w32; ++wd) {
         uint32_t bt = K.bits_thick[(int64_t)wd * C.cap + slot];
         while (bt) {
-            const int view = wd * 32 + __ffs(bt) - 1;
-            bt &= bt - 1;
-            const double kw = K.w[(int64_t)view * C.cap + slot];
-            const double km = K.mw[(int64_t)view * C.cap + slot];
-            int j = n_thick - 1;   // stable insertion by (w, m*w): fusion.py:389-407
-            while (j >= 0 && (tw[j] > kw || (tw[j] == kw && tmw[j] > km))) {
-                tw[j + 1] = tw[j];
-                tmw[j + 1] = tmw[j];
-                --j;
+            double kw[4], km[4];
+            int c = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (bt) {
+                    const int view = wd * 32 + __ffs(bt) - 1;
+                    bt &= bt - 1;
+                    kw[u] = K.w[(int64_t)view * C.cap + slot];
+                    km[u] = K.mw[(int64_t)view * C.cap + slot];
+                    c = u + 1;
+                }
             }
-            tw[j + 1] = kw;
-            tmw[j + 1] = km;
-            ++n_thick;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (u < c) {
+                    int j = n_thick - 1;   // stable insertion by (w, m*w): fusion.py:389-407
+                    while (j >= 0 && (tw[j] > kw[u] || (tw[j] == kw[u] && tmw[j] > km[u]))) {
+                        tw[j + 1] = tw[j];
+                        tmw[j + 1] = tmw[j];
+                        --j;
+                    }
+                    tw[j + 1] = kw[u];
+                    tmw[j + 1] = km[u];
+                    ++n_thick;
+                }
+            }
         }
         uint32_t bn = K.bits_thin[(int64_t)wd * C.cap + slot];
         while (bn) {
-            const int view = wd * 32 + __ffs(bn) - 1;
-            bn &= bn - 1;
-            const double kt = K.t[(int64_t)view * C.cap + slot];
-            int j = n_thin - 1;    // fusion.py:373-386
-            while (j >= 0 && tt[j] > kt) { tt[j + 1] = tt[j]; --j; }
-            tt[j + 1] = kt;
-            ++n_thin;
+            double kt[4];
+            int c = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (bn) {
+                    const int view = wd * 32 + __ffs(bn) - 1;
+                    bn &= bn - 1;
+                    kt[u] = K.t[(int64_t)view * C.cap + slot];
+                    c = u + 1;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (u < c) {
+                    int j = n_thin - 1;    // fusion.py:373-386
+                    while (j >= 0 && tt[j] > kt[u]) { tt[j + 1] = tt[j]; --j; }
+                    tt[j + 1] = kt[u];
+                    ++n_thin;
+                }
+            }
         }
     }
     double sw = 0.0, smw = 0.0, st = 0.0;
