@@ -177,6 +177,7 @@ fuse_gate(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__re
         unsigned bits = 0;
         for (int k = 0; k < k4; ++k)
             if (density_gate(r[k], C)) bits |= 1u << k;
+        if (__ballot_sync(0xffffffffu, bits != 0) == 0) continue;   // ~99 % of warps
         const int cnt = __popc(bits);
         int incl = cnt;
         for (int o = 1; o < 32; o <<= 1) {
