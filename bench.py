@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--slabs", default="balanced", choices=["balanced", "equal"])
+    ap.add_argument("--windows", default="on", choices=["on", "off"],
+                    help="build the fusion's scan records only inside each view's window "
+                         "around the projection of the (slab's) gated voxels")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="slab mode, N>1: occupancy all-gather fused into the fusion's stores "
                          "over NVLink (symmetric memory), or a separate NCCL all_gather")
@@ -363,6 +366,12 @@ def run_ours(args):
             except Exception as e:  # noqa: BLE001
                 gather_mode = f"nccl all_gather (symmetric memory unavailable: {type(e).__name__})"
 
+    roi = None
+    if args.windows == "on" and not views_mode:
+        roi = sharding.slab_view_rois(wl.density, pv, g, wl.origin, wl.dx, cams_t.cpu().numpy(),
+                                      [(H, W)] * nv, vox_range=(lo, hi))
+    roi_frac = roi.fraction(H, W) if roi is not None else 1.0
+
     def step(ev=None, check=False):
         nonlocal ws, bands
         if ev is not None:
@@ -374,7 +383,7 @@ def run_ours(args):
                                     aux=bands.view_slices(v0, v1, nv, H, W), planar=False)
         else:
             _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps,
-                                            params, wl.dx, aux=bands, planar=False)
+                                            params, wl.dx, aux=bands, planar=False, roi=roi)
         if ev is not None:
             ev[1].record(stream)
         if views_mode:
@@ -492,6 +501,10 @@ def run_ours(args):
         extra["parity"] = parity_check(wl, det, out["probs"].cpu().numpy(),
                                        out["n_thick"].cpu().numpy(), out["n_thin"].cpu().numpy(),
                                        dv.masks.cpu().numpy())
+        # the timed step's own output (windowed records, fused threshold) is
+        # the full fusion's, bit for bit
+        extra["parity"]["timed_step_probs_equal_full_fusion"] = bool(torch.equal(probs, out["probs"]))
+        extra["parity"]["timed_step_occ_equal_full_fusion"] = bool(torch.equal(occ_buf, out["occ"]))
 
     # --- e2e through the public API, host buffers (rank-local, N = 1 semantics) --
     e2e = None
@@ -513,9 +526,12 @@ def run_ours(args):
                    "slabs": slabs, "slab_policy": args.slabs,
                    "step": ("refine+aux(own views) + gate + bcast(gated list) + pairs(own views)"
                             " + all-gather(contributions) + reduce" if views_mode else
-                            "refine+aux(all views) + fuse(slab, threshold fused)"
+                            "refine+aux(all views; records in windows) + fuse(slab, threshold fused)"
                             + (" + all-gather(occupancy)" if world > 1 else "")),
                    "gather": gather_mode,
+                   "windows": (None if roi is None else
+                               f"scan records/bands built in per-view windows around the "
+                               f"projected gated region: {roi_frac:.3f} of the pixels"),
                    "l2": "flushed (256 MiB write) between steps, outside the events",
                    "params": "FusionParams() defaults"},
         "breakdown_ms": {"refine": refine_ms, "fuse": fuse_ms, "gather": float(np.mean(t_gath)),

@@ -84,6 +84,19 @@ int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm,
                        const float *dexp, float *out, const double *pv, double dx_vox,
                        void *records, void *bands, void *workspace, size_t workspace_bytes,
                        void *stream);
+/* As divas_refine_bands, but records and bands are built only inside one
+ * window per view: roi = DEVICE int32 [nv][4] {x0, y0, x1, y1} (inclusive
+ * pixel bounds, x0 and y0 multiples of 8), roi_w / roi_h = the largest
+ * window's width / height (grid size).  The per-view min/max of z still
+ * covers the whole view (the refinement is exactly the full one inside the
+ * window); `out`, records and bands outside the windows are left untouched.
+ * Used with the projection of a slab's gated voxels: the fusion of that slab
+ * reads no pixel outside it (sharding.slab_view_rois). */
+int divas_refine_bands_roi(int32_t nv, int64_t hm, int64_t wm,
+                           const float *mask, const float *z_surface, const int32_t *n_samples,
+                           const float *dexp, float *out, const double *pv, double dx_vox,
+                           void *records, void *bands, void *workspace, size_t workspace_bytes,
+                           const int32_t *roi, int32_t roi_w, int32_t roi_h, void *stream);
 
 /* ---------------------------------------------------------------------- */
 /* Fusion                                                                   */

@@ -9,7 +9,7 @@ entry points on top.  See DESIGN.md.
 from .geometry import Camera, SceneBounds, VoxelGrid, look_at
 from .render import ViewGeometry
 from .scene import DensityGrid
-from .segmenter import (ConfidenceMask, ViewAux, refine_bands_device, refine_mask, refine_masks,
+from .segmenter import (ConfidenceMask, ViewAux, ViewWindows, refine_bands_device, refine_mask, refine_masks,
                         refine_masks_device)
 from .fusion import (DeviceViews, FusionParams, FusionStats, Fuser, OccupancyGrid,
                      extract, extract_device, fuse, fuse_with_stats, project_grid_overlay,
@@ -24,7 +24,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Camera", "SceneBounds", "VoxelGrid", "look_at", "ViewGeometry", "DensityGrid",
-    "ConfidenceMask", "ViewAux", "refine_mask", "refine_masks", "refine_masks_device", "refine_bands_device",
+    "ConfidenceMask", "ViewAux", "ViewWindows", "refine_mask", "refine_masks", "refine_masks_device", "refine_bands_device",
     "DeviceViews", "FusionParams", "FusionStats", "Fuser", "OccupancyGrid",
     "fuse", "fuse_with_stats", "refine_and_fuse", "project_grid_overlay",
     "threshold", "threshold_device", "extract", "extract_device", "FusionSession",

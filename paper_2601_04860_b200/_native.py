@@ -26,7 +26,7 @@ EXPORTS = (
     "divas_gradient_maps", "divas_pair_trace",
     "divas_threshold_workspace_size", "divas_threshold",
     "divas_overlay", "divas_vgrid_payload",
-    "divas_last_error", "divas_abi_version",
+    "divas_last_error", "divas_abi_version", "divas_refine_bands_roi",
 )
 
 _VP = ctypes.c_void_p
@@ -68,6 +68,9 @@ def _declare(lib):
         "divas_bands_size": (S, [I32, I64, I64]),
         "divas_refine_bands": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP,
                                               ctypes.POINTER(D), D, _VP, _VP, _VP, S, _VP]),
+        "divas_refine_bands_roi": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP,
+                                                  ctypes.POINTER(D), D, _VP, _VP, _VP, S, _VP,
+                                                  I32, I32, _VP]),
         "divas_fuse_workspace_size": (S, [I64, I32, I32, I32]),
         "divas_fuse": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, S, _VP]),
         "divas_gate_count": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, _VP]),

@@ -50,14 +50,25 @@ __global__ void __launch_bounds__(256)
 band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict__ z,
           const int32_t *__restrict__ nsamp, const float *__restrict__ dexp,
           float *__restrict__ refined, const uint32_t *__restrict__ minmax,
-          double2 *__restrict__ bands, float4 *__restrict__ records, int nv) {
+          double2 *__restrict__ bands, float4 *__restrict__ records, int nv,
+          const int4 *__restrict__ roi = nullptr) {
     constexpr int TPW = kBandTile / VEC;
     const int v = nv - 1 - (int)blockIdx.z;          // reverse view order: L2 reuse of z / n
     const int64_t plane = (int64_t)B.hm * B.wm;
     const int64_t off = (int64_t)v * plane;
+    // ROI (optional): the view's tile-aligned window {x0, y0, x1, y1}; the
+    // grid covers the largest window, blocks past this view's window idle
+    int rx0 = 0, rx1 = B.wm - 1, ty = (int)blockIdx.y;
+    if (roi) {
+        const int4 w = roi[v];
+        rx0 = w.x;
+        rx1 = min(w.z, B.wm - 1);
+        ty += w.y / kBandTile;
+        if (ty * kBandTile > min(w.w, B.hm - 1)) return;
+    }
     const int chunk = blockIdx.x * blockDim.x + threadIdx.x;
-    const int x0 = chunk * VEC;
-    const bool active = x0 < B.wm;
+    const int x0 = rx0 + chunk * VEC;
+    const bool active = x0 <= rx1 && x0 < B.wm;
     bool any = false;
     double lo_ref = 0.0, span = 0.0;
     if (REFINE) {
@@ -71,7 +82,7 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
     double hi = -lo;
     if (active) {
         for (int r = 0; r < kBandTile; ++r) {
-            const int row = blockIdx.y * kBandTile + r;
+            const int row = ty * kBandTile + r;
             if (row >= B.hm) break;
             const int64_t p = off + (int64_t)row * B.wm + x0;
             float m[VEC], d[VEC];
@@ -113,7 +124,7 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
     }
     if (active && (threadIdx.x % TPW) == 0) {
         const int tx = x0 / kBandTile;
-        bands[((int64_t)v * B.nty + blockIdx.y) * B.ntx + tx] = make_double2(lo, hi);
+        bands[((int64_t)v * B.nty + ty) * B.ntx + tx] = make_double2(lo, hi);
     }
 }
 

@@ -156,11 +156,11 @@ extern "C" int divas_refine(int32_t nv, int64_t hm, int64_t wm, const float *mas
     return check_launch("divas_refine");
 }
 
-extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const float *mask,
-                                  const float *z_surface, const int32_t *n_samples,
-                                  const float *dexp, float *out, const double *pv, double dx_vox,
-                                  void *records, void *bands, void *workspace,
-                                  size_t workspace_bytes, void *stream) {
+static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *mask,
+                             const float *z_surface, const int32_t *n_samples, const float *dexp,
+                             float *out, const double *pv, double dx_vox, void *records,
+                             void *bands, void *workspace, size_t workspace_bytes,
+                             const int32_t *roi, int32_t roi_w, int32_t roi_h, void *stream) {
     if (nv <= 0 || hm <= 0 || wm <= 0) { set_error("divas_refine_bands: empty view set"); return DIVAS_EINVAL; }
     if (nv > 65535 || hm > 0x7fffffff / 2 || wm > 0x7fffffff / 2) {
         set_error("divas_refine_bands: plane too large");
@@ -183,18 +183,48 @@ extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const floa
     refine_init<<<(nv + 255) / 256, 256, 0, s>>>(ws, nv);
     dim3 grid(blocks_per_view(plane, nv), nv);
     const BandParams B = band_params(pv, dx_vox, (int)hm, (int)wm);
+    // grid extent: the whole plane, or the largest window (+ one tile of slack
+    // for a window start that is not tile aligned in the caller's numbers)
+    const int64_t gw = roi ? std::min<int64_t>(wm, (int64_t)roi_w + kBandTile) : wm;
+    const int64_t gty = roi ? std::min<int64_t>(B.nty, (roi_h + kBandTile - 1) / kBandTile + 1)
+                            : B.nty;
+    const int4 *r4 = reinterpret_cast<const int4 *>(roi);
     if (vec) {
         refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
-        dim3 bg((unsigned)((wm / 4 + 255) / 256), (unsigned)B.nty, (unsigned)nv);
+        dim3 bg((unsigned)((gw / 4 + 255) / 256), (unsigned)gty, (unsigned)nv);
         band_pass<4, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
-                                              (double2 *)bands, (float4 *)records, nv);
+                                              (double2 *)bands, (float4 *)records, nv, r4);
     } else {
         refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
-        dim3 bg((unsigned)((wm + 255) / 256), (unsigned)B.nty, (unsigned)nv);
+        dim3 bg((unsigned)((gw + 255) / 256), (unsigned)gty, (unsigned)nv);
         band_pass<1, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
-                                              (double2 *)bands, (float4 *)records, nv);
+                                              (double2 *)bands, (float4 *)records, nv, r4);
     }
     return check_launch("divas_refine_bands");
+}
+
+extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const float *mask,
+                                  const float *z_surface, const int32_t *n_samples,
+                                  const float *dexp, float *out, const double *pv, double dx_vox,
+                                  void *records, void *bands, void *workspace,
+                                  size_t workspace_bytes, void *stream) {
+    return refine_bands_impl(nv, hm, wm, mask, z_surface, n_samples, dexp, out, pv, dx_vox,
+                             records, bands, workspace, workspace_bytes, nullptr, 0, 0, stream);
+}
+
+extern "C" int divas_refine_bands_roi(int32_t nv, int64_t hm, int64_t wm, const float *mask,
+                                      const float *z_surface, const int32_t *n_samples,
+                                      const float *dexp, float *out, const double *pv,
+                                      double dx_vox, void *records, void *bands, void *workspace,
+                                      size_t workspace_bytes, const int32_t *roi, int32_t roi_w,
+                                      int32_t roi_h, void *stream) {
+    if (!roi || roi_w < 1 || roi_h < 1) {
+        set_error("divas_refine_bands_roi: empty window");
+        return DIVAS_EINVAL;
+    }
+    return refine_bands_impl(nv, hm, wm, mask, z_surface, n_samples, dexp, out, pv, dx_vox,
+                             records, bands, workspace, workspace_bytes, roi, roi_w, roi_h,
+                             stream);
 }
 
 extern "C" size_t divas_records_size(int32_t nv, int64_t hm, int64_t wm) {

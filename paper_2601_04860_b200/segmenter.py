@@ -15,8 +15,8 @@ import numpy as np
 from . import _native
 from ._device import as_device, device, empty
 
-__all__ = ["ConfidenceMask", "ViewAux", "refine_mask", "refine_masks", "refine_masks_device",
-           "refine_bands_device"]
+__all__ = ["ConfidenceMask", "ViewAux", "ViewWindows", "refine_mask", "refine_masks",
+           "refine_masks_device", "refine_bands_device"]
 
 
 @dataclass
@@ -93,14 +93,17 @@ class ViewAux:
 
 
 def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, out=None,
-                        aux=None, stream=None, planar=True):
+                        aux=None, stream=None, planar=True, roi=None):
     """``refine_masks_device`` fused with the fusion's per-view aux data.
 
     One pass over the planes writes the refined masks (``planar=True``) and
     the ``ViewAux`` (scan records + tile depth bands) that ``Fuser.run(aux=)``
     consumes, so the fusion never re-reads the planar masks.  ``aux`` may be
     a preallocated ViewAux or a pair of byte tensors (records, bands) for a
-    slice of a larger set.  Returns (out or None, aux).
+    slice of a larger set.  ``roi``: a ``ViewWindows`` -- build records and
+    bands only inside one window per view (``divas_refine_bands_roi``; the
+    planar output, if any, is also written only there).  Returns (out or
+    None, aux).
     """
     import ctypes
     import torch
@@ -127,12 +130,44 @@ def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, 
     wsb = lib.divas_refine_workspace_size(nv)
     ws = torch.empty(wsb, dtype=torch.uint8, device=masks.device)
     pvc = (ctypes.c_double * 14)(*pv.tolist())
+    if roi is not None:
+        if roi.nv != nv:
+            raise ValueError("one window per view")
+        _native.check(lib.divas_refine_bands_roi(
+            nv, hm, wm, _native.ptr(masks), _native.ptr(z_surface), _native.ptr(n_samples),
+            _native.ptr(d_exp), _native.ptr(out), pvc, float(voxel_size), _native.ptr(rec),
+            _native.ptr(bands), _native.ptr(ws), wsb, _native.ptr(roi.rects), roi.max_w,
+            roi.max_h, _native.stream_handle(stream)), "divas_refine_bands_roi")
+        return out, aux
     _native.check(lib.divas_refine_bands(nv, hm, wm, _native.ptr(masks), _native.ptr(z_surface),
                                          _native.ptr(n_samples), _native.ptr(d_exp),
                                          _native.ptr(out), pvc, float(voxel_size),
                                          _native.ptr(rec), _native.ptr(bands), _native.ptr(ws), wsb,
                                          _native.stream_handle(stream)), "divas_refine_bands")
     return out, aux
+
+
+class ViewWindows:
+    """One pixel window per view ({x0, y0, x1, y1}, inclusive, x0 / y0 on the
+    8-pixel tile grid) on the device, for ``refine_bands_device(roi=...)``."""
+
+    def __init__(self, rects, dev):
+        import torch
+        r = np.ascontiguousarray(np.asarray(rects, dtype=np.int32).reshape(-1, 4))
+        if (r[:, 0] % 8).any() or (r[:, 1] % 8).any() or (r[:, 2] < r[:, 0]).any() or \
+                (r[:, 3] < r[:, 1]).any():
+            raise ValueError("windows must be non-empty and start on the 8-pixel tile grid")
+        self.host = r
+        self.nv = int(r.shape[0])
+        self.max_w = int((r[:, 2] - r[:, 0] + 1).max())
+        self.max_h = int((r[:, 3] - r[:, 1] + 1).max())
+        self.rects = torch.from_numpy(r).to(dev)
+
+    def fraction(self, hm: int, wm: int) -> float:
+        """Share of the padded pixels inside the windows."""
+        a = (np.minimum(self.host[:, 2], wm - 1) - self.host[:, 0] + 1) * \
+            (np.minimum(self.host[:, 3], hm - 1) - self.host[:, 1] + 1)
+        return float(a.sum()) / float(self.nv * hm * wm)
 
 
 def refine_mask(mask: ConfidenceMask, view) -> ConfidenceMask:

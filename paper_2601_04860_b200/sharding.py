@@ -27,7 +27,7 @@ import numpy as np
 
 __all__ = ["slice_weights", "balanced_slabs", "equal_slabs", "slab_voxel_range",
            "broadcast_views", "gather_occupancy", "gather_slab_values",
-           "view_blocks", "ViewShardPlan", "PeerOccupancy"]
+           "view_blocks", "ViewShardPlan", "PeerOccupancy", "gated_bbox", "slab_view_rois"]
 
 # relative cost of one voxel in the dense gate pass vs one gated voxel-view pair
 STREAM_WEIGHT = 0.02
@@ -93,6 +93,77 @@ def equal_slabs(g: int, n: int):
 def slab_voxel_range(slab, g: int):
     ix0, ix1 = slab
     return ix0 * g * g, ix1 * g * g
+
+
+def gated_bbox(density, pv, g: int, vox_range=None):
+    """Inclusive (ix, iy, iz) bounds of the voxels in ``vox_range`` (an axis-0
+    slab's flat range) that pass the exact density gate, or None.  ``density``
+    is the device f32 [G^3] grid; compares widen to f64 as the kernel does."""
+    import torch
+    lo, hi = (0, g ** 3) if vox_range is None else (int(vox_range[0]), int(vox_range[1]))
+    if hi <= lo:
+        return None
+    if lo % (g * g) or hi % (g * g):
+        raise ValueError("vox_range must be whole ix slices")
+    d = density.reshape(-1)[lo:hi].reshape(-1, g, g).double()
+    m = d >= float(pv[4])
+    if float(pv[13]) != 0.0:
+        m |= d >= float(pv[5])
+    axes = []
+    for dims in ((1, 2), (0, 2), (0, 1)):
+        a = torch.nonzero(m.any(dim=dims[1]).any(dim=dims[0])).flatten()
+        if a.numel() == 0:
+            return None
+        axes.append((int(a.min()), int(a.max())))
+    (x0, x1), (y0, y1), (z0, z1) = axes
+    ix0 = lo // (g * g)
+    return (x0 + ix0, y0, z0), (x1 + ix0, y1, z1)
+
+
+def slab_view_rois(density, pv, g: int, origin, dx: float, cams, sizes, vox_range=None,
+                   margin: int = 4):
+    """Per-view pixel windows outside which the fusion of ``vox_range`` reads
+    no record or band: the projection of the gated voxels' bounding box (a
+    convex set in front of the camera projects inside the hull of its
+    corners' projections; every footprint, centre pixel and gradient
+    neighbour lies inside), widened by ``margin`` px, x0 / y0 snapped to the
+    8-pixel tile grid.  A view with a bbox corner at or behind the camera
+    plane keeps its whole plane.  Returns a ``segmenter.ViewWindows``."""
+    from .segmenter import ViewWindows
+    cams = np.asarray(cams, dtype=np.float64).reshape(-1, 18)
+    bb = gated_bbox(density, pv, g, vox_range)
+    rects = np.zeros((len(cams), 4), dtype=np.int64)
+    origin = np.asarray(origin, dtype=np.float64).reshape(3)
+    for v, c in enumerate(cams):
+        h, w = (int(sizes[v][0]), int(sizes[v][1]))
+        full = (0, 0, w - 1, h - 1)
+        if bb is None:
+            rects[v] = (0, 0, min(7, w - 1), min(7, h - 1))   # nothing gated: one idle tile
+            continue
+        lo = origin + np.asarray(bb[0], dtype=np.float64) * dx
+        hi = origin + (np.asarray(bb[1], dtype=np.float64) + 1.0) * dx
+        corners = np.array([[(lo, hi)[(j >> a) & 1][a] for a in range(3)] for j in range(8)])
+        R = c[:9].reshape(3, 3)
+        rel = corners - c[9:12]
+        xc, yc, dep = rel @ R[:, 0], rel @ R[:, 1], -(rel @ R[:, 2])
+        scale = np.abs(corners).sum(axis=1).max() + np.abs(c[9:12]).sum()
+        if (dep <= 1e-9 * max(scale, 1.0)).any():
+            rects[v] = full
+            continue
+        fx, fy, cx, cy = c[12:16]
+        u = fx * (xc / dep) + cx
+        vv = cy - fy * (yc / dep)
+        x0 = int(np.floor(u.min())) - margin
+        x1 = int(np.ceil(u.max())) + margin
+        y0 = int(np.floor(vv.min())) - margin
+        y1 = int(np.ceil(vv.max())) + margin
+        if x1 < 0 or y1 < 0 or x0 > w - 1 or y0 > h - 1:
+            rects[v] = (0, 0, min(7, w - 1), min(7, h - 1))   # projects outside the view
+            continue
+        x0, y0 = max(0, x0) // 8 * 8, max(0, y0) // 8 * 8
+        x1, y1 = min(w - 1, x1 | 7), min(h - 1, y1 | 7)
+        rects[v] = (x0, y0, x1, y1)
+    return ViewWindows(rects, density.device)
 
 
 def broadcast_views(views, src: int = 0, group=None):
