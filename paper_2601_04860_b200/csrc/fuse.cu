@@ -872,6 +872,12 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
 // ---------------------------------------------------------------------------
 // reduction: value-sorted sums per voxel
 // ---------------------------------------------------------------------------
+// bits of views [lo, hi) within 32-bit word wd
+__device__ __forceinline__ uint32_t view_word_mask(int wd, int view_lo, int view_hi) {
+    const int a = max(view_lo - wd * 32, 0), b = min(view_hi - wd * 32, 32);
+    return ((b >= 32) ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << a) - 1u);
+}
+
 constexpr int kReduceThreads = 128;
 
 __device__ __forceinline__ void reduce_store(const FuseConst &C, const FuseOut &O, uint32_t vi,
@@ -959,13 +965,24 @@ __device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &
     reduce_store(C, O, work[slot], n_thick, n_thin, sw, smw, st);
 }
 
+// dirty != NULL (incremental update of views [view_lo, view_hi)): only slots
+// that held or now hold a contribution of those views are re-reduced; the
+// others' outputs are already those of the unchanged contribution set.
 template <int MAXV>
 __global__ void __launch_bounds__(kReduceThreads)
 fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work,
-            const WsHeader *__restrict__ hdr) {
+            const WsHeader *__restrict__ hdr, const uint8_t *__restrict__ dirty, int view_lo,
+            int view_hi) {
     const long long n = min((long long)hdr->count, (long long)C.cap);
     const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (slot >= n) return;
+    if (dirty && !dirty[slot]) {
+        uint32_t now = 0;
+        for (int wd = view_lo >> 5; wd <= (view_hi - 1) >> 5; ++wd)
+            now |= (K.bits_thick[(int64_t)wd * C.cap + slot] | K.bits_thin[(int64_t)wd * C.cap + slot]) &
+                   view_word_mask(wd, view_lo, view_hi);
+        if (!now) return;
+    }
     reduce_local<MAXV>(C, K, O, work, slot);
 }
 
@@ -1152,17 +1169,23 @@ __global__ void pair_trace_kernel(divas_trace_args A, FuseConst C) {
 
 // Incremental updates: drop the contribution bits of views [lo, hi) before
 // they are re-evaluated.
+// Clears the bits of views [lo, hi); dirty[slot] = the slot had one of them
+// (its sums change even if the re-evaluated views add nothing back).
 __global__ void clear_view_bits(Contrib K, int64_t cap, int view_lo, int view_hi,
-                                const WsHeader *__restrict__ hdr) {
+                                const WsHeader *__restrict__ hdr, uint8_t *__restrict__ dirty) {
     const long long n = min((long long)hdr->count, (long long)cap);
     for (long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x; slot < n;
          slot += (long long)gridDim.x * blockDim.x) {
+        uint32_t had = 0;
         for (int wd = view_lo >> 5; wd <= (view_hi - 1) >> 5; ++wd) {
-            const int a = max(view_lo - wd * 32, 0), b = min(view_hi - wd * 32, 32);
-            const uint32_t keep = ~(((b >= 32) ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << a) - 1u));
-            K.bits_thick[(int64_t)wd * cap + slot] &= keep;
-            K.bits_thin[(int64_t)wd * cap + slot] &= keep;
+            const uint32_t m = view_word_mask(wd, view_lo, view_hi);
+            const uint32_t bt = K.bits_thick[(int64_t)wd * cap + slot];
+            const uint32_t bn = K.bits_thin[(int64_t)wd * cap + slot];
+            had |= (bt | bn) & m;
+            if (bt & m) K.bits_thick[(int64_t)wd * cap + slot] = bt & ~m;
+            if (bn & m) K.bits_thin[(int64_t)wd * cap + slot] = bn & ~m;
         }
+        dirty[slot] = had ? 1 : 0;
     }
 }
 
@@ -1170,7 +1193,7 @@ __global__ void clear_view_bits(Contrib K, int64_t cap, int view_lo, int view_hi
 // workspace layout
 // ---------------------------------------------------------------------------
 struct WsLayout {
-    size_t work, bits_thick, bits_thin, w, mw, t, rec, bands, total;
+    size_t work, bits_thick, bits_thin, w, mw, t, dirty, rec, bands, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1186,6 +1209,7 @@ static WsLayout ws_layout(int64_t cap, int32_t nv_cap, int32_t hm, int32_t wm) {
     L.w = off;          off = align256(off + (size_t)nv_cap * c * 8);
     L.mw = off;         off = align256(off + (size_t)nv_cap * c * 8);
     L.t = off;          off = align256(off + (size_t)nv_cap * c * 8);
+    L.dirty = off;      off = align256(off + c);
     L.rec = off;        off = align256(off + record_bytes(nv_cap, hm, wm));
     L.bands = off;      off = align256(off + band_bytes(nv_cap, hm, wm));
     L.total = off;
@@ -1383,7 +1407,8 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     }
     if (steps & DIVAS_STEP_CLEAR_VIEWS) {
         const int64_t blocks = std::min<int64_t>((cap + 255) / 256, (int64_t)sm_count() * 8);
-        clear_view_bits<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(K, cap, v0, v1, hdr);
+        clear_view_bits<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
+            K, cap, v0, v1, hdr, (uint8_t *)(ws + L.dirty));
         if ((rc = check_launch("divas_fuse(clear)"))) return rc;
     }
     if (steps & DIVAS_STEP_PAIRS) {
@@ -1397,11 +1422,17 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     if (steps & DIVAS_STEP_REDUCE) {
         const unsigned rblocks =
             (unsigned)std::max<int64_t>((cap + kReduceThreads - 1) / kReduceThreads, 1);
-        if (a->nv <= 32) fuse_reduce<32><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
-        else if (a->nv <= 64) fuse_reduce<64><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
-        else if (a->nv <= 128) fuse_reduce<128><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
-        else if (a->nv <= 256) fuse_reduce<256><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
-        else fuse_reduce<1024><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr);
+        // incremental (CLEAR_VIEWS + REDUCE in one call): only dirty slots
+        const uint8_t *dirty = ((steps & DIVAS_STEP_CLEAR_VIEWS) && (steps & DIVAS_STEP_PAIRS))
+                                   ? (const uint8_t *)(ws + L.dirty) : nullptr;
+#define DIVAS_REDUCE(MV) \
+        fuse_reduce<MV><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr, dirty, v0, v1)
+        if (a->nv <= 32) DIVAS_REDUCE(32);
+        else if (a->nv <= 64) DIVAS_REDUCE(64);
+        else if (a->nv <= 128) DIVAS_REDUCE(128);
+        else if (a->nv <= 256) DIVAS_REDUCE(256);
+        else DIVAS_REDUCE(1024);
+#undef DIVAS_REDUCE
         if ((rc = check_launch("divas_fuse(reduce)"))) return rc;
     }
     return DIVAS_OK;

@@ -65,6 +65,7 @@ class FusionSession:
         self._cap = self.fuser.capacity(self.density, 0, self.g ** 3)
         self._fused = False
         self._out = None
+        self._graphs = {}          # (view, nv) -> CUDA graph of its re-refine + re-fuse
 
     # -- state ---------------------------------------------------------------
     def _views(self):
@@ -124,6 +125,7 @@ class FusionSession:
         for k, (vg, m) in enumerate(pairs):
             self._upload(v0 + k, vg, m)
         self.nv += len(pairs)
+        self._graphs.clear()       # captured launches carry the old view count
         self._refine(v0, self.nv)
         self._fuse(v0, self.nv)
 
@@ -150,17 +152,41 @@ class FusionSession:
         self._refine(index, index + 1)
         self._fuse(index, index + 1)
 
-    def replace_mask_device(self, index, raw_plane):
+    def replace_mask_device(self, index, raw_plane, graph=True):
         """As ``replace_mask`` with the new raw mask already on the device
-        (a [h, w] float32 CUDA tensor); no host synchronisation."""
+        (a [h, w] float32 CUDA tensor); no host synchronisation.
+
+        ``graph``: the view's re-refine + re-fuse launches (refine init /
+        min-max / band pass, clear bits, pair kernel, reduction) are captured
+        once into a CUDA graph and replayed, so an update costs one graph
+        launch instead of the Python / driver overhead of six kernel launches.
+        """
+        import torch
         if not 0 <= index < self.nv:
             raise IndexError(index)
         h, w = self.sizes[index]
         if tuple(raw_plane.shape) != (h, w):
             raise ValueError("mask and view dimensions differ")
         self.raw[index, :h, :w].copy_(raw_plane)
-        self._refine(index, index + 1)
-        self._fuse(index, index + 1)
+        if not (graph and self._fused):
+            self._refine(index, index + 1)
+            self._fuse(index, index + 1)
+            return
+        key = (index, self.nv)
+        g = self._graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(device=self.dev)
+            side.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(side):             # warm the allocator outside capture
+                self._refine(index, index + 1)
+                self._fuse(index, index + 1)
+            torch.cuda.current_stream(self.dev).wait_stream(side)
+            with torch.cuda.graph(g):
+                self._refine(index, index + 1)
+                self._fuse(index, index + 1)
+            self._graphs[key] = g
+        g.replay()
 
     def refuse(self):
         """Full recompute of the current view set (same result, for checking)."""

@@ -74,3 +74,32 @@ def test_mixed_resolution_session():
     s.add_views(pairs[:2])
     order = [pairs[2], pairs[0], pairs[1]]
     assert np.array_equal(s.occupancy_grid().probs, _full(grid, dens, order, params, bounds))
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_replace_mask_device_graph_replay(scene, graph):
+    """Device-side replacements, replayed from captured CUDA graphs (a view's
+    graph is reused across updates with new masks) or launched eagerly, give
+    the full recompute's bits; adding a view invalidates the graphs."""
+    import torch
+    from paper_2601_04860_b200 import ConfidenceMask, FusionSession
+    grid, dens, pairs, params, bounds = scene
+    h, w = pairs[0][0].z_surface.shape
+    s = FusionSession(grid, dens, params, (h, w), bounds=bounds, max_views=8)
+    s.add_views(pairs[:4])
+    rng = np.random.default_rng(11)
+    cur = list(pairs[:4])
+    for it in range(8):
+        i = it % 3                                  # views 0..2 reuse their graphs
+        vals = np.clip(cur[i][1].values * rng.uniform(0.3, 1.5), 0, 1).astype(np.float32)
+        s.replace_mask_device(i, torch.from_numpy(vals).to(s.dev), graph=graph)
+        cur[i] = (cur[i][0], ConfidenceMask(vals))
+        assert np.array_equal(s.occupancy_grid().probs, _full(grid, dens, cur, params, bounds))
+    assert (len(s._graphs) == 3) == graph
+    s.add_views(pairs[4:5])
+    cur.append(pairs[4])
+    assert not s._graphs
+    vals = np.clip(cur[0][1].values * 0.7, 0, 1).astype(np.float32)
+    s.replace_mask_device(0, torch.from_numpy(vals).to(s.dev), graph=graph)
+    cur[0] = (cur[0][0], ConfidenceMask(vals))
+    assert np.array_equal(s.occupancy_grid().probs, _full(grid, dens, cur, params, bounds))
