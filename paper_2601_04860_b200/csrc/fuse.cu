@@ -37,6 +37,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include <cstdio>
+
 #include "bands.cuh"
 
 namespace divas {
@@ -387,6 +389,19 @@ __device__ __forceinline__ int cert_axis(double Ua, double E, double n, long lon
 // ---------------------------------------------------------------------------
 constexpr int kPairThreads = 256;
 
+// Debug builds (-DDIVAS_CHECK=1, tests only): trap on any out-of-range read.
+#if DIVAS_CHECK
+#define DIVAS_BOUND(ptr, base, n)                                                          \
+    do {                                                                                   \
+        if ((ptr) < (base) || (ptr) >= (base) + (n)) {                                     \
+            printf("divas bound check failed at %s:%d\n", __FILE__, __LINE__);              \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define DIVAS_BOUND(ptr, base, n) ((void)0)
+#endif
+
 #if DIVAS_STATS
 // experiment builds only: per-stage pair counters (tools/pair_stats.py)
 __device__ unsigned long long g_pair_stats[24];
@@ -511,6 +526,7 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
         double2 b[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
+            DIVAS_BOUND(bp, M.bands + (int64_t)view * C.nty * C.ntx, (int64_t)C.nty * C.ntx);
             b[j] = __ldg(bp);
             if (i0 + j + 1 < nt) {
                 ++bp;
@@ -666,6 +682,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     if (cu == 2 || cv == 2) PSTAT(14, 1);
     const int64_t vplane = (int64_t)view * C.hm * C.wm;
     const int64_t pix = vplane + py * (int64_t)C.wm + px;
+    DIVAS_BOUND(M.rec + pix, M.rec + (int64_t)view * C.hm * C.wm, (int64_t)C.hm * C.wm);
     const float4 rc = __ldg(M.rec + pix);                      // {m, d_exp, tau32, n}
     const int32_t ns = __float_as_int(rc.w);
     if (ns <= 0) return false;                                 // valids[view, py, px] == 0
@@ -688,6 +705,8 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
             // missing neighbour reads the centre itself (|d - d| = 0 never
             // raises the max, exactly like skipping it)
             const float *de = M.dexps + pix;
+            DIVAS_BOUND(de - (px > 0 ? 1 : 0), M.dexps + vplane, (int64_t)C.hm * C.wm);
+            DIVAS_BOUND(de + (py < C.hm - 1 ? C.wm : 0), M.dexps + vplane, (int64_t)C.hm * C.wm);
             const float dmin = __ldg(M.dmins + pix), dmax = __ldg(M.dmaxs + pix);
             const float nl = __ldg(de - (px > 0 ? 1 : 0));
             const float nr = __ldg(de + (px < C.wm - 1 ? 1 : 0));
@@ -789,6 +808,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     int left = bw;
 #pragma unroll 4
     for (int i = 0; i < npix; ++i) {
+        DIVAS_BOUND(pp, M.rec + (int64_t)view * C.hm * C.wm, (int64_t)C.hm * C.wm);
         const float4 r = __ldg(pp);
         mmax = fmaxf(mmax, r.x);
         const float e = fabsf(xd32 - r.y) - r.z;
