@@ -117,87 +117,207 @@ __device__ __forceinline__ bool density_gate(float rho, const FuseConst &C) {
     return r >= C.rho_thr || (C.enable_thin && r >= C.rho_thin);
 }
 
-// Each thread owns 4 consecutive voxels (one float4 of rho).  The loop walks
-// warp-uniform strides so all 32 lanes reach the shuffles together.
-__global__ void __launch_bounds__(kGateThreads)
-fuse_gate(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__restrict__ work,
-          WsHeader *__restrict__ hdr, int count_only) {
-    const int lane = threadIdx.x & 31;
-    const int64_t n = C.hi - C.lo;
-    const int64_t nquads = (n + 3) / 4;
-    const bool aligned = (C.lo & 3) == 0;
+// One quad = 4 consecutive voxels of [lo, hi) starting at `base`: loads rho
+// (one float4 when aligned), zeroes the outputs (unless count_only) and
+// returns the density-gate bits of its k4 <= 4 voxels.
+__device__ __forceinline__ unsigned gate_quad(const float *__restrict__ dens, const FuseConst &C,
+                                              const FuseOut &O, int64_t base, bool aligned,
+                                              bool count_only) {
+    if (base >= C.hi) return 0u;
+    const int64_t left = C.hi - base;
+    const int k4 = left < 4 ? (int)left : 4;
     const uint8_t occ0 = (0.0 >= C.occ_thr) ? 1 : 0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); wbase < nquads;
-         wbase += stride) {
-        const int64_t q = wbase + lane;
-        const int64_t base = C.lo + 4 * q;
-        float r[4] = {0.f, 0.f, 0.f, 0.f};
-        int k4 = 0;
-        if (q < nquads) {
-            const int64_t left = C.hi - base;
-            k4 = left < 4 ? (int)left : 4;
-            if (aligned && k4 == 4) {
-                const float4 v = __ldg(reinterpret_cast<const float4 *>(dens + base));
-                r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
-            } else {
-                for (int k = 0; k < k4; ++k) r[k] = __ldg(dens + base + k);
+    float r[4] = {0.f, 0.f, 0.f, 0.f};
+    if (aligned && k4 == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4 *>(dens + base));
+        r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
+    } else {
+        for (int k = 0; k < k4; ++k) r[k] = __ldg(dens + base + k);
+    }
+    if (!count_only) {
+        if (aligned && k4 == 4) {
+            const double2 z2 = make_double2(0.0, 0.0);
+            if (O.probs) {
+                __stcs(reinterpret_cast<double2 *>(O.probs + base), z2);
+                __stcs(reinterpret_cast<double2 *>(O.probs + base) + 1, z2);
             }
-            if (!count_only) {
-                if (aligned && k4 == 4) {
-                    const double2 z2 = make_double2(0.0, 0.0);
-                    if (O.probs) {
-                        __stcs(reinterpret_cast<double2 *>(O.probs + base), z2);
-                        __stcs(reinterpret_cast<double2 *>(O.probs + base) + 1, z2);
-                    }
-                    if (O.n_thick) *reinterpret_cast<int4 *>(O.n_thick + base) = make_int4(0, 0, 0, 0);
-                    if (O.n_thin) *reinterpret_cast<int4 *>(O.n_thin + base) = make_int4(0, 0, 0, 0);
-                    double *sums[3] = {O.sw, O.smw, O.st};
-                    for (int s = 0; s < 3; ++s)
-                        if (sums[s]) {
-                            reinterpret_cast<double2 *>(sums[s] + base)[0] = z2;
-                            reinterpret_cast<double2 *>(sums[s] + base)[1] = z2;
-                        }
-                    if (O.occ) *reinterpret_cast<uchar4 *>(O.occ + base) = make_uchar4(occ0, occ0, occ0, occ0);
-                    for (int r = 0; r < O.n_peers; ++r)       // NVLink stores to every rank
-                        *reinterpret_cast<uchar4 *>(O.occ_peers[r] + base) =
-                            make_uchar4(occ0, occ0, occ0, occ0);
-                } else {
-                    for (int k = 0; k < k4; ++k) {
-                        if (O.probs) O.probs[base + k] = 0.0;
-                        if (O.n_thick) O.n_thick[base + k] = 0;
-                        if (O.n_thin) O.n_thin[base + k] = 0;
-                        if (O.sw) O.sw[base + k] = 0.0;
-                        if (O.smw) O.smw[base + k] = 0.0;
-                        if (O.st) O.st[base + k] = 0.0;
-                        if (O.occ) O.occ[base + k] = occ0;
-                        for (int r = 0; r < O.n_peers; ++r) O.occ_peers[r][base + k] = occ0;
-                    }
+            if (O.n_thick) *reinterpret_cast<int4 *>(O.n_thick + base) = make_int4(0, 0, 0, 0);
+            if (O.n_thin) *reinterpret_cast<int4 *>(O.n_thin + base) = make_int4(0, 0, 0, 0);
+            double *sums[3] = {O.sw, O.smw, O.st};
+            for (int s = 0; s < 3; ++s)
+                if (sums[s]) {
+                    reinterpret_cast<double2 *>(sums[s] + base)[0] = z2;
+                    reinterpret_cast<double2 *>(sums[s] + base)[1] = z2;
                 }
+            if (O.occ) *reinterpret_cast<uchar4 *>(O.occ + base) = make_uchar4(occ0, occ0, occ0, occ0);
+            for (int p = 0; p < O.n_peers; ++p)           // NVLink stores to every rank
+                *reinterpret_cast<uchar4 *>(O.occ_peers[p] + base) =
+                    make_uchar4(occ0, occ0, occ0, occ0);
+        } else {
+            for (int k = 0; k < k4; ++k) {
+                if (O.probs) O.probs[base + k] = 0.0;
+                if (O.n_thick) O.n_thick[base + k] = 0;
+                if (O.n_thin) O.n_thin[base + k] = 0;
+                if (O.sw) O.sw[base + k] = 0.0;
+                if (O.smw) O.smw[base + k] = 0.0;
+                if (O.st) O.st[base + k] = 0.0;
+                if (O.occ) O.occ[base + k] = occ0;
+                for (int p = 0; p < O.n_peers; ++p) O.occ_peers[p][base + k] = occ0;
             }
         }
-        unsigned bits = 0;
-        for (int k = 0; k < k4; ++k)
-            if (density_gate(r[k], C)) bits |= 1u << k;
-        if (__ballot_sync(0xffffffffu, bits != 0) == 0) continue;   // ~99 % of warps
-        const int cnt = __popc(bits);
-        int incl = cnt;
+    }
+    unsigned bits = 0;
+    for (int k = 0; k < k4; ++k)
+        if (density_gate(r[k], C)) bits |= 1u << k;
+    return bits;
+}
+
+// Counting pass (divas_gate_count): grid-stride over quads, one atomic per
+// warp that found gated voxels.
+__global__ void __launch_bounds__(kGateThreads)
+fuse_gate_count(const float *__restrict__ dens, FuseConst C, WsHeader *__restrict__ hdr) {
+    const int64_t nquads = (C.hi - C.lo + 3) / 4;
+    const bool aligned = (C.lo & 3) == 0;
+    const FuseOut none{};
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+         q - (threadIdx.x & 31) < nquads; q += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned bits = q < nquads ? gate_quad(dens, C, none, C.lo + 4 * q, aligned, true) : 0u;
+        int cnt = __popc(bits);
+        if (__ballot_sync(0xffffffffu, cnt != 0) == 0) continue;
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&hdr->count, (unsigned long long)cnt);
+    }
+}
+
+// Ordered gate, pass 1: tiles of kGateTile voxels; zero the outputs and count
+// each tile's gated voxels.  Quad j of a tile is handled by thread j % 256 in
+// round j / 256, so the rounds walk the tile in C order.
+#ifndef DIVAS_GATE_ROUNDS
+#define DIVAS_GATE_ROUNDS 4
+#endif
+constexpr int kGateRounds = DIVAS_GATE_ROUNDS;     // quads per thread per tile
+constexpr int kGateTile = 4 * kGateRounds * kGateThreads;
+constexpr int64_t kGateTileMax = (1LL << 32) / kGateTile;   // tiles of any u32 voxel range
+
+__global__ void __launch_bounds__(kGateThreads)
+gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__restrict__ tiles) {
+    __shared__ int s_w[kGateThreads / 32];
+    const bool aligned = (C.lo & 3) == 0;
+    const int64_t t0 = C.lo + (int64_t)blockIdx.x * kGateTile;
+    int cnt = 0;
+#pragma unroll
+    for (int r = 0; r < kGateRounds; ++r)
+        cnt += __popc(gate_quad(dens, C, O, t0 + 4 * (r * kGateThreads + (int)threadIdx.x), aligned,
+                                false));
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < kGateThreads / 32; ++w) t += s_w[w];
+        tiles[blockIdx.x] = (uint32_t)t;
+    }
+}
+
+// pass 2 (one CTA): exclusive scan of the tile counts in place; the total is
+// the gated count, beyond `cap` the overflow flag
+__global__ void __launch_bounds__(1024)
+gate_scan(uint32_t *__restrict__ tiles, int64_t ntiles, int64_t cap, WsHeader *__restrict__ hdr) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t b = 0; b < ntiles; b += blockDim.x) {
+        const int64_t i = b + threadIdx.x;
+        const unsigned long long v = i < ntiles ? tiles[i] : 0ull;
+        unsigned long long incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_w[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const unsigned long long w = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0ull;
+            unsigned long long wi = w;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
+            }
+            s_w[lane] = wi - w;
+        }
+        __syncthreads();
+        const unsigned long long carry = s_carry;
+        if (i < ntiles) tiles[i] = (uint32_t)(carry + s_w[warp] + incl - v);
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = carry + s_w[warp] + incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        hdr->count = s_carry;
+        hdr->overflow = s_carry > (unsigned long long)cap ? 1u : 0u;
+    }
+}
+
+// pass 3: each gated voxel's C-order rank -> its slot (deterministic order);
+// tiles without a gated voxel (most of the grid) return at once
+__global__ void __launch_bounds__(kGateThreads)
+gate_emit(const float *__restrict__ dens, FuseConst C, const uint32_t *__restrict__ tiles,
+          int64_t ntiles, const WsHeader *__restrict__ hdr, uint32_t *__restrict__ work) {
+    constexpr int NW = kGateThreads / 32;
+    constexpr int NC = kGateRounds * NW;               // (round, warp) chunks, C order
+    static_assert(NC % 32 == 0, "chunk scan");
+    __shared__ int s_pre[NC];
+    const int64_t off = tiles[blockIdx.x];
+    const int64_t end = (int64_t)blockIdx.x + 1 < ntiles ? (int64_t)tiles[blockIdx.x + 1]
+                                                          : (int64_t)hdr->count;
+    if (end == off) return;
+    const bool aligned = (C.lo & 3) == 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t t0 = C.lo + (int64_t)blockIdx.x * kGateTile;
+    const FuseOut none{};
+    unsigned bits[kGateRounds];
+    int lp[kGateRounds];
+#pragma unroll
+    for (int r = 0; r < kGateRounds; ++r) {
+        bits[r] = gate_quad(dens, C, none, t0 + 4 * (r * kGateThreads + (int)threadIdx.x), aligned,
+                            true);
+        const int c = __popc(bits[r]);
+        int incl = c;
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        if (total == 0) continue;
-        unsigned long long slot = 0;
-        if (lane == 31) slot = atomicAdd(&hdr->count, (unsigned long long)total);
-        slot = __shfl_sync(0xffffffffu, slot, 31) + (unsigned long long)(incl - cnt);
-        if (count_only) continue;
-        while (bits) {
-            const int k = __ffs(bits) - 1;
-            bits &= bits - 1;
-            if ((long long)slot < C.cap) work[slot] = (uint32_t)(base + k);
-            else hdr->overflow = 1u;
-            ++slot;
+        lp[r] = incl - c;
+        if (lane == 31) s_pre[r * NW + warp] = incl;
+    }
+    __syncthreads();
+    if (warp == 0) {   // exclusive scan of the chunk totals, NC / 32 per lane
+        constexpr int PER = NC / 32;
+        int v[PER], sum = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) { v[k] = s_pre[lane * PER + k]; sum += v[k]; }
+        int incl = sum;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int run = incl - sum;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) { s_pre[lane * PER + k] = run; run += v[k]; }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kGateRounds; ++r) {
+        unsigned b = bits[r];
+        int64_t pos = off + s_pre[r * NW + warp] + lp[r];
+        const int64_t base = t0 + 4 * (r * kGateThreads + (int)threadIdx.x);
+        while (b) {
+            const int k = __ffs(b) - 1;
+            b &= b - 1;
+            if (pos < C.cap) work[pos] = (uint32_t)(base + k);
+            ++pos;
         }
     }
 }
@@ -1213,7 +1333,7 @@ __global__ void clear_view_bits(Contrib K, int64_t cap, int view_lo, int view_hi
 // workspace layout
 // ---------------------------------------------------------------------------
 struct WsLayout {
-    size_t work, bits_thick, bits_thin, w, mw, t, dirty, rec, bands, total;
+    size_t work, bits_thick, bits_thin, w, mw, t, dirty, gtiles, rec, bands, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1230,6 +1350,7 @@ static WsLayout ws_layout(int64_t cap, int32_t nv_cap, int32_t hm, int32_t wm) {
     L.mw = off;         off = align256(off + (size_t)nv_cap * c * 8);
     L.t = off;          off = align256(off + (size_t)nv_cap * c * 8);
     L.dirty = off;      off = align256(off + c);
+    L.gtiles = off;     off = align256(off + (size_t)kGateTileMax * 4);
     L.rec = off;        off = align256(off + record_bytes(nv_cap, hm, wm));
     L.bands = off;      off = align256(off + band_bytes(nv_cap, hm, wm));
     L.total = off;
@@ -1273,14 +1394,23 @@ static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     C.occ_thr = a->occ_thr;
 }
 
-static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O, uint32_t *work,
-                        WsHeader *hdr, int count_only, cudaStream_t s) {
-    const int64_t n = C.hi - C.lo;
-    const int64_t nquads = (n + 3) / 4;
+static void launch_gate_count(const FuseConst &C, const float *dens, WsHeader *hdr,
+                              cudaStream_t s) {
+    const int64_t nquads = (C.hi - C.lo + 3) / 4;
     int64_t blocks = (nquads + kGateThreads - 1) / kGateThreads;
     blocks = std::min<int64_t>(blocks, (int64_t)sm_count() * 16);
-    fuse_gate<<<(unsigned)std::max<int64_t>(blocks, 1), kGateThreads, 0, s>>>(dens, C, O, work,
-                                                                             hdr, count_only);
+    fuse_gate_count<<<(unsigned)std::max<int64_t>(blocks, 1), kGateThreads, 0, s>>>(dens, C, hdr);
+}
+
+// The ordered gate: slots hold the gated voxels in C order, so a pair CTA's
+// 256 slots are spatially adjacent voxels (their footprints overlap: L1 reuse)
+// and the slot order is reproducible.
+static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O, uint32_t *work,
+                        WsHeader *hdr, uint32_t *tiles, cudaStream_t s) {
+    const int64_t ntiles = (C.hi - C.lo + kGateTile - 1) / kGateTile;
+    gate_tiles<<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, O, tiles);
+    gate_scan<<<1, 1024, 0, s>>>(tiles, ntiles, C.cap, hdr);
+    gate_emit<<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, tiles, ntiles, hdr, work);
 }
 
 // records + bands of views [v0, v0 + cnt) from planar refined masks
@@ -1345,10 +1475,7 @@ extern "C" int divas_gate_count(const divas_fuse_args *a, void *workspace, void 
     WsHeader *hdr = (WsHeader *)workspace;
     if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess)
         return check_launch("divas_gate_count(memset)");
-    if (a->vox_hi > a->vox_lo) {
-        FuseOut O{};
-        launch_gate(C, a->density, O, nullptr, hdr, 1, s);
-    }
+    if (a->vox_hi > a->vox_lo) launch_gate_count(C, a->density, hdr, s);
     return check_launch("divas_gate_count");
 }
 
@@ -1418,7 +1545,7 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     if (steps & DIVAS_STEP_GATE) {
         if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess)
             return check_launch("divas_fuse(memset)");
-        launch_gate(C, a->density, O, work, hdr, 0, s);
+        launch_gate(C, a->density, O, work, hdr, (uint32_t *)(ws + L.gtiles), s);
         if ((rc = check_launch("divas_fuse(gate)"))) return rc;
     }
     if (steps & DIVAS_STEP_CLEAR_ALL) {
