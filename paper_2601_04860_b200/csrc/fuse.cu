@@ -117,25 +117,25 @@ __device__ __forceinline__ bool density_gate(float rho, const FuseConst &C) {
     return r >= C.rho_thr || (C.enable_thin && r >= C.rho_thin);
 }
 
-// One quad = 4 consecutive voxels of [lo, hi) starting at `base`: loads rho
-// (one float4 when aligned), zeroes the outputs (unless count_only) and
-// returns the density-gate bits of its k4 <= 4 voxels.
+// One quad = up to 4 consecutive voxels base + [k0, k1) (k0 > 0 or k1 < 4 where
+// the range or the grid row ends): loads rho (one float4 when the whole quad
+// is valid and aligned), zeroes the outputs (unless count_only) and returns
+// the density-gate bits of the valid voxels.
 __device__ __forceinline__ unsigned gate_quad(const float *__restrict__ dens, const FuseConst &C,
-                                              const FuseOut &O, int64_t base, bool aligned,
-                                              bool count_only) {
-    if (base >= C.hi) return 0u;
-    const int64_t left = C.hi - base;
-    const int k4 = left < 4 ? (int)left : 4;
+                                              const FuseOut &O, int64_t base, int k0, int k1,
+                                              bool vec_ok, bool count_only) {
+    if (k1 <= k0) return 0u;
+    const bool full = vec_ok && k0 == 0 && k1 == 4;
     const uint8_t occ0 = (0.0 >= C.occ_thr) ? 1 : 0;
     float r[4] = {0.f, 0.f, 0.f, 0.f};
-    if (aligned && k4 == 4) {
+    if (full) {
         const float4 v = __ldg(reinterpret_cast<const float4 *>(dens + base));
         r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
     } else {
-        for (int k = 0; k < k4; ++k) r[k] = __ldg(dens + base + k);
+        for (int k = k0; k < k1; ++k) r[k] = __ldg(dens + base + k);
     }
     if (!count_only) {
-        if (aligned && k4 == 4) {
+        if (full) {
             const double2 z2 = make_double2(0.0, 0.0);
             if (O.probs) {
                 __stcs(reinterpret_cast<double2 *>(O.probs + base), z2);
@@ -154,7 +154,7 @@ __device__ __forceinline__ unsigned gate_quad(const float *__restrict__ dens, co
                 *reinterpret_cast<uchar4 *>(O.occ_peers[p] + base) =
                     make_uchar4(occ0, occ0, occ0, occ0);
         } else {
-            for (int k = 0; k < k4; ++k) {
+            for (int k = k0; k < k1; ++k) {
                 if (O.probs) O.probs[base + k] = 0.0;
                 if (O.n_thick) O.n_thick[base + k] = 0;
                 if (O.n_thin) O.n_thin[base + k] = 0;
@@ -167,21 +167,58 @@ __device__ __forceinline__ unsigned gate_quad(const float *__restrict__ dens, co
         }
     }
     unsigned bits = 0;
-    for (int k = 0; k < k4; ++k)
+    for (int k = k0; k < k1; ++k)
         if (density_gate(r[k], C)) bits |= 1u << k;
     return bits;
 }
 
+// A flat-range quad (the counting pass): voxels [base, base + 4) cut to [lo, hi)
+__device__ __forceinline__ unsigned gate_flat_quad(const float *__restrict__ dens,
+                                                   const FuseConst &C, const FuseOut &O,
+                                                   int64_t base, bool count_only) {
+    const int64_t left = C.hi - base;
+    const int k1 = left < 4 ? (int)left : 4;
+    return gate_quad(dens, C, O, base, 0, k1, (C.lo & 3) == 0, count_only);
+}
+
+// Brick tiles for the ordered gate: 16 x 16 x 16 voxels; quad j of a brick
+// is (ix, iy) = (j / 64, (j / 4) % 16) and iz = 4 (j % 4) .. +3 locally.
+constexpr int kBrick = 16;
+struct BrickGrid {
+    int64_t ix0;      // first ix of the range
+    int nbx, nby, nbz;
+};
+
+__device__ __forceinline__ unsigned gate_brick_quad(const float *__restrict__ dens,
+                                                    const FuseConst &C, const FuseOut &O,
+                                                    const BrickGrid &G, int64_t tile, int j,
+                                                    bool count_only, int64_t &base_out) {
+    const int64_t bz = tile % G.nbz;
+    const int64_t t1 = tile / G.nbz;
+    const int64_t by = t1 % G.nby;
+    const int64_t bx = t1 / G.nby;
+    const int64_t ix = G.ix0 + bx * kBrick + (j >> 6);
+    const int64_t iy = by * kBrick + ((j >> 2) & 15);
+    const int64_t iz = bz * kBrick + 4 * (j & 3);
+    const int64_t g = C.g;
+    base_out = (ix * g + iy) * g + iz;
+    if (ix >= g || iy >= g || iz >= g) return 0u;
+    // valid part of the quad: inside the row and inside [lo, hi)
+    const int64_t rowleft = g - iz, before = C.lo - base_out, after = C.hi - base_out;
+    int k0 = 0, k1 = rowleft < 4 ? (int)rowleft : 4;
+    if (before > 0) k0 = before < 4 ? (int)before : 4;
+    if (after < k1) k1 = after > 0 ? (int)after : 0;
+    return gate_quad(dens, C, O, base_out, k0, k1, (g & 3) == 0, count_only);
+}
 // Counting pass (divas_gate_count): grid-stride over quads, one atomic per
 // warp that found gated voxels.
 __global__ void __launch_bounds__(kGateThreads)
 fuse_gate_count(const float *__restrict__ dens, FuseConst C, WsHeader *__restrict__ hdr) {
     const int64_t nquads = (C.hi - C.lo + 3) / 4;
-    const bool aligned = (C.lo & 3) == 0;
     const FuseOut none{};
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
          q - (threadIdx.x & 31) < nquads; q += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned bits = q < nquads ? gate_quad(dens, C, none, C.lo + 4 * q, aligned, true) : 0u;
+        const unsigned bits = q < nquads ? gate_flat_quad(dens, C, none, C.lo + 4 * q, true) : 0u;
         int cnt = __popc(bits);
         if (__ballot_sync(0xffffffffu, cnt != 0) == 0) continue;
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -192,23 +229,20 @@ fuse_gate_count(const float *__restrict__ dens, FuseConst C, WsHeader *__restric
 // Ordered gate, pass 1: tiles of kGateTile voxels; zero the outputs and count
 // each tile's gated voxels.  Quad j of a tile is handled by thread j % 256 in
 // round j / 256, so the rounds walk the tile in C order.
-#ifndef DIVAS_GATE_ROUNDS
-#define DIVAS_GATE_ROUNDS 4
-#endif
-constexpr int kGateRounds = DIVAS_GATE_ROUNDS;     // quads per thread per tile
-constexpr int kGateTile = 4 * kGateRounds * kGateThreads;
+constexpr int kGateRounds = 4;                     // quads per thread per 16^3 brick
+constexpr int kGateTile = 4 * kGateRounds * kGateThreads;   // 4096 = 16^3
 constexpr int64_t kGateTileMax = (1LL << 32) / kGateTile;   // tiles of any u32 voxel range
 
 __global__ void __launch_bounds__(kGateThreads)
-gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, uint32_t *__restrict__ tiles) {
+gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
+           uint32_t *__restrict__ tiles) {
     __shared__ int s_w[kGateThreads / 32];
-    const bool aligned = (C.lo & 3) == 0;
-    const int64_t t0 = C.lo + (int64_t)blockIdx.x * kGateTile;
     int cnt = 0;
+    int64_t base;
 #pragma unroll
     for (int r = 0; r < kGateRounds; ++r)
-        cnt += __popc(gate_quad(dens, C, O, t0 + 4 * (r * kGateThreads + (int)threadIdx.x), aligned,
-                                false));
+        cnt += __popc(gate_brick_quad(dens, C, O, G, blockIdx.x, r * kGateThreads + (int)threadIdx.x,
+                                      false, base));
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = cnt;
     __syncthreads();
@@ -263,8 +297,9 @@ gate_scan(uint32_t *__restrict__ tiles, int64_t ntiles, int64_t cap, WsHeader *_
 // pass 3: each gated voxel's C-order rank -> its slot (deterministic order);
 // tiles without a gated voxel (most of the grid) return at once
 __global__ void __launch_bounds__(kGateThreads)
-gate_emit(const float *__restrict__ dens, FuseConst C, const uint32_t *__restrict__ tiles,
-          int64_t ntiles, const WsHeader *__restrict__ hdr, uint32_t *__restrict__ work) {
+gate_emit(const float *__restrict__ dens, FuseConst C, BrickGrid G,
+          const uint32_t *__restrict__ tiles, int64_t ntiles, const WsHeader *__restrict__ hdr,
+          uint32_t *__restrict__ work) {
     constexpr int NW = kGateThreads / 32;
     constexpr int NC = kGateRounds * NW;               // (round, warp) chunks, C order
     static_assert(NC % 32 == 0, "chunk scan");
@@ -273,16 +308,15 @@ gate_emit(const float *__restrict__ dens, FuseConst C, const uint32_t *__restric
     const int64_t end = (int64_t)blockIdx.x + 1 < ntiles ? (int64_t)tiles[blockIdx.x + 1]
                                                           : (int64_t)hdr->count;
     if (end == off) return;
-    const bool aligned = (C.lo & 3) == 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t t0 = C.lo + (int64_t)blockIdx.x * kGateTile;
     const FuseOut none{};
     unsigned bits[kGateRounds];
     int lp[kGateRounds];
+    int64_t qbase[kGateRounds];
 #pragma unroll
     for (int r = 0; r < kGateRounds; ++r) {
-        bits[r] = gate_quad(dens, C, none, t0 + 4 * (r * kGateThreads + (int)threadIdx.x), aligned,
-                            true);
+        bits[r] = gate_brick_quad(dens, C, none, G, blockIdx.x, r * kGateThreads + (int)threadIdx.x,
+                                  true, qbase[r]);
         const int c = __popc(bits[r]);
         int incl = c;
         for (int o = 1; o < 32; o <<= 1) {
@@ -312,7 +346,7 @@ gate_emit(const float *__restrict__ dens, FuseConst C, const uint32_t *__restric
     for (int r = 0; r < kGateRounds; ++r) {
         unsigned b = bits[r];
         int64_t pos = off + s_pre[r * NW + warp] + lp[r];
-        const int64_t base = t0 + 4 * (r * kGateThreads + (int)threadIdx.x);
+        const int64_t base = qbase[r];
         while (b) {
             const int k = __ffs(b) - 1;
             b &= b - 1;
@@ -1407,10 +1441,16 @@ static void launch_gate_count(const FuseConst &C, const float *dens, WsHeader *h
 // and the slot order is reproducible.
 static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O, uint32_t *work,
                         WsHeader *hdr, uint32_t *tiles, cudaStream_t s) {
-    const int64_t ntiles = (C.hi - C.lo + kGateTile - 1) / kGateTile;
-    gate_tiles<<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, O, tiles);
+    const int64_t g = C.g, gg = g * g;
+    BrickGrid G;
+    G.ix0 = C.lo / gg;
+    const int64_t ix1 = (C.hi + gg - 1) / gg;          // exclusive
+    G.nbx = (int)((ix1 - G.ix0 + kBrick - 1) / kBrick);
+    G.nby = G.nbz = (int)((g + kBrick - 1) / kBrick);
+    const int64_t ntiles = (int64_t)G.nbx * G.nby * G.nbz;
+    gate_tiles<<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, O, G, tiles);
     gate_scan<<<1, 1024, 0, s>>>(tiles, ntiles, C.cap, hdr);
-    gate_emit<<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, tiles, ntiles, hdr, work);
+    gate_emit<<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, G, tiles, ntiles, hdr, work);
 }
 
 // records + bands of views [v0, v0 + cnt) from planar refined masks
