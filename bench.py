@@ -105,21 +105,29 @@ class ClockSampler:
 
     def __enter__(self):
         if self._nv is not None:
+            self._switch = sys.getswitchinterval()
+            sys.setswitchinterval(0.0005)          # let the sampler thread in while launching
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
+            t0 = time.perf_counter()               # the timed region starts once sampling runs
+            while not self.samples and time.perf_counter() - t0 < 1.0:
+                time.sleep(0.0005)
+            self._n0 = len(self.samples)
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
         if self._t is not None:
             self._t.join()
+            sys.setswitchinterval(self._switch)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml-unavailable"]}
         reasons = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "samples": len(self.samples), "reasons": reasons}
+        live = self.samples[getattr(self, "_n0", 0):] or self.samples   # under load
+        return {"sm_mhz": float(statistics.median(live)), "sm_max_mhz": self.max_mhz,
+                "samples": len(live), "reasons": reasons}
 
 
 # ---------------------------------------------------------------------------
