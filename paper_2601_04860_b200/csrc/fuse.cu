@@ -791,6 +791,10 @@ struct QItem {                  // a thin candidate that survived the band test
 };
 
 constexpr int kQueue = kPairThreads;
+#ifndef DIVAS_CARVEOUT
+#define DIVAS_CARVEOUT 25
+#endif
+constexpr int kPairCarveout = DIVAS_CARVEOUT;      // % of the unified L1 / shared memory
 
 // Per-lane part of one (view, voxel) pair: centre projection, routing, the
 // thick path, the thin gates and the band test.  Returns true when the pair
@@ -1602,6 +1606,14 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         const int64_t cap_blocks = (cap + kPairThreads - 1) / kPairThreads;
         if (cap_blocks > 0x7fffffffLL) { set_error("divas_fuse: too many slots"); return DIVAS_EINVAL; }
         C.view0 = v0;
+        // a small shared-memory carveout (the queues of 4 CTAs fit in 64 KB)
+        // leaves ~190 KB of L1 for the footprint / band / gradient gathers
+        static bool carve_set = false;
+        if (!carve_set) {
+            cudaFuncSetAttribute(fuse_pairs, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 kPairCarveout);
+            carve_set = true;
+        }
         fuse_pairs<<<dim3((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)(v1 - v0)),
                      kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr, v1 - v0);
         if ((rc = check_launch("divas_fuse(pairs)"))) return rc;
