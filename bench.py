@@ -286,12 +286,27 @@ def run_ours(args):
     from paper_2601_04860_b200.segmenter import refine_bands_device
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    # DIVAS_FORCE_DIST=1 (testing): take the multi-rank code paths at any world size
+    dist_on = world > 1 or os.environ.get("DIVAS_FORCE_DIST") == "1"
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if dist_on:
+        # NCCL prints its banner (NCCL_DEBUG=VERSION in this image) on stdout when
+        # the communicator comes up: send fd 1 to stderr meanwhile, so stdout
+        # carries only the JSON result line
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=dev)
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     params = FusionParams()
     pv = params.as_vector()
 
@@ -301,7 +316,7 @@ def run_ours(args):
         wl = workloads.make(args.config, device=dev)
     else:
         wl = None
-    if world > 1:
+    if dist_on:
         shapes = [None]
         if rank == 0:
             shapes = [dict(nv=wl.nv, h=wl.shape[1], w=wl.shape[2], g=wl.g, cams=wl.cams,
@@ -321,7 +336,7 @@ def run_ours(args):
     dv = DeviceViews(cams_t, torch.empty_like(wl.raw_masks), wl.dmins, wl.dmaxs, wl.dexps,
                      wl.nsamps, z_surface=wl.z_surface, raw_masks=wl.raw_masks)
     bcast_ms = 0.0
-    if world > 1:
+    if dist_on:
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -343,7 +358,7 @@ def run_ours(args):
                                         world)
     else:
         slabs = sharding.equal_slabs(g, world)
-    views_mode = args.shard == "views" and world > 1
+    views_mode = args.shard == "views" and dist_on
     if views_mode:
         slabs = [(0, g)] * world
     lo, hi = sharding.slab_voxel_range(slabs[rank], g)
@@ -364,7 +379,7 @@ def run_ours(args):
 
     peer = None
     gather_mode = None
-    if world > 1 and not views_mode:
+    if dist_on and not views_mode:
         gather_mode = "nccl all_gather of the slab occupancy bytes"
         if args.gather == "p2p":
             try:
@@ -412,7 +427,7 @@ def run_ours(args):
         if ev is not None:
             ev[2].record(stream)
         occ_full = None
-        if world > 1 and not views_mode:
+        if dist_on and not views_mode:
             if peer is not None:
                 peer.barrier()
                 occ_full = peer.buf
@@ -426,7 +441,7 @@ def run_ours(args):
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         dist.barrier()
     if peer is not None:
         # the fused gather must equal the NCCL one bit for bit, or it is not used
@@ -444,13 +459,13 @@ def run_ours(args):
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         for k in range(K):
             flush.zero_()
             step(evs[k])
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
     t_ref = [a.elapsed_time(b) for a, b, _c, _d in evs]
     t_fuse = [b.elapsed_time(c) for _a, b, c, _d in evs]
@@ -458,7 +473,7 @@ def run_ours(args):
     t_step = [a.elapsed_time(d) for a, _b, _c, d in evs]
     ms_local = float(np.mean(t_step))
     ms = ms_local
-    if world > 1:
+    if dist_on:
         t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -530,12 +545,12 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIG_DESC[args.config], "grid": g, "views": nv,
                    "width": W, "height": H,
-                   "parallelism": (f"{args.shard} x{world}" if world > 1 else "1 GPU"),
+                   "parallelism": (f"{args.shard} x{world}" if dist_on else "1 GPU"),
                    "slabs": slabs, "slab_policy": args.slabs,
                    "step": ("refine+aux(own views) + gate + bcast(gated list) + pairs(own views)"
                             " + all-gather(contributions) + reduce" if views_mode else
                             "refine+aux(all views; records in windows) + fuse(slab, threshold fused)"
-                            + (" + all-gather(occupancy)" if world > 1 else "")),
+                            + (" + all-gather(occupancy)" if dist_on else "")),
                    "gather": gather_mode,
                    "windows": (None if roi is None else
                                f"scan records/bands built in per-view windows around the "
@@ -550,11 +565,11 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     line.update(extra)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 
