@@ -389,6 +389,14 @@ def run_ours(args):
             except Exception as e:  # noqa: BLE001
                 gather_mode = f"nccl all_gather (symmetric memory unavailable: {type(e).__name__})"
 
+    # slab mode, several ranks: each rank takes the z min/max pass of its block
+    # of views and the keys are all-gathered (the band pass needs every view's)
+    mm_keys = None
+    if dist_on and not views_mode:
+        from paper_2601_04860_b200.segmenter import refine_minmax_device
+        mm_blocks, mm_rows = sharding.view_blocks(nv, world)
+        mm_mine = torch.zeros((mm_rows, 2), dtype=torch.int32, device=dev)
+        mm_all = torch.zeros((world * mm_rows, 2), dtype=torch.int32, device=dev)
     roi = None
     if args.windows == "on" and not views_mode:
         roi = sharding.slab_view_rois(wl.density, pv, g, wl.origin, wl.dx, cams_t.cpu().numpy(),
@@ -404,6 +412,14 @@ def run_ours(args):
                 refine_bands_device(dv.raw_masks[v0:v1], dv.z_surface[v0:v1], dv.nsamps[v0:v1],
                                     dv.dexps[v0:v1], params, wl.dx,
                                     aux=bands.view_slices(v0, v1, nv, H, W), planar=False)
+        elif dist_on:
+            b0, b1 = mm_blocks[rank]
+            if b1 > b0:
+                refine_minmax_device(dv.z_surface[b0:b1], dv.nsamps[b0:b1], keys=mm_mine[:b1 - b0])
+            dist.all_gather_into_tensor(mm_all, mm_mine)
+            _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps,
+                                            params, wl.dx, aux=bands, planar=False, roi=roi,
+                                            keys=mm_all[:nv])
         else:
             _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps,
                                             params, wl.dx, aux=bands, planar=False, roi=roi)

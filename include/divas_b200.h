@@ -92,6 +92,18 @@ int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm,
  * window); `out`, records and bands outside the windows are left untouched.
  * Used with the projection of a slab's gated voxels: the fusion of that slab
  * reads no pixel outside it (sharding.slab_view_rois). */
+/* The per-view z min / max on their own: keys [nv][2] order-preserving u32
+ * (min, max) over the valid pixels (an empty view has min > max).  Lets the
+ * views' min/max passes be split across ranks and the keys exchanged; then
+ * divas_refine_bands_keys builds the records from them (roi may be NULL). */
+int divas_refine_minmax(int32_t nv, int64_t hm, int64_t wm, const float *z_surface,
+                        const int32_t *n_samples, uint32_t *keys, void *stream);
+int divas_refine_bands_keys(int32_t nv, int64_t hm, int64_t wm,
+                            const float *mask, const float *z_surface, const int32_t *n_samples,
+                            const float *dexp, float *out, const double *pv, double dx_vox,
+                            void *records, void *bands, const uint32_t *keys, void *workspace,
+                            size_t workspace_bytes, const int32_t *roi, int32_t roi_w,
+                            int32_t roi_h, void *stream);
 int divas_refine_bands_roi(int32_t nv, int64_t hm, int64_t wm,
                            const float *mask, const float *z_surface, const int32_t *n_samples,
                            const float *dexp, float *out, const double *pv, double dx_vox,

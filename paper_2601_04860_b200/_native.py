@@ -26,7 +26,8 @@ EXPORTS = (
     "divas_gradient_maps", "divas_pair_trace",
     "divas_threshold_workspace_size", "divas_threshold",
     "divas_overlay", "divas_vgrid_payload",
-    "divas_last_error", "divas_abi_version", "divas_refine_bands_roi",
+    "divas_last_error", "divas_abi_version", "divas_refine_bands_roi", "divas_refine_minmax",
+    "divas_refine_bands_keys",
 )
 
 _VP = ctypes.c_void_p
@@ -71,6 +72,10 @@ def _declare(lib):
         "divas_refine_bands_roi": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP,
                                                   ctypes.POINTER(D), D, _VP, _VP, _VP, S, _VP,
                                                   I32, I32, _VP]),
+        "divas_refine_minmax": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP]),
+        "divas_refine_bands_keys": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP,
+                                                   ctypes.POINTER(D), D, _VP, _VP, _VP, _VP, S,
+                                                   _VP, I32, I32, _VP]),
         "divas_fuse_workspace_size": (S, [I64, I32, I32, I32]),
         "divas_fuse": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, S, _VP]),
         "divas_gate_count": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, _VP]),

@@ -160,7 +160,8 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
                              const float *z_surface, const int32_t *n_samples, const float *dexp,
                              float *out, const double *pv, double dx_vox, void *records,
                              void *bands, void *workspace, size_t workspace_bytes,
-                             const int32_t *roi, int32_t roi_w, int32_t roi_h, void *stream) {
+                             const int32_t *roi, int32_t roi_w, int32_t roi_h,
+                             const uint32_t *keys, void *stream) {
     if (nv <= 0 || hm <= 0 || wm <= 0) { set_error("divas_refine_bands: empty view set"); return DIVAS_EINVAL; }
     if (nv > 65535 || hm > 0x7fffffff / 2 || wm > 0x7fffffff / 2) {
         set_error("divas_refine_bands: plane too large");
@@ -180,7 +181,10 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
     const bool vec = (wm % 4 == 0) &&
                      ((((uintptr_t)mask) | ((uintptr_t)z_surface) | ((uintptr_t)n_samples) |
                        ((uintptr_t)out) | ((uintptr_t)dexp) | ((uintptr_t)records)) & 15) == 0;
-    refine_init<<<(nv + 255) / 256, 256, 0, s>>>(ws, nv);
+    // keys: the views' z min / max computed elsewhere (divas_refine_minmax,
+    // e.g. by another rank); else computed here
+    if (!keys) refine_init<<<(nv + 255) / 256, 256, 0, s>>>(ws, nv);
+    const uint32_t *mm = keys ? keys : ws;
     dim3 grid(blocks_per_view(plane, nv), nv);
     const BandParams B = band_params(pv, dx_vox, (int)hm, (int)wm);
     // grid extent: the whole plane, or the largest window (+ one tile of slack
@@ -190,14 +194,14 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
                             : B.nty;
     const int4 *r4 = reinterpret_cast<const int4 *>(roi);
     if (vec) {
-        refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
+        if (!keys) refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((gw / 4 + 255) / 256), (unsigned)gty, (unsigned)nv);
-        band_pass<4, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
+        band_pass<4, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, mm,
                                               (double2 *)bands, (float4 *)records, nv, r4);
     } else {
-        refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
+        if (!keys) refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((gw + 255) / 256), (unsigned)gty, (unsigned)nv);
-        band_pass<1, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, ws,
+        band_pass<1, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, mm,
                                               (double2 *)bands, (float4 *)records, nv, r4);
     }
     return check_launch("divas_refine_bands");
@@ -209,7 +213,41 @@ extern "C" int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm, const floa
                                   void *records, void *bands, void *workspace,
                                   size_t workspace_bytes, void *stream) {
     return refine_bands_impl(nv, hm, wm, mask, z_surface, n_samples, dexp, out, pv, dx_vox,
-                             records, bands, workspace, workspace_bytes, nullptr, 0, 0, stream);
+                             records, bands, workspace, workspace_bytes, nullptr, 0, 0, nullptr,
+                             stream);
+}
+
+extern "C" int divas_refine_minmax(int32_t nv, int64_t hm, int64_t wm, const float *z_surface,
+                                   const int32_t *n_samples, uint32_t *keys, void *stream) {
+    if (nv <= 0 || hm <= 0 || wm <= 0 || !z_surface || !n_samples || !keys) {
+        set_error("divas_refine_minmax: bad arguments");
+        return DIVAS_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t plane = hm * wm;
+    refine_init<<<(nv + 255) / 256, 256, 0, s>>>(keys, nv);
+    dim3 grid(blocks_per_view(plane, nv), nv);
+    const bool vec = (wm % 4 == 0) && ((((uintptr_t)z_surface) | ((uintptr_t)n_samples)) & 15) == 0;
+    if (vec) refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, keys);
+    else refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, keys);
+    return check_launch("divas_refine_minmax");
+}
+
+extern "C" int divas_refine_bands_keys(int32_t nv, int64_t hm, int64_t wm, const float *mask,
+                                       const float *z_surface, const int32_t *n_samples,
+                                       const float *dexp, float *out, const double *pv,
+                                       double dx_vox, void *records, void *bands,
+                                       const uint32_t *keys, void *workspace,
+                                       size_t workspace_bytes, const int32_t *roi, int32_t roi_w,
+                                       int32_t roi_h, void *stream) {
+    if (!keys) { set_error("divas_refine_bands_keys: null keys"); return DIVAS_EINVAL; }
+    if (roi && (roi_w < 1 || roi_h < 1)) {
+        set_error("divas_refine_bands_keys: empty window");
+        return DIVAS_EINVAL;
+    }
+    return refine_bands_impl(nv, hm, wm, mask, z_surface, n_samples, dexp, out, pv, dx_vox,
+                             records, bands, workspace, workspace_bytes, roi, roi_w, roi_h, keys,
+                             stream);
 }
 
 extern "C" int divas_refine_bands_roi(int32_t nv, int64_t hm, int64_t wm, const float *mask,
@@ -224,7 +262,7 @@ extern "C" int divas_refine_bands_roi(int32_t nv, int64_t hm, int64_t wm, const 
     }
     return refine_bands_impl(nv, hm, wm, mask, z_surface, n_samples, dexp, out, pv, dx_vox,
                              records, bands, workspace, workspace_bytes, roi, roi_w, roi_h,
-                             stream);
+                             nullptr, stream);
 }
 
 extern "C" size_t divas_records_size(int32_t nv, int64_t hm, int64_t wm) {

@@ -16,7 +16,7 @@ from . import _native
 from ._device import as_device, device, empty
 
 __all__ = ["ConfidenceMask", "ViewAux", "ViewWindows", "refine_mask", "refine_masks",
-           "refine_masks_device", "refine_bands_device"]
+           "refine_masks_device", "refine_bands_device", "refine_minmax_device"]
 
 
 @dataclass
@@ -92,15 +92,32 @@ class ViewAux:
         return self.records[v0 * r1: v1 * r1], self.bands[v0 * b1: v1 * b1]
 
 
+def refine_minmax_device(z_surface, n_samples, keys=None, stream=None):
+    """Per-view z min / max over valid pixels as order-preserving uint32 keys
+    [nv, 2] (int32 tensor view), for ``refine_bands_device(keys=...)``; the
+    views of a block can be computed on one rank and the keys all-gathered."""
+    import torch
+    nv, hm, wm = z_surface.shape
+    if keys is None:
+        keys = torch.empty((nv, 2), dtype=torch.int32, device=z_surface.device)
+    _native.check(_native.lib().divas_refine_minmax(nv, hm, wm, _native.ptr(z_surface),
+                                                    _native.ptr(n_samples), _native.ptr(keys),
+                                                    _native.stream_handle(stream)),
+                  "divas_refine_minmax")
+    return keys
+
+
 def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, out=None,
-                        aux=None, stream=None, planar=True, roi=None):
+                        aux=None, stream=None, planar=True, roi=None, keys=None):
     """``refine_masks_device`` fused with the fusion's per-view aux data.
 
     One pass over the planes writes the refined masks (``planar=True``) and
     the ``ViewAux`` (scan records + tile depth bands) that ``Fuser.run(aux=)``
     consumes, so the fusion never re-reads the planar masks.  ``aux`` may be
     a preallocated ViewAux or a pair of byte tensors (records, bands) for a
-    slice of a larger set.  ``roi``: a ``ViewWindows`` -- build records and
+    slice of a larger set.  ``keys``: the views' min/max keys from
+    ``refine_minmax_device`` (skips the min/max pass).  ``roi``: a
+    ``ViewWindows`` -- build records and
     bands only inside one window per view (``divas_refine_bands_roi``; the
     planar output, if any, is also written only there).  Returns (out or
     None, aux).
@@ -130,6 +147,17 @@ def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, 
     wsb = lib.divas_refine_workspace_size(nv)
     ws = torch.empty(wsb, dtype=torch.uint8, device=masks.device)
     pvc = (ctypes.c_double * 14)(*pv.tolist())
+    if keys is not None:
+        if keys.numel() < 2 * nv or keys.dtype != torch.int32 or not keys.is_cuda:
+            raise ValueError("keys must be a CUDA int32 [nv, 2] tensor")
+        _native.check(lib.divas_refine_bands_keys(
+            nv, hm, wm, _native.ptr(masks), _native.ptr(z_surface), _native.ptr(n_samples),
+            _native.ptr(d_exp), _native.ptr(out), pvc, float(voxel_size), _native.ptr(rec),
+            _native.ptr(bands), _native.ptr(keys), _native.ptr(ws), wsb,
+            _native.ptr(roi.rects) if roi is not None else None,
+            roi.max_w if roi is not None else 0, roi.max_h if roi is not None else 0,
+            _native.stream_handle(stream)), "divas_refine_bands_keys")
+        return out, aux
     if roi is not None:
         if roi.nv != nv:
             raise ValueError("one window per view")

@@ -68,3 +68,27 @@ def test_windowed_planar_output_inside_windows():
     o = out.cpu().numpy()
     for v, (x0, y0, x1, y1) in enumerate(roi.host):
         assert np.array_equal(o[v, y0:y1 + 1, x0:x1 + 1], refined[v, y0:y1 + 1, x0:x1 + 1])
+
+
+def test_minmax_keys_split_equal_full():
+    """Min/max keys computed in view blocks (as ranks do) + the keys-based band
+    pass == the one-call refine: refined masks, records and bands bit-exact."""
+    import torch
+    from paper_2601_04860_b200.segmenter import (ViewAux, refine_bands_device,
+                                                 refine_minmax_device)
+    case = golden_io.scene_cases()["sop"]
+    raw, zs, refined = golden_io.scene_raw()
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    m, z, n, d = t(raw), t(zs), t(case.nsamps), t(case.dexps)
+    nv, hm, wm = m.shape
+    out_a, aux_a = refine_bands_device(m, z, n, d, case.pv, case.dx)
+    keys = torch.zeros((nv, 2), dtype=torch.int32, device=dev)
+    cut = nv // 2
+    refine_minmax_device(z[:cut], n[:cut], keys=keys[:cut])
+    refine_minmax_device(z[cut:], n[cut:], keys=keys[cut:])
+    aux_b = ViewAux.empty(nv, hm, wm, dev)
+    out_b, _ = refine_bands_device(m, z, n, d, case.pv, case.dx, aux=aux_b, keys=keys)
+    assert torch.equal(out_a, out_b)
+    assert np.array_equal(out_b.cpu().numpy(), refined)
+    assert torch.equal(aux_a.records, aux_b.records) and torch.equal(aux_a.bands, aux_b.bands)
