@@ -617,8 +617,10 @@ def run_e2e(args, wl, params, dev):
                           planes["nsamps"][v], planes["z_surface"][v])
         views.append((vg, ConfidenceMask(planes["raw_masks"][v])))
 
+    xfer = {}
+
     def once():
-        return refine_and_fuse(grid, dens, views, params)
+        return refine_and_fuse(grid, dens, views, params, transfer_stats=xfer)
 
     once()
     torch.cuda.synchronize()
@@ -629,12 +631,7 @@ def run_e2e(args, wl, params, dev):
         og, refined = once()
         times.append(time.perf_counter() - t0)
     ms = 1e3 * float(np.median(times))
-    px = nv * H * W
-    h2d = px * 24 + wl.g ** 3 * 4 + nv * 18 * 8
-    rho = np.asarray(dens.values, dtype=np.float64)
-    pv = params.as_vector()
-    gated = int(((rho >= pv[4]) | ((pv[13] != 0) & (rho >= pv[5]))).sum())
-    d2h = px * 4 + 8 + gated * 12
+    h2d, d2h = xfer["h2d_bytes"], xfer["d2h_bytes"]   # counted by refine_and_fuse
     return {"value": wl.updates() / (ms / 1e3), "unit": "updates/s", "ms_per_step": ms,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "api": "refine_and_fuse(grid, density, [(ViewGeometry, raw ConfidenceMask)], params)"

@@ -282,6 +282,11 @@ int divas_overlay(const double *cam, int32_t h, int32_t w, const float *dmin,
 
 /* ---------------------------------------------------------------------- */
 const char *divas_last_error(void);
+
+/* Host -> device copy of a pitched sub-rectangle (cudaMemcpy2DAsync): the
+ * windowed upload of view planes in refine_and_fuse. */
+int divas_copy2d_h2d(void *dst, size_t dpitch, const void *src, size_t spitch,
+                     size_t width_bytes, size_t height, void *stream);
 int divas_abi_version(void);
 
 #ifdef __cplusplus

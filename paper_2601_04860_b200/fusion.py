@@ -556,7 +556,7 @@ def _side_stream(dev, name):
 
 
 def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
-                    return_refined=True, chunk_views=4):
+                    return_refined=True, chunk_views=4, windows=True, transfer_stats=None):
     """``refine_mask`` on every (ViewGeometry, raw ConfidenceMask) pair, then
     ``fuse`` of the refined set -- the session's update (session.py:204-215)
     as one device pass: each host map is uploaded once, refinement writes the
@@ -569,6 +569,11 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     k-1's refined masks download (second side stream).  After the last chunk
     only the value-sorted reduction and the (index, p) download of the gated
     voxels remain, so an update costs about the host-link time of its inputs.
+    ``windows``: d_min / d_max are read by the fusion only at the centre
+    pixels of gated voxels (and their neighbours), all inside each view's
+    window around the projected gated region (``sharding.slab_view_rois``), so
+    only those sub-rectangles are uploaded (C3: 49 % of the pixels).
+    ``transfer_stats``: a dict that receives the bytes copied each way.
 
     Same validation and errors as the two reference calls; results identical
     to ``fuse(grid, density, [(v, refine_mask(m, v)) ...], params, bounds)``
@@ -618,18 +623,53 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     ready = []
     srcs = [{"raw": m.values if hasattr(m, "values") else m, "z": vg.z_surface, "dmins": vg.d_min,
              "dmaxs": vg.d_max, "dexps": vg.d_exp, "nsamps": vg.n_samples} for vg, m in views]
+
+    h2d = [int(np.asarray(density.values).size) * 4]
+
+    def upload_full(k, v0, v1):
+        dt = np.int32 if k == "nsamps" else np.float32
+        h2d[0] += sum(sizes[i][0] * sizes[i][1] for i in range(v0, v1)) * 4
+        run = _adjacent_run([srcs[i][k] for i in range(v0, v1)], dt, (hm, wm))
+        if run is not None:                   # the views' planes are one host block
+            planes[k][v0:v1].copy_(torch.from_numpy(run), non_blocking=True)
+            return
+        for i in range(v0, v1):
+            h, w = sizes[i]
+            planes[k][i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(srcs[i][k], dt)),
+                                       non_blocking=True)
+
+    full_names = ("raw", "z", "dexps", "nsamps")
+    win_names = ("dmins", "dmaxs")
     with torch.cuda.stream(up):
         for v0, v1 in bounds_k:
-            for k in names:
-                dt = np.int32 if k == "nsamps" else np.float32
-                run = _adjacent_run([srcs[i][k] for i in range(v0, v1)], dt, (hm, wm))
-                if run is not None:           # the views' planes are one host block
-                    planes[k][v0:v1].copy_(torch.from_numpy(run), non_blocking=True)
+            for k in full_names:
+                upload_full(k, v0, v1)
+    # the windows need the gated voxels' bounding box: one wait for the density
+    # upload, while the full planes above keep the link busy
+    rois = None
+    if windows:
+        from .sharding import slab_view_rois
+        rois = slab_view_rois(dens, fuser.pv, g, np.asarray(grid.origin, dtype=np.float64),
+                              fuser.dx, pack_cameras(cams), sizes)
+    keep = []
+    lib = _native.lib()
+    with torch.cuda.stream(up):
+        for v0, v1 in bounds_k:
+            for k in win_names:
+                if rois is None:
+                    upload_full(k, v0, v1)
                     continue
                 for i in range(v0, v1):
                     h, w = sizes[i]
-                    planes[k][i, :h, :w].copy_(
-                        torch.from_numpy(np.ascontiguousarray(srcs[i][k], dt)), non_blocking=True)
+                    x0, y0, x1, y1 = (int(c) for c in rois.host[i])
+                    x1, y1 = min(x1, w - 1), min(y1, h - 1)
+                    a = np.ascontiguousarray(srcs[i][k], np.float32)
+                    keep.append(a)
+                    h2d[0] += 4 * (x1 - x0 + 1) * (y1 - y0 + 1)
+                    _native.check(lib.divas_copy2d_h2d(
+                        planes[k][i].data_ptr() + 4 * (y0 * wm + x0), 4 * wm,
+                        a.ctypes.data + 4 * (y0 * w + x0), 4 * w, 4 * (x1 - x0 + 1), y1 - y0 + 1,
+                        _native.stream_handle(up)), "divas_copy2d_h2d")
             ev = torch.cuda.Event()
             ev.record(up)
             ready.append(ev)
@@ -665,6 +705,12 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     if int(hdr_h[8:12].view(torch.int32).item()) != 0:
         raise RuntimeError("divas_fuse: gated voxels exceeded the workspace capacity")
     hpn = hp.numpy()
+    if transfer_stats is not None:
+        transfer_stats["h2d_bytes"] = h2d[0] + cam_t.numel() * 8
+        # the header, each gated voxel's p (stored into the host grid by the
+        # reduction) and the refined masks
+        transfer_stats["d2h_bytes"] = 16 + 8 * cap + (sum(h * w for h, w in sizes) * 4
+                                                      if return_refined else 0)
     masks = None
     if return_refined:
         down.synchronize()

@@ -347,8 +347,9 @@ def test_refine_and_fuse_chunking(dev, name):
     params = FusionParams(*[float(x) for x in case.pv[:13]], enable_thin=bool(case.pv[13]))
     raws = [(vg, ConfidenceMask(m.values.copy())) for vg, m in views]
     ref = fuse(grid, dens, [(vg, refine_mask(m, vg)) for vg, m in raws], params, bounds=bounds)
-    for chunk in (1, 2, 3, 64):
-        og, masks = refine_and_fuse(grid, dens, raws, params, bounds=bounds, chunk_views=chunk)
+    for chunk, win in ((1, True), (2, False), (3, True), (64, True), (64, False)):
+        og, masks = refine_and_fuse(grid, dens, raws, params, bounds=bounds, chunk_views=chunk,
+                                    windows=win)
         assert np.array_equal(og.probs, ref.probs), chunk
         for (vg, m), got in zip(raws, masks):
             assert got.shape == m.shape
