@@ -553,7 +553,8 @@ def run_ours(args):
             extra["incremental"] = run_incremental(args, wl, params, dev, probs)
             extra["incremental"]["full_recompute_ms_for_comparison"] = ms
 
-    launches_per_step = 3 + 3          # refine: init, minmax, band_pass; fuse: gate, pairs, reduce
+    # refine: init, minmax, band_pass; fuse: gate_tiles, gate_scan, gate_emit, pairs, reduce
+    launches_per_step = 3 + 5
     line = {
         "metric": "voxel-view updates/s", "value": value, "unit": "updates/s",
         "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms,
