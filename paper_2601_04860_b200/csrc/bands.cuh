@@ -22,10 +22,40 @@ struct BandParams {
     int hm, wm, ntx, nty;
 };
 
-// Per-pixel scan record: {refined mask, d_exp, tau_d(n) as f32 (or -1e30 when
-// the pixel cannot support: mask <= 0.5 or n == 0), n_samples bits}.  One
-// 128-bit load gives the footprint scan everything it reads per pixel.
+// Per-pixel scan records, two 8-byte planes per view (16 B/px in all):
+//   A = {refined mask, d_exp, or NaN when the pixel cannot support a thin
+//        candidate (mask <= 0.5 or n == 0)}
+//   B = {tau_d(n) as f32 (or -1e30 when it cannot support), n_samples bits}
+// A view whose supporting pixels all share one tau (the renderer's n is
+// constant per view, e.g. n = 1 on the reference's scenes) is scanned from
+// plane A alone (8 bytes per pixel, half the L1 traffic), with that tau from
+// the view's tau-range entry; other views read B as well.
+// View v's records start at v * 2 * hm * wm float2: A plane, then B plane.
 constexpr float kIneligible = -1e30f;
+
+// Bands: per view nty * ntx tile entries, then one entry holding the view's
+// {min, max} key (order-preserving u32, as the z keys) of tau32 over the
+// supporting pixels the pass saw.
+__host__ __device__ inline int64_t band_view_stride(int nty, int ntx) {
+    return (int64_t)nty * ntx + 1;
+}
+
+__device__ __forceinline__ uint32_t tau_key(float t) {   // t >= 0: order-preserving
+    return __float_as_uint(t);
+}
+
+// tau-range entries of views [0, nv) of a band buffer: {UINT_MAX, 0} (empty)
+static __global__ void band_init(double2 *__restrict__ bands, int nv, int nty, int ntx) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < nv) {
+        uint32_t *e = reinterpret_cast<uint32_t *>(bands + v * band_view_stride(nty, ntx) +
+                                                   (int64_t)nty * ntx);
+        e[0] = 0xffffffffu;
+        e[1] = 0u;
+        e[2] = 0u;                                   // unused half of the entry
+        e[3] = 0u;
+    }
+}
 
 __device__ __forceinline__ float band_px(float m, int32_t n, float d, const BandParams &B,
                                          double &lo, double &hi) {
@@ -50,12 +80,15 @@ __global__ void __launch_bounds__(256)
 band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict__ z,
           const int32_t *__restrict__ nsamp, const float *__restrict__ dexp,
           float *__restrict__ refined, const uint32_t *__restrict__ minmax,
-          double2 *__restrict__ bands, float4 *__restrict__ records, int nv,
+          double2 *__restrict__ bands, float2 *__restrict__ records, int nv,
           const int4 *__restrict__ roi = nullptr) {
     constexpr int TPW = kBandTile / VEC;
     const int v = nv - 1 - (int)blockIdx.z;          // reverse view order: L2 reuse of z / n
     const int64_t plane = (int64_t)B.hm * B.wm;
     const int64_t off = (int64_t)v * plane;
+    float2 *__restrict__ recA = records + 2 * off;   // this view's A plane
+    float2 *__restrict__ recB = recA + plane;        // and B plane
+    uint32_t tmin = 0xffffffffu, tmax = 0u;          // tau keys of the supporting pixels
     // ROI (optional): the view's tile-aligned window {x0, y0, x1, y1}; the
     // grid covers the largest window, blocks past this view's window idle
     int rx0 = 0, rx1 = B.wm - 1, ty = (int)blockIdx.y;
@@ -110,10 +143,29 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
                     if (refined) refined[p] = m[0];
                 }
             }
+            const int64_t q = p - off;                 // pixel within the view
+            float2 a[VEC], b[VEC];
 #pragma unroll
             for (int k = 0; k < VEC; ++k) {
                 const float t32 = band_px(m[k], n[k], d[k], B, lo, hi);
-                records[p + k] = make_float4(m[k], d[k], t32, __int_as_float(n[k]));
+                const bool sup = t32 >= 0.0f;
+                a[k] = make_float2(m[k], sup ? d[k] : __int_as_float(0x7fc00000));
+                b[k] = make_float2(t32, __int_as_float(n[k]));
+                if (sup) {
+                    tmin = min(tmin, tau_key(t32));
+                    tmax = max(tmax, tau_key(t32));
+                }
+            }
+            if (VEC == 4) {
+                float4 *a4 = reinterpret_cast<float4 *>(recA + q);
+                float4 *b4 = reinterpret_cast<float4 *>(recB + q);
+                a4[0] = make_float4(a[0].x, a[0].y, a[1 % VEC].x, a[1 % VEC].y);
+                a4[1] = make_float4(a[2 % VEC].x, a[2 % VEC].y, a[3 % VEC].x, a[3 % VEC].y);
+                b4[0] = make_float4(b[0].x, b[0].y, b[1 % VEC].x, b[1 % VEC].y);
+                b4[1] = make_float4(b[2 % VEC].x, b[2 % VEC].y, b[3 % VEC].x, b[3 % VEC].y);
+            } else {
+                recA[q] = a[0];
+                recB[q] = b[0];
             }
         }
     }
@@ -122,9 +174,20 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
         lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
+    double2 *bv = bands + (int64_t)v * band_view_stride(B.nty, B.ntx);
     if (active && (threadIdx.x % TPW) == 0) {
         const int tx = x0 / kBandTile;
-        bands[((int64_t)v * B.nty + ty) * B.ntx + tx] = make_double2(lo, hi);
+        bv[(int64_t)ty * B.ntx + tx] = make_double2(lo, hi);
+    }
+    // the view's tau range: warp-reduce, one atomic pair per warp
+    for (int o = 16; o > 0; o >>= 1) {
+        tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+        tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    }
+    if ((threadIdx.x & 31) == 0 && tmin <= tmax) {
+        uint32_t *e = reinterpret_cast<uint32_t *>(bv + (int64_t)B.nty * B.ntx);
+        atomicMin(e, tmin);
+        atomicMax(e + 1, tmax);
     }
 }
 
@@ -138,10 +201,16 @@ inline BandParams band_params(const double *pv, double dx, int hm, int wm) {
 }
 
 inline size_t band_bytes(int nv, int hm, int wm) {
-    return (size_t)nv * ((hm + kBandTile - 1) / kBandTile) * ((wm + kBandTile - 1) / kBandTile) *
-           sizeof(double2);
+    return (size_t)nv * band_view_stride((hm + kBandTile - 1) / kBandTile,
+                                         (wm + kBandTile - 1) / kBandTile) * sizeof(double2);
 }
 
-inline size_t record_bytes(int nv, int hm, int wm) { return (size_t)nv * hm * wm * sizeof(float4); }
+inline size_t record_bytes(int nv, int hm, int wm) {
+    return (size_t)nv * hm * wm * 2 * sizeof(float2);
+}
+
+static inline void launch_band_init(double2 *bands, const BandParams &B, int nv, cudaStream_t s) {
+    band_init<<<(nv + 255) / 256, 256, 0, s>>>(bands, nv, B.nty, B.ntx);
+}
 
 }  // namespace divas

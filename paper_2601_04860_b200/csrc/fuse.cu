@@ -92,7 +92,7 @@ struct FuseMaps {
     const float *masks, *dmins, *dmaxs, *dexps;
     const int32_t *nsamps;
     const double2 *bands;   // [nv][nty][ntx] depth bands (bands.cuh)
-    const float4 *rec;      // [nv][hm][wm] scan records (bands.cuh)
+    const float2 *rec;      // [nv][2][hm][wm] scan record planes A, B (bands.cuh)
 };
 
 struct Contrib {                 // all [view or word][cap]
@@ -667,7 +667,7 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     const int ty0 = (int)fmax(fy0, 0.0), ty1 = (int)fmin(fy1, (double)(C.nty - 1));
     if (tx1 < tx0 || ty1 < ty0) return false;
     if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16) { PSTAT(15, 1); return false; }
-    const double2 *bv = M.bands + (int64_t)view * C.nty * C.ntx;
+    const double2 *bv = M.bands + (int64_t)view * band_view_stride(C.nty, C.ntx);
     // tiles in row-major order, four loads in flight per round trip (indices
     // past the last tile repeat it: always in range, never changes the answer)
     const int nx = tx1 - tx0 + 1;
@@ -680,7 +680,7 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
         double2 b[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            DIVAS_BOUND(bp, M.bands + (int64_t)view * C.nty * C.ntx, (int64_t)C.nty * C.ntx);
+            DIVAS_BOUND(bp, bv, (int64_t)C.nty * C.ntx);
             b[j] = __ldg(bp);
             if (i0 + j + 1 < nt) {
                 ++bp;
@@ -838,13 +838,17 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     }
     PSTAT(1, 1);
     if (cu == 2 || cv == 2) PSTAT(14, 1);
-    const int64_t vplane = (int64_t)view * C.hm * C.wm;
-    const int64_t pix = vplane + py * (int64_t)C.wm + px;
-    DIVAS_BOUND(M.rec + pix, M.rec + (int64_t)view * C.hm * C.wm, (int64_t)C.hm * C.wm);
-    const float4 rc = __ldg(M.rec + pix);                      // {m, d_exp, tau32, n}
-    const int32_t ns = __float_as_int(rc.w);
+    const int64_t plane = (int64_t)C.hm * C.wm;
+    const int64_t vplane = (int64_t)view * plane;
+    const int64_t q = py * (int64_t)C.wm + px;
+    const int64_t pix = vplane + q;
+    const float2 *recA = M.rec + 2 * vplane;                   // this view's record planes
+    DIVAS_BOUND(recA + q, recA, plane);
+    const float2 ra = __ldg(recA + q);                         // {m, d_exp or NaN}
+    const float2 rb = __ldg(recA + plane + q);                 // {tau32, n}
+    const int32_t ns = __float_as_int(rb.y);
     if (ns <= 0) return false;                                 // valids[view, py, px] == 0
-    const float m = rc.x;
+    const float m = ra.x;
     PSTAT(2, 1);
 #if defined(DIVAS_ABL) && DIVAS_ABL >= 3
     K.t[kidx] = (double)m;
@@ -852,7 +856,8 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
 #endif
 
     if ((double)m >= C.mask_thr && rho >= C.rho_thr) {
-        const float dexp = rc.y;
+        // plane A holds d_exp only where a thin candidate could be supported
+        const float dexp = (ra.y == ra.y) ? ra.y : __ldg(M.dexps + pix);
         PSTAT(3, 1);
         double b = C.beta * (double)ns;
         if (b > C.bmax) b = C.bmax;
@@ -943,14 +948,20 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     K.t[(int64_t)view * C.cap + q.slot] = q.x_d + (double)(xe - xs);
     return;
 #endif
-    // Footprint scan over the 16-byte records {m, D, tau32, n}.  m_max: f32
-    // widening is exact and monotone, so fmaxf in f32 equals the reference's
-    // f64 `if mv > m_max` (NaN never wins).  Support: the f32 margin test
-    // e = |f32(x_d) - D| - tau32 has |error| < 2^-22 (|x_d| + tau_max); beyond
-    // M = 2^-20 (|x_d| + tau_max) from 0 it decides the reference's f64 test
-    // |x_d - f64(D)| <= tau(n) exactly, inside M the f64 test runs.  Ineligible
-    // pixels (mask <= 0.5 or n == 0) carry tau32 = -1e30: never counted.
-    const float4 *__restrict__ rp = M.rec + (int64_t)view * C.hm * C.wm + ys * (int64_t)C.wm + xs;
+    // Footprint scan over record plane A {m, D (NaN: cannot support)} and,
+    // for views whose supporting pixels do not share one tau, plane B {tau32,
+    // n}.  m_max: f32 widening is exact and monotone, so fmaxf in f32 equals
+    // the reference's f64 `if mv > m_max` (NaN never wins).  Support: the f32
+    // margin test e = |f32(x_d) - D| - tau32 has |error| < 2^-22 (|x_d| +
+    // tau_max); beyond M = 2^-20 (|x_d| + tau_max) from 0 it decides the
+    // reference's f64 test |x_d - f64(D)| <= tau(n) exactly, inside M the f64
+    // test runs.  NaN D (mask <= 0.5 or n == 0) never counts, never is unsure.
+    const int64_t plane = (int64_t)C.hm * C.wm;
+    const float2 *__restrict__ recA = M.rec + 2 * (int64_t)view * plane;
+    const float2 *__restrict__ rp = recA + ys * (int64_t)C.wm + xs;
+    const uint32_t *te = reinterpret_cast<const uint32_t *>(
+        M.bands + (int64_t)view * band_view_stride(C.nty, C.ntx) + (int64_t)C.nty * C.ntx);
+    const uint32_t tk0 = __ldg(te), tk1 = __ldg(te + 1);
     const double xd = q.x_d;
     const float xd32 = (float)xd;
     const float Mg = (float)(9.5367431640625e-07 * (fabs(xd) + C.tau_max));   // 2^-20
@@ -962,18 +973,34 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     bool unsure = false;
     // a running record pointer: +1 per pixel, + (wm - bw) at the end of a row
     const int64_t skip = (int64_t)C.wm - bw;
-    const float4 *__restrict__ pp = rp;
+    const float2 *__restrict__ pp = rp;
     int left = bw;
+    if (tk0 >= tk1) {   // one tau for every supporting pixel of the view (or none)
+        const float tau = __uint_as_float(tk0);
 #pragma unroll 4
-    for (int i = 0; i < npix; ++i) {
-        DIVAS_BOUND(pp, M.rec + (int64_t)view * C.hm * C.wm, (int64_t)C.hm * C.wm);
-        const float4 r = __ldg(pp);
-        mmax = fmaxf(mmax, r.x);
-        const float e = fabsf(xd32 - r.y) - r.z;
-        sup += (e <= -Mg) ? 1 : 0;
-        unsure |= fabsf(e) < Mg;
-        ++pp;
-        if (--left == 0) { left = bw; pp += skip; }
+        for (int i = 0; i < npix; ++i) {
+            DIVAS_BOUND(pp, recA, plane);
+            const float2 r = __ldg(pp);
+            mmax = fmaxf(mmax, r.x);
+            const float e = fabsf(xd32 - r.y) - tau;
+            sup += (e <= -Mg) ? 1 : 0;
+            unsure |= fabsf(e) < Mg;
+            ++pp;
+            if (--left == 0) { left = bw; pp += skip; }
+        }
+    } else {
+#pragma unroll 4
+        for (int i = 0; i < npix; ++i) {
+            DIVAS_BOUND(pp, recA, plane);
+            const float2 r = __ldg(pp);
+            const float t32 = __ldg(pp + plane).x;
+            mmax = fmaxf(mmax, r.x);
+            const float e = fabsf(xd32 - r.y) - t32;
+            sup += (e <= -Mg) ? 1 : 0;
+            unsure |= fabsf(e) < Mg;
+            ++pp;
+            if (--left == 0) { left = bw; pp += skip; }
+        }
     }
     if (unsure) PSTAT(10, 1);
     if (unsure) {   // some pixel within the margin: recount with the reference's f64 test
@@ -981,9 +1008,9 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
         pp = rp;
         left = bw;
         for (int i = 0; i < npix; ++i) {
-            const float4 r = __ldg(pp);
-            sup += (r.z >= 0.0f && fabs(xd - (double)r.y) <= tau_thin(C, __float_as_int(r.w)))
-                       ? 1 : 0;
+            const float2 r = __ldg(pp);
+            const int32_t n = __float_as_int(__ldg(pp + plane).y);
+            sup += (r.y == r.y && fabs(xd - (double)r.y) <= tau_thin(C, n)) ? 1 : 0;
             ++pp;
             if (--left == 0) { left = bw; pp += skip; }
         }
@@ -1458,15 +1485,16 @@ static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O,
 }
 
 // records + bands of views [v0, v0 + cnt) from planar refined masks
-static void launch_aux(const divas_fuse_args *a, int v0, int cnt, float4 *rec, double2 *bands,
+static void launch_aux(const divas_fuse_args *a, int v0, int cnt, float2 *rec, double2 *bands,
                        cudaStream_t s) {
     const BandParams B = band_params(a->pv, a->dx_vox, a->hm, a->wm);
     const int64_t plane = (int64_t)a->hm * a->wm;
     const float *m = a->masks + v0 * plane;
     const int32_t *n = a->nsamps + v0 * plane;
     const float *d = a->dexps + v0 * plane;
-    float4 *r = rec + v0 * plane;
-    double2 *b = bands + (int64_t)v0 * B.nty * B.ntx;
+    float2 *r = rec + 2 * v0 * plane;
+    double2 *b = bands + (int64_t)v0 * band_view_stride(B.nty, B.ntx);
+    launch_band_init(b, B, cnt, s);
     const bool vec = (a->wm % 4 == 0) &&
                      ((((uintptr_t)m) | ((uintptr_t)n) | ((uintptr_t)d)) & 15) == 0;
     if (vec) {
@@ -1571,7 +1599,7 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     FuseOut O{a->probs, a->n_thick, a->n_thin, a->sw, a->smw, a->st, a->occ,
               a->occ_peers, a->occ_peers ? a->n_peers : 0};
     FuseMaps M{a->masks, a->dmins, a->dmaxs, a->dexps, a->nsamps,
-               (const double2 *)a->bands, (const float4 *)a->records};
+               (const double2 *)a->bands, (const float2 *)a->records};
     char *ws = (char *)workspace;
     WsHeader *hdr = (WsHeader *)ws;
     uint32_t *work = (uint32_t *)(ws + L.work);
@@ -1579,7 +1607,7 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
               (double *)(ws + L.w), (double *)(ws + L.mw), (double *)(ws + L.t)};
     if (a->vox_hi == a->vox_lo) return DIVAS_OK;
     if (!M.rec && (steps & DIVAS_STEP_PAIRS)) {   // records + bands of the evaluated views
-        float4 *rec = (float4 *)(ws + L.rec);
+        float2 *rec = (float2 *)(ws + L.rec);
         double2 *bands = (double2 *)(ws + L.bands);
         launch_aux(a, v0, v1 - v0, rec, bands, s);
         if ((rc = check_launch("divas_fuse(aux)"))) return rc;

@@ -193,16 +193,17 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
     const int64_t gty = roi ? std::min<int64_t>(B.nty, (roi_h + kBandTile - 1) / kBandTile + 1)
                             : B.nty;
     const int4 *r4 = reinterpret_cast<const int4 *>(roi);
+    launch_band_init((double2 *)bands, B, nv, s);
     if (vec) {
         if (!keys) refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((gw / 4 + 255) / 256), (unsigned)gty, (unsigned)nv);
         band_pass<4, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, mm,
-                                              (double2 *)bands, (float4 *)records, nv, r4);
+                                              (double2 *)bands, (float2 *)records, nv, r4);
     } else {
         if (!keys) refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((gw + 255) / 256), (unsigned)gty, (unsigned)nv);
         band_pass<1, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, mm,
-                                              (double2 *)bands, (float4 *)records, nv, r4);
+                                              (double2 *)bands, (float2 *)records, nv, r4);
     }
     return check_launch("divas_refine_bands");
 }
