@@ -68,15 +68,17 @@ int divas_refine(int32_t nv, int64_t hm, int64_t wm,
 
 /* Refinement fused with the fusion's per-view "aux" data, in one pass:
  *   out      [nv][hm][wm] f32 refined masks as divas_refine (may be NULL);
- *   records  [nv][hm][wm] 16-byte scan records {refined mask, d_exp,
- *            tau_d(n) as f32 or -1e30 when the pixel cannot support a thin
- *            candidate, n_samples} (divas_records_size bytes);
- *   bands    [nv][ceil(hm/8)][ceil(wm/8)] {lo, hi} f64 per 8x8 tile: the depth
- *            interval in which a thin candidate can find support
- *            (divas_bands_size bytes).
+ *   records  per view two [hm][wm] float2 planes (divas_records_size bytes):
+ *            A = {refined mask, d_exp or NaN where the pixel cannot support a
+ *            thin candidate}, B = {tau_d(n) as f32 or -1e30, n_samples bits};
+ *   bands    per view [ceil(hm/8)][ceil(wm/8)] {lo, hi} f64 per 8x8 tile (the
+ *            depth interval in which a thin candidate can find support) and
+ *            one more 16-byte entry: the {min, max} order-preserving u32 key
+ *            of tau_d over the view's supporting pixels (divas_bands_size).
  * pv = FusionParams.as_vector() and dx_vox (the tolerances depend on them).
- * Views are independent: view k's slices start at k*hm*wm / k*nty*ntx, so a
- * single view can be (re)built in place with nv = 1 and offset pointers. */
+ * Views are independent: view k's slices start at k * divas_records_size(1,..)
+ * / k * divas_bands_size(1,..) bytes, so a single view can be (re)built in
+ * place with nv = 1 and offset pointers. */
 size_t divas_records_size(int32_t nv, int64_t hm, int64_t wm);
 size_t divas_bands_size(int32_t nv, int64_t hm, int64_t wm);
 int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm,

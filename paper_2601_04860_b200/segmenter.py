@@ -69,8 +69,9 @@ def refine_masks_device(masks, z_surface, n_samples, out=None, stream=None):
 
 class ViewAux:
     """The fusion's per-view auxiliary data (csrc/bands.cuh), device-resident:
-    ``records`` [nv, hm, wm] 16-byte scan records {refined mask, d_exp, tau,
-    n_samples} and ``bands`` [nv, ceil(hm/8), ceil(wm/8)] tile depth bands.
+    ``records`` (per view two float2 planes: {refined mask, d_exp or NaN},
+    {tau, n_samples}) and ``bands`` (per view the 8x8-tile depth bands and the
+    view's tau range), as bytes.
     Built by ``refine_bands_device`` for given FusionParams / voxel size."""
 
     def __init__(self, records, bands):
