@@ -395,8 +395,8 @@ def run_ours(args):
     if dist_on and not views_mode:
         from paper_2601_04860_b200.segmenter import refine_minmax_device
         mm_blocks, mm_rows = sharding.view_blocks(nv, world)
-        mm_mine = torch.zeros((mm_rows, 2), dtype=torch.int32, device=dev)
-        mm_all = torch.zeros((world * mm_rows, 2), dtype=torch.int32, device=dev)
+        mm_mine = torch.zeros((mm_rows, 4), dtype=torch.int32, device=dev)
+        mm_all = torch.zeros((world * mm_rows, 4), dtype=torch.int32, device=dev)
     roi = None
     if args.windows == "on" and not views_mode:
         roi = sharding.slab_view_rois(wl.density, pv, g, wl.origin, wl.dx, cams_t.cpu().numpy(),

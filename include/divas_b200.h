@@ -94,8 +94,9 @@ int divas_refine_bands(int32_t nv, int64_t hm, int64_t wm,
  * window); `out`, records and bands outside the windows are left untouched.
  * Used with the projection of a slab's gated voxels: the fusion of that slab
  * reads no pixel outside it (sharding.slab_view_rois). */
-/* The per-view z min / max on their own: keys [nv][2] order-preserving u32
- * (min, max) over the valid pixels (an empty view has min > max).  Lets the
+/* The per-view refine keys on their own: keys [nv][4] u32 = z min, z max
+ * (order-preserving f32 keys) and n min, n max over the valid pixels (an
+ * empty view has min > max).  Lets the
  * views' min/max passes be split across ranks and the keys exchanged; then
  * divas_refine_bands_keys builds the records from them (roi may be NULL). */
 int divas_refine_minmax(int32_t nv, int64_t hm, int64_t wm, const float *z_surface,

@@ -16,6 +16,9 @@
 namespace divas {
 
 constexpr int kBandTile = 8;
+// per-view refine keys: z min, z max (order-preserving f32 keys), n min, n max
+// over the valid pixels (n > 0)
+constexpr int kKeys = 4;
 
 struct BandParams {
     double gamma, beta, bmax, dx;
@@ -89,6 +92,15 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
     float2 *__restrict__ recA = records + 2 * off;   // this view's A plane
     float2 *__restrict__ recB = recA + plane;        // and B plane
     uint32_t tmin = 0xffffffffu, tmax = 0u;          // tau keys of the supporting pixels
+    // plane B is needed only when the view's supporting pixels can differ in
+    // tau: with the n range known (refine keys), one tau(n) for all -> skip it
+    bool write_b = true;
+    if (minmax) {
+        const uint32_t n0 = minmax[kKeys * v + 2], n1 = minmax[kKeys * v + 3];
+        double l0 = 0.0, h0 = 0.0;
+        write_b = n0 <= n1 && band_px(1.0f, (int32_t)n0, 0.0f, B, l0, h0) !=
+                                  band_px(1.0f, (int32_t)n1, 0.0f, B, l0, h0);
+    }
     // ROI (optional): the view's tile-aligned window {x0, y0, x1, y1}; the
     // grid covers the largest window, blocks past this view's window idle
     int rx0 = 0, rx1 = B.wm - 1, ty = (int)blockIdx.y;
@@ -105,7 +117,7 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
     bool any = false;
     double lo_ref = 0.0, span = 0.0;
     if (REFINE) {
-        const uint32_t kmin = minmax[2 * v], kmax = minmax[2 * v + 1];
+        const uint32_t kmin = minmax[kKeys * v], kmax = minmax[kKeys * v + 1];
         any = kmin <= kmax;
         lo_ref = any ? (double)key_f32(kmin) : 0.0;
         const double hi_ref = any ? (double)key_f32(kmax) : 0.0;
@@ -158,14 +170,16 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
             }
             if (VEC == 4) {
                 float4 *a4 = reinterpret_cast<float4 *>(recA + q);
-                float4 *b4 = reinterpret_cast<float4 *>(recB + q);
                 a4[0] = make_float4(a[0].x, a[0].y, a[1 % VEC].x, a[1 % VEC].y);
                 a4[1] = make_float4(a[2 % VEC].x, a[2 % VEC].y, a[3 % VEC].x, a[3 % VEC].y);
-                b4[0] = make_float4(b[0].x, b[0].y, b[1 % VEC].x, b[1 % VEC].y);
-                b4[1] = make_float4(b[2 % VEC].x, b[2 % VEC].y, b[3 % VEC].x, b[3 % VEC].y);
+                if (write_b) {
+                    float4 *b4 = reinterpret_cast<float4 *>(recB + q);
+                    b4[0] = make_float4(b[0].x, b[0].y, b[1 % VEC].x, b[1 % VEC].y);
+                    b4[1] = make_float4(b[2 % VEC].x, b[2 % VEC].y, b[3 % VEC].x, b[3 % VEC].y);
+                }
             } else {
                 recA[q] = a[0];
-                recB[q] = b[0];
+                if (write_b) recB[q] = b[0];
             }
         }
     }

@@ -845,8 +845,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     const float2 *recA = M.rec + 2 * vplane;                   // this view's record planes
     DIVAS_BOUND(recA + q, recA, plane);
     const float2 ra = __ldg(recA + q);                         // {m, d_exp or NaN}
-    const float2 rb = __ldg(recA + plane + q);                 // {tau32, n}
-    const int32_t ns = __float_as_int(rb.y);
+    const int32_t ns = __ldg(M.nsamps + pix);
     if (ns <= 0) return false;                                 // valids[view, py, px] == 0
     const float m = ra.x;
     PSTAT(2, 1);
@@ -1006,13 +1005,14 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     if (unsure) {   // some pixel within the margin: recount with the reference's f64 test
         sup = 0;
         pp = rp;
+        const int32_t *np = M.nsamps + (int64_t)view * plane + ys * (int64_t)C.wm + xs;
         left = bw;
         for (int i = 0; i < npix; ++i) {
             const float2 r = __ldg(pp);
-            const int32_t n = __float_as_int(__ldg(pp + plane).y);
-            sup += (r.y == r.y && fabs(xd - (double)r.y) <= tau_thin(C, n)) ? 1 : 0;
+            sup += (r.y == r.y && fabs(xd - (double)r.y) <= tau_thin(C, __ldg(np))) ? 1 : 0;
             ++pp;
-            if (--left == 0) { left = bw; pp += skip; }
+            ++np;
+            if (--left == 0) { left = bw; pp += skip; np += skip; }
         }
     }
     const double m_max = (double)mmax;

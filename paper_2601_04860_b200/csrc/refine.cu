@@ -21,8 +21,10 @@ constexpr int kRefineThreads = 256;
 __global__ void refine_init(uint32_t *ws, int nv) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nv) {
-        ws[2 * i] = 0xffffffffu;  // min key
-        ws[2 * i + 1] = 0u;       // max key
+        ws[kKeys * i] = 0xffffffffu;      // z min key
+        ws[kKeys * i + 1] = 0u;           // z max key
+        ws[kKeys * i + 2] = 0xffffffffu;  // n min over valid pixels
+        ws[kKeys * i + 3] = 0u;           // n max
     }
 }
 
@@ -57,26 +59,38 @@ refine_minmax(const float *__restrict__ z, const int32_t *__restrict__ n, int64_
     const int v = blockIdx.y;
     const float *zv = z + (int64_t)v * plane;
     const int32_t *nvp = n + (int64_t)v * plane;
-    uint32_t kmin = 0xffffffffu, kmax = 0u;
+    uint32_t kmin = 0xffffffffu, kmax = 0u, nmin = 0xffffffffu, nmax = 0u;
     const int64_t nvec = plane / VEC;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
          i += (int64_t)gridDim.x * blockDim.x) {
         if (VEC == 4) {
             const float4 zz = __ldg(reinterpret_cast<const float4 *>(zv) + i);
             const int4 nn = __ldg(reinterpret_cast<const int4 *>(nvp) + i);
+            // n > 0 pixels: z keys, and the n range (as unsigned: n > 0)
             if (nn.x > 0) { uint32_t k = f32_key(zz.x); kmin = min(kmin, k); kmax = max(kmax, k); }
             if (nn.y > 0) { uint32_t k = f32_key(zz.y); kmin = min(kmin, k); kmax = max(kmax, k); }
             if (nn.z > 0) { uint32_t k = f32_key(zz.z); kmin = min(kmin, k); kmax = max(kmax, k); }
             if (nn.w > 0) { uint32_t k = f32_key(zz.w); kmin = min(kmin, k); kmax = max(kmax, k); }
+            // invalid pixels (n <= 0) map to the neutral elements
+            nmin = min(nmin, min(min(nn.x > 0 ? (uint32_t)nn.x : 0xffffffffu,
+                                     nn.y > 0 ? (uint32_t)nn.y : 0xffffffffu),
+                                 min(nn.z > 0 ? (uint32_t)nn.z : 0xffffffffu,
+                                     nn.w > 0 ? (uint32_t)nn.w : 0xffffffffu)));
+            nmax = max(nmax, (uint32_t)max(max(nn.x, nn.y), max(max(nn.z, nn.w), 0)));
         } else {
-            if (__ldg(nvp + i) > 0) {
+            const int32_t nk = __ldg(nvp + i);
+            if (nk > 0) {
                 uint32_t k = f32_key(__ldg(zv + i));
                 kmin = min(kmin, k);
                 kmax = max(kmax, k);
+                nmin = min(nmin, (uint32_t)nk);
+                nmax = max(nmax, (uint32_t)nk);
             }
         }
     }
-    block_minmax_publish(kmin, kmax, ws + 2 * v);
+    block_minmax_publish(kmin, kmax, ws + kKeys * v);
+    __syncthreads();                                   // the publish reuses shared memory
+    block_minmax_publish(nmin, nmax, ws + kKeys * v + 2);
 }
 
 template <int VEC>
@@ -85,7 +99,7 @@ refine_apply(const float *__restrict__ mask, const float *__restrict__ z,
              const int32_t *__restrict__ n, float *__restrict__ out, int64_t plane,
              const uint32_t *__restrict__ ws) {
     const int v = gridDim.y - 1 - blockIdx.y;   // reverse view order: L2 reuse
-    const uint32_t kmin = ws[2 * v], kmax = ws[2 * v + 1];
+    const uint32_t kmin = ws[kKeys * v], kmax = ws[kKeys * v + 1];
     const bool any = kmin <= kmax;
     const double lo = any ? (double)key_f32(kmin) : 0.0;
     const double hi = any ? (double)key_f32(kmax) : 0.0;
@@ -123,7 +137,9 @@ static int blocks_per_view(int64_t plane, int nv) {
 
 using namespace divas;
 
-extern "C" size_t divas_refine_workspace_size(int32_t nv) { return (size_t)(nv > 0 ? nv : 1) * 8; }
+extern "C" size_t divas_refine_workspace_size(int32_t nv) {
+    return (size_t)(nv > 0 ? nv : 1) * kKeys * sizeof(uint32_t);
+}
 
 extern "C" int divas_refine(int32_t nv, int64_t hm, int64_t wm, const float *mask,
                             const float *z_surface, const int32_t *n_samples, float *out,

@@ -94,13 +94,14 @@ class ViewAux:
 
 
 def refine_minmax_device(z_surface, n_samples, keys=None, stream=None):
-    """Per-view z min / max over valid pixels as order-preserving uint32 keys
-    [nv, 2] (int32 tensor view), for ``refine_bands_device(keys=...)``; the
+    """Per-view z min / max (order-preserving uint32 keys) and n min / max over
+    valid pixels, [nv, 4] (int32 tensor view), for
+    ``refine_bands_device(keys=...)``; the
     views of a block can be computed on one rank and the keys all-gathered."""
     import torch
     nv, hm, wm = z_surface.shape
     if keys is None:
-        keys = torch.empty((nv, 2), dtype=torch.int32, device=z_surface.device)
+        keys = torch.empty((nv, 4), dtype=torch.int32, device=z_surface.device)
     _native.check(_native.lib().divas_refine_minmax(nv, hm, wm, _native.ptr(z_surface),
                                                     _native.ptr(n_samples), _native.ptr(keys),
                                                     _native.stream_handle(stream)),
@@ -149,8 +150,8 @@ def refine_bands_device(masks, z_surface, n_samples, d_exp, params, voxel_size, 
     ws = torch.empty(wsb, dtype=torch.uint8, device=masks.device)
     pvc = (ctypes.c_double * 14)(*pv.tolist())
     if keys is not None:
-        if keys.numel() < 2 * nv or keys.dtype != torch.int32 or not keys.is_cuda:
-            raise ValueError("keys must be a CUDA int32 [nv, 2] tensor")
+        if keys.numel() < 4 * nv or keys.dtype != torch.int32 or not keys.is_cuda:
+            raise ValueError("keys must be a CUDA int32 [nv, 4] tensor")
         _native.check(lib.divas_refine_bands_keys(
             nv, hm, wm, _native.ptr(masks), _native.ptr(z_surface), _native.ptr(n_samples),
             _native.ptr(d_exp), _native.ptr(out), pvc, float(voxel_size), _native.ptr(rec),

@@ -83,7 +83,7 @@ def test_minmax_keys_split_equal_full():
     m, z, n, d = t(raw), t(zs), t(case.nsamps), t(case.dexps)
     nv, hm, wm = m.shape
     out_a, aux_a = refine_bands_device(m, z, n, d, case.pv, case.dx)
-    keys = torch.zeros((nv, 2), dtype=torch.int32, device=dev)
+    keys = torch.zeros((nv, 4), dtype=torch.int32, device=dev)
     cut = nv // 2
     refine_minmax_device(z[:cut], n[:cut], keys=keys[:cut])
     refine_minmax_device(z[cut:], n[cut:], keys=keys[cut:])
