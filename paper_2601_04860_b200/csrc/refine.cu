@@ -212,9 +212,13 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
     launch_band_init((double2 *)bands, B, nv, s);
     if (vec) {
         if (!keys) refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
-        dim3 bg((unsigned)((gw / 4 + 255) / 256), (unsigned)gty, (unsigned)nv);
-        band_pass<4, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, mm,
-                                              (double2 *)bands, (float2 *)records, nv, r4);
+        // threads per block: enough 4-pixel chunks for the (window) width, in
+        // warps, so narrow windows do not idle half of every block
+        const int64_t chunks = gw / 4;
+        const int bt = (int)std::min<int64_t>(256, std::max<int64_t>(32, (chunks + 31) / 32 * 32));
+        dim3 bg((unsigned)((chunks + bt - 1) / bt), (unsigned)gty, (unsigned)nv);
+        band_pass<4, true><<<bg, bt, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, mm,
+                                             (double2 *)bands, (float2 *)records, nv, r4);
     } else {
         if (!keys) refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((gw + 255) / 256), (unsigned)gty, (unsigned)nv);
