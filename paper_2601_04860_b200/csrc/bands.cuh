@@ -78,8 +78,11 @@ __device__ __forceinline__ float band_px(float m, int32_t n, float d, const Band
 // One thread per VEC-pixel column chunk and 8 rows; TPW = 8 / VEC threads form
 // a tile row and combine with shuffles.  REFINE: also produce the refined mask
 // from the raw one (segmenter.py:141-152) and band on the refined values.
+#ifndef DIVAS_BAND_MINB
+#define DIVAS_BAND_MINB 6
+#endif
 template <int VEC, bool REFINE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, DIVAS_BAND_MINB)
 band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict__ z,
           const int32_t *__restrict__ nsamp, const float *__restrict__ dexp,
           float *__restrict__ refined, const uint32_t *__restrict__ minmax,
