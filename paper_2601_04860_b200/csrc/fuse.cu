@@ -189,17 +189,26 @@ struct BrickGrid {
     int nbx, nby, nbz;
 };
 
+// A brick's origin voxel, once per CTA (tile = blockIdx.x)
+struct BrickOrigin {
+    int64_t ix, iy, iz;
+};
+
+__device__ __forceinline__ BrickOrigin brick_origin(const BrickGrid &G, uint32_t tile) {
+    const uint32_t bz = tile % (uint32_t)G.nbz;
+    const uint32_t t1 = tile / (uint32_t)G.nbz;
+    const uint32_t by = t1 % (uint32_t)G.nby;
+    const uint32_t bx = t1 / (uint32_t)G.nby;
+    return BrickOrigin{G.ix0 + (int64_t)bx * kBrick, (int64_t)by * kBrick, (int64_t)bz * kBrick};
+}
+
 __device__ __forceinline__ unsigned gate_brick_quad(const float *__restrict__ dens,
                                                     const FuseConst &C, const FuseOut &O,
-                                                    const BrickGrid &G, int64_t tile, int j,
+                                                    const BrickOrigin &Bo, int j,
                                                     bool count_only, int64_t &base_out) {
-    const int64_t bz = tile % G.nbz;
-    const int64_t t1 = tile / G.nbz;
-    const int64_t by = t1 % G.nby;
-    const int64_t bx = t1 / G.nby;
-    const int64_t ix = G.ix0 + bx * kBrick + (j >> 6);
-    const int64_t iy = by * kBrick + ((j >> 2) & 15);
-    const int64_t iz = bz * kBrick + 4 * (j & 3);
+    const int64_t ix = Bo.ix + (j >> 6);
+    const int64_t iy = Bo.iy + ((j >> 2) & 15);
+    const int64_t iz = Bo.iz + 4 * (j & 3);
     const int64_t g = C.g;
     base_out = (ix * g + iy) * g + iz;
     if (ix >= g || iy >= g || iz >= g) return 0u;
@@ -239,10 +248,11 @@ gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
     __shared__ int s_w[kGateThreads / 32];
     int cnt = 0;
     int64_t base;
+    const BrickOrigin Bo = brick_origin(G, blockIdx.x);
 #pragma unroll
     for (int r = 0; r < kGateRounds; ++r)
-        cnt += __popc(gate_brick_quad(dens, C, O, G, blockIdx.x, r * kGateThreads + (int)threadIdx.x,
-                                      false, base));
+        cnt += __popc(gate_brick_quad(dens, C, O, Bo, r * kGateThreads + (int)threadIdx.x, false,
+                                      base));
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = cnt;
     __syncthreads();
@@ -313,10 +323,11 @@ gate_emit(const float *__restrict__ dens, FuseConst C, BrickGrid G,
     unsigned bits[kGateRounds];
     int lp[kGateRounds];
     int64_t qbase[kGateRounds];
+    const BrickOrigin Bo = brick_origin(G, blockIdx.x);
 #pragma unroll
     for (int r = 0; r < kGateRounds; ++r) {
-        bits[r] = gate_brick_quad(dens, C, none, G, blockIdx.x, r * kGateThreads + (int)threadIdx.x,
-                                  true, qbase[r]);
+        bits[r] = gate_brick_quad(dens, C, none, Bo, r * kGateThreads + (int)threadIdx.x, true,
+                                  qbase[r]);
         const int c = __popc(bits[r]);
         int incl = c;
         for (int o = 1; o < 32; o <<= 1) {

@@ -10,6 +10,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C3")
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--windows", default="on", choices=["on", "off"])
     args = ap.parse_args()
     import torch
     import workloads
@@ -26,10 +27,18 @@ def main():
     ws = None
     bands = None
     params = FusionParams()
-    for _ in range(args.steps):      # the bench step: refine+bands, fuse with those bands
+    roi = None
+    if args.windows == "on":
+        from paper_2601_04860_b200 import sharding
+        roi = sharding.slab_view_rois(wl.density, params.as_vector(), wl.g, wl.origin, wl.dx,
+                                      pack_cameras(wl.cams), [tuple(wl.shape[1:])] * wl.nv)
+    cap = fuser.capacity(wl.density, 0, wl.g ** 3)
+    occ = torch.empty(wl.g ** 3, dtype=torch.uint8, device=dev)
+    for _ in range(args.steps):      # the bench step: refine+records (windows), fuse
         _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps, params,
-                                        wl.dx, out=dv.masks, aux=bands)
-        out = fuser.run(wl.density, dv, probs=probs, occ=True, workspace=ws, aux=bands)
+                                        wl.dx, aux=bands, planar=False, roi=roi)
+        out = fuser.run(wl.density, dv, probs=probs, occ=occ, workspace=ws, aux=bands,
+                        max_gated=cap)
         ws = out["workspace"]
     torch.cuda.synchronize()
     print("gated", int(Fuser.gated_count(out).item()))
