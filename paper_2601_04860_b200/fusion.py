@@ -581,7 +581,8 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     on how the views are grouped).
     """
     import torch
-    from .segmenter import ViewAux, refine_bands_device
+    from .segmenter import (ViewAux, refine_bands_device, refine_masks_device,
+                            refine_minmax_device)
     g = int(grid.resolution)
     nvox = g ** 3
     _check_layout(grid, density)
@@ -607,6 +608,7 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     planes = {k: alloc((nv, hm, wm), dtype=torch.int32 if k == "nsamps" else torch.float32,
                        device=dev) for k in names}
     aux = ViewAux.empty(nv, hm, wm, dev)
+    keys_all = torch.empty((nv, 4), dtype=torch.int32, device=dev)
     refined = torch.empty((nv, hm, wm), dtype=torch.float32, device=dev) if return_refined else None
     host = (torch.empty((nv, hm, wm), dtype=torch.float32, pin_memory=True)
             if return_refined else None)
@@ -638,8 +640,10 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
             planes[k][i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(srcs[i][k], dt)),
                                        non_blocking=True)
 
-    full_names = ("raw", "z", "dexps", "nsamps")
-    win_names = ("dmins", "dmaxs")
+    # with windows, d_exp too is read only inside them (the band pass builds
+    # records there; the planar refinement does not need it)
+    full_names = ("raw", "z", "nsamps") if windows else ("raw", "z", "dexps", "nsamps")
+    win_names = ("dmins", "dmaxs", "dexps") if windows else ("dmins", "dmaxs")
     with torch.cuda.stream(up):
         for v0, v1 in bounds_k:
             for k in full_names:
@@ -687,10 +691,24 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     # 3. per chunk: refine -> pairs of those views; refined masks download
     for (v0, v1), ev in zip(bounds_k, ready):
         cur.wait_event(ev)
-        refine_bands_device(planes["raw"][v0:v1], planes["z"][v0:v1], planes["nsamps"][v0:v1],
-                            planes["dexps"][v0:v1], fuser.pv, fuser.dx,
-                            out=refined[v0:v1] if return_refined else None,
-                            aux=aux.view_slices(v0, v1, nv, hm, wm), planar=return_refined)
+        if rois is not None:
+            # planar refinement over the full planes (its keys kept), then the
+            # scan records / bands inside the windows only
+            keys = keys_all[v0:v1]
+            if return_refined:
+                refine_masks_device(planes["raw"][v0:v1], planes["z"][v0:v1],
+                                    planes["nsamps"][v0:v1], out=refined[v0:v1], keys=keys)
+            else:
+                refine_minmax_device(planes["z"][v0:v1], planes["nsamps"][v0:v1], keys=keys)
+            refine_bands_device(planes["raw"][v0:v1], planes["z"][v0:v1],
+                                planes["nsamps"][v0:v1], planes["dexps"][v0:v1], fuser.pv,
+                                fuser.dx, aux=aux.view_slices(v0, v1, nv, hm, wm), planar=False,
+                                roi=rois.subset(v0, v1), keys=keys)
+        else:
+            refine_bands_device(planes["raw"][v0:v1], planes["z"][v0:v1],
+                                planes["nsamps"][v0:v1], planes["dexps"][v0:v1], fuser.pv,
+                                fuser.dx, out=refined[v0:v1] if return_refined else None,
+                                aux=aux.view_slices(v0, v1, nv, hm, wm), planar=return_refined)
         fuser.run(dens, dv, steps=_native.STEP_PAIRS, view_range=(v0, v1), probs=False, **kw)
         if return_refined:
             down.wait_stream(cur)

@@ -38,12 +38,14 @@ class ConfidenceMask:
         return self.values.shape
 
 
-def refine_masks_device(masks, z_surface, n_samples, out=None, stream=None):
+def refine_masks_device(masks, z_surface, n_samples, out=None, stream=None, keys=None):
     """Batched refinement of device-resident planes ``[nv, hm, wm]``.
 
     ``masks``/``z_surface`` float32, ``n_samples`` int32 (CUDA tensors, C
     order).  Each view is normalised over its own valid pixels (padding with
     ``n_samples == 0`` is ignored and comes out as 0).  Returns ``out``.
+    ``keys``: an int32 [nv, 4] CUDA tensor that receives the views' refine
+    keys (as ``refine_minmax_device``), e.g. for ``refine_bands_device(keys=)``.
     """
     import torch
     if masks.dim() == 2:
@@ -60,7 +62,12 @@ def refine_masks_device(masks, z_surface, n_samples, out=None, stream=None):
         out = torch.empty_like(masks)
     lib = _native.lib()
     wsb = lib.divas_refine_workspace_size(nv)
-    ws = torch.empty(wsb, dtype=torch.uint8, device=masks.device)
+    if keys is not None:
+        if keys.numel() * keys.element_size() < wsb or not keys.is_cuda:
+            raise ValueError("keys must be a CUDA int32 [nv, 4] tensor")
+        ws = keys
+    else:
+        ws = torch.empty(wsb, dtype=torch.uint8, device=masks.device)
     _native.check(lib.divas_refine(nv, hm, wm, _native.ptr(masks), _native.ptr(z_surface),
                                    _native.ptr(n_samples), _native.ptr(out), _native.ptr(ws),
                                    wsb, _native.stream_handle(stream)), "divas_refine")
@@ -192,6 +199,16 @@ class ViewWindows:
         self.max_w = int((r[:, 2] - r[:, 0] + 1).max())
         self.max_h = int((r[:, 3] - r[:, 1] + 1).max())
         self.rects = torch.from_numpy(r).to(dev)
+
+    def subset(self, v0: int, v1: int) -> "ViewWindows":
+        """The windows of views [v0, v1) (shares the device rectangles)."""
+        w = ViewWindows.__new__(ViewWindows)
+        w.host = self.host[v0:v1]
+        w.nv = v1 - v0
+        w.max_w = int((w.host[:, 2] - w.host[:, 0] + 1).max())
+        w.max_h = int((w.host[:, 3] - w.host[:, 1] + 1).max())
+        w.rects = self.rects[v0:v1]
+        return w
 
     def fraction(self, hm: int, wm: int) -> float:
         """Share of the padded pixels inside the windows."""
