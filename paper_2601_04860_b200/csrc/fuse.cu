@@ -1647,11 +1647,16 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         C.view0 = v0;
         // a small shared-memory carveout (the queues of 4 CTAs fit in 64 KB)
         // leaves ~190 KB of L1 for the footprint / band / gradient gathers
-        static bool carve_set = false;
-        if (!carve_set) {
-            cudaFuncSetAttribute(fuse_pairs, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 kPairCarveout);
-            carve_set = true;
+        {   // once per device (an attribute of the function in each context)
+            static unsigned long long carve_set = 0;   // bit per device ordinal < 64
+            int dev = 0;
+            cudaGetDevice(&dev);
+            const unsigned long long bit = 1ull << (dev & 63);
+            if (!(__atomic_load_n(&carve_set, __ATOMIC_RELAXED) & bit)) {
+                cudaFuncSetAttribute(fuse_pairs, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     kPairCarveout);
+                __atomic_fetch_or(&carve_set, bit, __ATOMIC_RELAXED);
+            }
         }
         fuse_pairs<<<dim3((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)(v1 - v0)),
                      kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr, v1 - v0);
