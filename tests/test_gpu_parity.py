@@ -354,3 +354,27 @@ def test_refine_and_fuse_chunking(dev, name):
         for (vg, m), got in zip(raws, masks):
             assert got.shape == m.shape
             assert np.array_equal(got.values, refine_mask(m, vg).values), chunk
+
+
+@pytest.mark.parametrize("reps", [5, 9])
+def test_many_views_against_oracle(dev, reps):
+    """More than 32 / 64 views (several presence-bit words per slot, the
+    larger reduction instances): the sop scene's views repeated, each copy's
+    masks scaled differently, fused on the GPU and by the oracle."""
+    import dataclasses
+    case = golden_io.scene_cases()["sop"]
+    t = lambda a: np.concatenate([a] * reps, axis=0)  # noqa: E731
+    scale = np.repeat(np.linspace(0.55, 1.0, reps), case.masks.shape[0])[:, None, None]
+    big = dataclasses.replace(case, rots=t(case.rots), poss=t(case.poss), intr=t(case.intr),
+                              masks=np.clip(t(case.masks) * scale, 0, 1).astype(np.float32),
+                              dmins=t(case.dmins), dmaxs=t(case.dmaxs), dexps=t(case.dexps),
+                              nsamps=t(case.nsamps))
+    assert big.rots.shape[0] == 8 * reps
+    ref = _oracle(big)
+    got, _ = _gpu_fuse(big, dev)
+    assert np.array_equal(got["n_thick"], ref["n_thick"])
+    assert np.array_equal(got["n_thin"], ref["n_thin"])
+    assert np.array_equal(got["probs"] >= 0.5, ref["p"] >= 0.5)
+    rel = np.abs(got["probs"] - ref["p"]) / np.maximum(np.abs(ref["p"]), 1e-300)
+    assert rel.max(initial=0.0) <= REL_TOL
+    assert int(ref["n_thin"].max()) > 32 or int(ref["n_thick"].max()) > 0
