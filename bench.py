@@ -397,6 +397,12 @@ def run_ours(args):
         mm_blocks, mm_rows = sharding.view_blocks(nv, world)
         mm_mine = torch.zeros((mm_rows, 4), dtype=torch.int32, device=dev)
         mm_all = torch.zeros((world * mm_rows, 4), dtype=torch.int32, device=dev)
+        mm_peer = None
+        if args.gather == "p2p":
+            try:              # the keys' all-gather as NVLink stores + a device barrier
+                mm_peer = sharding.PeerGather((mm_rows, 4), torch.int32, dev)
+            except Exception:  # noqa: BLE001
+                mm_peer = None
     roi = None
     if args.windows == "on" and not views_mode:
         roi = sharding.slab_view_rois(wl.density, pv, g, wl.origin, wl.dx, cams_t.cpu().numpy(),
@@ -416,10 +422,14 @@ def run_ours(args):
             b0, b1 = mm_blocks[rank]
             if b1 > b0:
                 refine_minmax_device(dv.z_surface[b0:b1], dv.nsamps[b0:b1], keys=mm_mine[:b1 - b0])
-            dist.all_gather_into_tensor(mm_all, mm_mine)
+            if mm_peer is not None:
+                keys_all = mm_peer.gather(mm_mine).reshape(-1, 4)
+            else:
+                dist.all_gather_into_tensor(mm_all, mm_mine)
+                keys_all = mm_all
             _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps,
                                             params, wl.dx, aux=bands, planar=False, roi=roi,
-                                            keys=mm_all[:nv])
+                                            keys=keys_all[:nv])
         else:
             _m, bands = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps,
                                             params, wl.dx, aux=bands, planar=False, roi=roi)

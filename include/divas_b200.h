@@ -290,6 +290,13 @@ const char *divas_last_error(void);
  * windowed upload of view planes in refine_and_fuse. */
 int divas_copy2d_h2d(void *dst, size_t dpitch, const void *src, size_t spitch,
                      size_t width_bytes, size_t height, void *stream);
+
+/* Store `bytes` of device memory src into every buffer of a DEVICE table of
+ * n_peers pointers (symmetric-memory peer mappings), at `offset`: one rank's
+ * block of an all-gather as NVLink stores in one launch (the caller then runs
+ * a device barrier). */
+int divas_peer_put(const void *src, size_t bytes, uint8_t *const *peers, int32_t n_peers,
+                   size_t offset, void *stream);
 int divas_abi_version(void);
 
 #ifdef __cplusplus

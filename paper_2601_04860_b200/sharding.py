@@ -27,7 +27,8 @@ import numpy as np
 
 __all__ = ["slice_weights", "balanced_slabs", "equal_slabs", "slab_voxel_range",
            "broadcast_views", "gather_occupancy", "gather_slab_values",
-           "view_blocks", "ViewShardPlan", "PeerOccupancy", "gated_bbox", "slab_view_rois"]
+           "view_blocks", "ViewShardPlan", "PeerOccupancy", "PeerGather", "gated_bbox",
+           "slab_view_rois"]
 
 # relative cost of one voxel in the dense gate pass vs one gated voxel-view pair
 STREAM_WEIGHT = 0.02
@@ -225,6 +226,37 @@ class PeerOccupancy:
         """Device-side barrier on the current stream: every rank's stores of
         this step have landed in every buffer after it."""
         self.hdl.barrier(channel=0)
+
+
+class PeerGather:
+    """A small all-gather as NVLink stores: a symmetric-memory buffer of
+    ``world`` blocks; ``gather(src)`` stores this rank's block into every
+    rank's buffer (``divas_peer_put``, one launch) and runs a device barrier,
+    after which ``buf`` holds every rank's block on every rank."""
+
+    def __init__(self, block_shape, dtype, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        group = group or dist.group.WORLD
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.block = tuple(block_shape)
+        self.buf = symm.empty((self.world,) + self.block, dtype=dtype, device=device)
+        self.hdl = symm.rendezvous(self.buf, group)
+        self.ptr_table = torch.tensor([int(p) for p in self.hdl.buffer_ptrs], dtype=torch.int64,
+                                      device=device)
+        self.block_bytes = self.buf[0].numel() * self.buf.element_size()
+
+    def gather(self, src):
+        from . import _native
+        if src.numel() * src.element_size() != self.block_bytes or not src.is_contiguous():
+            raise ValueError("one contiguous block per rank")
+        _native.check(_native.lib().divas_peer_put(
+            _native.ptr(src), self.block_bytes, _native.ptr(self.ptr_table), self.world,
+            self.rank * self.block_bytes, _native.stream_handle()), "divas_peer_put")
+        self.hdl.barrier(channel=0)
+        return self.buf
 
 
 def gather_slab_values(vals_slab, slabs, g: int, rank: int, group=None):

@@ -84,3 +84,44 @@ def test_peer_occupancy_unaligned_slab():
     torch.cuda.synchronize()
     assert torch.equal(buf, occ_full)
     assert int(np.count_nonzero(occ_full.cpu().numpy())) > 0
+
+
+def test_peer_put_blocks():
+    """divas_peer_put stores one block into every listed buffer at an offset."""
+    import torch
+    from paper_2601_04860_b200 import _native
+    dev = torch.device("cuda", 0)
+    bufs = [torch.zeros(3 * 1000 + 7, dtype=torch.uint8, device=dev) for _ in range(3)]
+    table = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=dev)
+    for r, nbytes in enumerate((1000, 1003, 17)):
+        src = torch.randint(0, 255, (nbytes,), dtype=torch.uint8, device=dev)
+        off = r * 1000 + (r == 2)
+        _native.check(_native.lib().divas_peer_put(src.data_ptr(), nbytes, table.data_ptr(), 3,
+                                                   off, _native.stream_handle()), "peer_put")
+        torch.cuda.synchronize()
+        for b in bufs:
+            assert torch.equal(b[off:off + nbytes], src)
+
+
+def test_peer_gather_world1():
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_2601_04860_b200 import sharding
+    dev = torch.device("cuda", 0)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=dev)
+    try:
+        pg = sharding.PeerGather((5, 4), torch.int32, dev)
+        src = torch.arange(20, dtype=torch.int32, device=dev).reshape(5, 4)
+        out = pg.gather(src)
+        torch.cuda.synchronize()
+        assert torch.equal(out[0], src)
+    finally:
+        dist.destroy_process_group()
