@@ -469,6 +469,16 @@ def run_ours(args):
     torch.cuda.synchronize()
     if dist_on:
         dist.barrier()
+    if dist_on and not views_mode and mm_peer is not None:
+        # the keys' NVLink all-gather must equal NCCL's, or it is not used
+        kp = mm_peer.gather(mm_mine).reshape(-1, 4).clone()
+        dist.all_gather_into_tensor(mm_all, mm_mine)
+        bad = torch.tensor([0 if torch.equal(kp, mm_all) else 1], device=dev)
+        dist.all_reduce(bad)
+        if int(bad.item()):
+            mm_peer = None
+        torch.cuda.synchronize()
+        dist.barrier()
     if peer is not None:
         # the fused gather must equal the NCCL one bit for bit, or it is not used
         out_c, occ_p = step(check=True)
@@ -579,6 +589,10 @@ def run_ours(args):
                             "refine+aux(all views; records in windows) + fuse(slab, threshold fused)"
                             + (" + all-gather(occupancy)" if dist_on else "")),
                    "gather": gather_mode,
+                   "refine_keys": (None if not dist_on or views_mode else
+                                   "per-rank view blocks, all-gathered as NVLink stores"
+                                   if mm_peer is not None else
+                                   "per-rank view blocks, NCCL all_gather"),
                    "windows": (None if roi is None else
                                f"scan records/bands built in per-view windows around the "
                                f"projected gated region: {roi_frac:.3f} of the pixels"),
