@@ -24,6 +24,9 @@
  *   divas_overlay        <- fusion._overlay_kernel           fusion.py:771-843
  *   divas_vgrid_payload  <- io.write_vgrid's transpose        io.py:59-69
  *   divas_pair_trace     <- fusion.thick_check / thin_check   fusion.py:549-646
+ *   divas_render         <- render._render (render_view)      render.py:221-292
+ *   divas_march_rays     <- render._march (march_ray)         render.py:160-218, :257-267
+ *   divas_bake_density   <- scene.bake_density_grid           scene.py:194-201
  */
 #ifndef DIVAS_B200_H
 #define DIVAS_B200_H
@@ -35,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DIVAS_ABI_VERSION 7
+#define DIVAS_ABI_VERSION 8
 
 /* error codes */
 #define DIVAS_OK          0
@@ -282,6 +285,54 @@ int divas_overlay(const double *cam, int32_t h, int32_t w, const float *dmin,
                   int64_t g, const double origin[3], double dx_vox,
                   const double bc[3], const double bh[3], int32_t unbounded,
                   double thr, uint8_t *out, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Fixture producers: the volumetric ray       */
+/* marcher and the density bake.  The scene is HOST memory (it is copied    */
+/* into the launch); cams / rays / outputs are DEVICE memory.               */
+/* ---------------------------------------------------------------------- */
+#define DIVAS_MAX_PRIMS 128
+
+typedef struct {                /* SceneModel.packed() (scene.py:126-151)   */
+    int32_t n_prims;            /* 0 .. DIVAS_MAX_PRIMS                     */
+    const uint8_t *kinds;       /* [n] 0 sphere, 1 box, 2 capsule           */
+    const double *params;       /* [n][7] (packed() layout)                 */
+    const double *density;      /* [n]                                      */
+    const double *colors;       /* [n][3]                                   */
+    const double *soft;         /* [n] soft-edge widths                     */
+    double background[3];
+} divas_scene;
+
+typedef struct {                /* RenderConfig (render.py:37-50)           */
+    int32_t samples_per_ray;
+    double near_, far_, tau_cw, min_weight;
+} divas_render_cfg;
+
+/* render_view for nv cameras of one size: outputs [nv][h][w] (rgb
+ * [nv][h][w][3]).  unsure (nullable, [nv][h][w]) flags the pixels whose
+ * bits could differ from the reference's because CUDA's exp and the C
+ * library's differ in the last place and that difference could cross a
+ * decision or an f32 rounding boundary (a certified bound, see render.cu);
+ * every other pixel is bit-identical to render_view's. */
+int divas_render(const divas_scene *scene, const divas_render_cfg *cfg, int32_t nv,
+                 const double *cams, int32_t h, int32_t w, float *rgb, float *d_min,
+                 float *d_max, float *d_exp, int32_t *n_samples, float *z_surface,
+                 uint8_t *unsure, void *stream);
+
+/* march_ray on n unit rays [n][6] (origin, direction): out [n][8] f64 =
+ * r, g, b, d_min, d_max, d_exp, n_samples, z_surface; err (nullable) [n][4] =
+ * bounds of |out - reference| for r, g, b, d_exp; unsure (nullable) [n] as
+ * above (d_min, d_max, z_surface, n_samples exact when 0). */
+int divas_march_rays(const divas_scene *scene, const divas_render_cfg *cfg, int64_t n,
+                     const double *rays, double *out, double *err, uint8_t *unsure,
+                     void *stream);
+
+/* bake_density_grid: out [G^3] f32, [ix,iy,iz], voxel centres
+ * origin + (i + 0.5) * dx_vox, contracted (geometry.contract) when
+ * unbounded with bounds centre bc / half extent bh (HOST arrays). */
+int divas_bake_density(const divas_scene *scene, int64_t g, const double origin[3],
+                       double dx_vox, int32_t unbounded, const double bc[3], const double bh[3],
+                       float *out, void *stream);
 
 /* ---------------------------------------------------------------------- */
 const char *divas_last_error(void);

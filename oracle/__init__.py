@@ -51,10 +51,22 @@ class _FuseArgs(ctypes.Structure):
     ]
 
 
+class _Scene(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("kinds", _U8P), ("params", _F64P), ("dens", _F64P),
+                ("cols", _F64P), ("soft", _F64P), ("bg", _F64P)]
+
+
+class _RenderCfg(ctypes.Structure):
+    _fields_ = [("n_steps", ctypes.c_int64), ("near_", ctypes.c_double),
+                ("far_", ctypes.c_double), ("tau_cw", ctypes.c_double),
+                ("min_w", ctypes.c_double)]
+
+
 def build(force: bool = False) -> str:
     """Compile divas_oracle.c with the committed Makefile; returns the .so path."""
-    if force or not os.path.exists(_LIB_PATH) or \
-            os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "divas_oracle.c")):
+    srcs = ("divas_oracle.c", "divas_oracle_render.c", "Makefile")
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
+            os.path.getmtime(os.path.join(_HERE, f)) for f in srcs):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return _LIB_PATH
 
@@ -70,6 +82,12 @@ def load():
                                                                        ctypes.c_double, ctypes.c_double, _F64P]
             lib.oracle_fuse.argtypes = [ctypes.POINTER(_FuseArgs)]
             lib.oracle_max_threads.restype = ctypes.c_int
+            sp, rp = ctypes.POINTER(_Scene), ctypes.POINTER(_RenderCfg)
+            lib.oracle_march.argtypes = [sp, rp, _F64P, _F64P]
+            lib.oracle_render.argtypes = [sp, rp, _F64P, _F64P, _F64P, _F32P, _F32P, _F32P,
+                                          _F32P, _I32P, _F32P, ctypes.c_int64]
+            lib.oracle_bake.argtypes = [sp, ctypes.c_int64, _F64P, ctypes.c_double,
+                                        ctypes.c_int64, _F64P, _F64P, _F32P, ctypes.c_int64]
             _lib = lib
     return _lib
 
@@ -265,3 +283,87 @@ def threshold(probs, thr=0.5) -> np.ndarray:
 
 def extract(probs, thr=0.5) -> np.ndarray:
     return np.argwhere(np.asarray(probs) >= thr)
+
+
+# --------------------------------------------------------------------------
+# fixture producers: render_view / march_ray (render.py:96-292) and
+# bake_density_grid (scene.py:194-201)
+# --------------------------------------------------------------------------
+
+def _scene_struct(scene):
+    """(ctypes struct, keep-alive arrays) from a SceneModel-like object
+    (``.packed()`` + ``.background``) or a packed tuple
+    (kinds, params, dens, cols, soft, bg)."""
+    if hasattr(scene, "packed"):
+        kinds, params, dens, cols, _oids, soft = scene.packed()
+        bg = scene.background
+    else:
+        kinds, params, dens, cols, soft, bg = scene
+    keep = [_c(kinds, np.uint8).reshape(-1), _c(params, np.float64).reshape(-1, 7),
+            _c(dens, np.float64).reshape(-1), _c(cols, np.float64).reshape(-1, 3),
+            _c(soft, np.float64).reshape(-1), _c(bg, np.float64).reshape(3)]
+    st = _Scene(len(keep[0]), _p(keep[0], _U8P), _p(keep[1], _F64P), _p(keep[2], _F64P),
+                _p(keep[3], _F64P), _p(keep[4], _F64P), _p(keep[5], _F64P))
+    return st, keep
+
+
+def _cfg_struct(cfg):
+    if hasattr(cfg, "samples_per_ray"):
+        cfg = (cfg.samples_per_ray, cfg.near, cfg.far, cfg.tau_cw, cfg.min_weight)
+    return _RenderCfg(int(cfg[0]), float(cfg[1]), float(cfg[2]), float(cfg[3]), float(cfg[4]))
+
+
+def march(scene, cfg, rays) -> np.ndarray:
+    """``_march`` on unit rays (n, 6) = origin, direction; returns (n, 8) f64
+    (r, g, b, d_min, d_max, d_exp, n_samples, z_surface)."""
+    st, _keep = _scene_struct(scene)
+    rc = _cfg_struct(cfg)
+    rays = _c(rays, np.float64).reshape(-1, 6)
+    out = np.zeros((len(rays), 8))
+    lib = load()
+    for i in range(len(rays)):
+        lib.oracle_march(ctypes.byref(st), ctypes.byref(rc), _p(rays[i], _F64P),
+                         _p(out[i], _F64P))
+    return out
+
+
+def render(scene, camera, cfg, nthreads=0):
+    """``render_view``'s per-pixel arrays for one camera: dict of rgb (H, W, 3),
+    d_min, d_max, d_exp, z_surface (H, W) f32 and n_samples (H, W) i32."""
+    st, _keep = _scene_struct(scene)
+    rc = _cfg_struct(cfg)
+    rot = _c(camera.rotation, np.float64)
+    pos = _c(camera.position, np.float64)
+    intr = np.array([camera.fx, camera.fy, camera.cx, camera.cy, camera.width, camera.height],
+                    np.float64)
+    h, w = int(camera.height), int(camera.width)
+    o = dict(rgb=np.zeros((h, w, 3), np.float32), d_min=np.zeros((h, w), np.float32),
+             d_max=np.zeros((h, w), np.float32), d_exp=np.zeros((h, w), np.float32),
+             n_samples=np.zeros((h, w), np.int32), z_surface=np.zeros((h, w), np.float32))
+    load().oracle_render(ctypes.byref(st), ctypes.byref(rc), _p(rot, _F64P), _p(pos, _F64P),
+                         _p(intr, _F64P), _p(o["rgb"], _F32P), _p(o["d_min"], _F32P),
+                         _p(o["d_max"], _F32P), _p(o["d_exp"], _F32P),
+                         _p(o["n_samples"], _I32P), _p(o["z_surface"], _F32P),
+                         nthreads or max_threads())
+    return o
+
+
+def bake(scene, g, half, origin, bounds=None, nthreads=0) -> np.ndarray:
+    """``bake_density_grid`` values (G, G, G) f32; ``bounds`` = (min, max,
+    unbounded) or a SceneBounds-like object."""
+    st, _keep = _scene_struct(scene)
+    origin = _c(origin, np.float64).reshape(3)
+    dx = 2.0 * float(half) / int(g)                    # VoxelGrid.voxel_size
+    unb = 0
+    bc = np.zeros(3)
+    bh = np.ones(3)
+    if bounds is not None:
+        lo, hi, unb = ((bounds.min, bounds.max, bounds.unbounded)
+                       if hasattr(bounds, "unbounded") else bounds)
+        lo, hi = np.asarray(lo, np.float64), np.asarray(hi, np.float64)
+        bc, bh = 0.5 * (lo + hi), 0.5 * (hi - lo)      # SceneBounds.center / half
+        unb = 1 if unb else 0
+    out = np.zeros(int(g) ** 3, np.float32)
+    load().oracle_bake(ctypes.byref(st), int(g), _p(origin, _F64P), dx, unb, _p(bc, _F64P),
+                       _p(bh, _F64P), _p(out, _F32P), nthreads or max_threads())
+    return out.reshape(int(g), int(g), int(g))

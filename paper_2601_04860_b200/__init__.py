@@ -7,8 +7,10 @@ entry points on top.  See DESIGN.md.
 """
 
 from .geometry import Camera, SceneBounds, VoxelGrid, look_at
-from .render import ViewGeometry
-from .scene import DensityGrid
+from .render import (RaySample, RenderConfig, ViewGeometry, march_ray, march_rays_device,
+                     render_view, render_views_device)
+from .scene import (DensityGrid, SceneModel, ScenePrimitive, bake_density_device,
+                    bake_density_grid)
 from .segmenter import (ConfidenceMask, ViewAux, ViewWindows, refine_bands_device, refine_mask, refine_masks,
                         refine_masks_device)
 from .fusion import (DeviceViews, FusionParams, FusionStats, Fuser, OccupancyGrid,
@@ -24,6 +26,9 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Camera", "SceneBounds", "VoxelGrid", "look_at", "ViewGeometry", "DensityGrid",
+    "RenderConfig", "RaySample", "render_view", "render_views_device", "march_ray",
+    "march_rays_device", "ScenePrimitive", "SceneModel", "bake_density_grid",
+    "bake_density_device",
     "ConfidenceMask", "ViewAux", "ViewWindows", "refine_mask", "refine_masks", "refine_masks_device", "refine_bands_device",
     "DeviceViews", "FusionParams", "FusionStats", "Fuser", "OccupancyGrid",
     "fuse", "fuse_with_stats", "refine_and_fuse", "project_grid_overlay",

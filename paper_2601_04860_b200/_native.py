@@ -28,6 +28,7 @@ EXPORTS = (
     "divas_overlay", "divas_vgrid_payload",
     "divas_last_error", "divas_abi_version", "divas_refine_bands_roi", "divas_refine_minmax",
     "divas_refine_bands_keys", "divas_copy2d_h2d", "divas_peer_put",
+    "divas_render", "divas_march_rays", "divas_bake_density",
 )
 
 _VP = ctypes.c_void_p
@@ -50,6 +51,24 @@ class FuseArgs(ctypes.Structure):
         ("view_lo", ctypes.c_int32), ("view_hi", ctypes.c_int32),
         ("occ_peers", _VP), ("n_peers", ctypes.c_int32),
     ]
+
+MAX_PRIMS = 128
+
+
+class Scene(ctypes.Structure):
+    """Mirror of ``divas_scene`` (host arrays; the struct is copied into the launch)."""
+
+    _fields_ = [("n_prims", ctypes.c_int32), ("kinds", _VP), ("params", _VP),
+                ("density", _VP), ("colors", _VP), ("soft", _VP), ("background", _D3)]
+
+
+class RenderCfg(ctypes.Structure):
+    """Mirror of ``divas_render_cfg``."""
+
+    _fields_ = [("samples_per_ray", ctypes.c_int32), ("near_", ctypes.c_double),
+                ("far_", ctypes.c_double), ("tau_cw", ctypes.c_double),
+                ("min_weight", ctypes.c_double)]
+
 
 FUSE_FULL = 0
 STEP_GATE, STEP_CLEAR_ALL, STEP_CLEAR_VIEWS, STEP_PAIRS, STEP_REDUCE = 1, 2, 4, 8, 16
@@ -93,6 +112,13 @@ def _declare(lib):
                                          ctypes.POINTER(D), D, ctypes.POINTER(D),
                                          ctypes.POINTER(D), I32, D, _VP, _VP]),
         "divas_vgrid_payload": (ctypes.c_int, [_VP, I64, _VP, _VP]),
+        "divas_render": (ctypes.c_int, [ctypes.POINTER(Scene), ctypes.POINTER(RenderCfg), I32,
+                                        _VP, I32, I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+        "divas_march_rays": (ctypes.c_int, [ctypes.POINTER(Scene), ctypes.POINTER(RenderCfg),
+                                            I64, _VP, _VP, _VP, _VP, _VP]),
+        "divas_bake_density": (ctypes.c_int, [ctypes.POINTER(Scene), I64, ctypes.POINTER(D), D,
+                                              I32, ctypes.POINTER(D), ctypes.POINTER(D), _VP,
+                                              _VP]),
         "divas_last_error": (ctypes.c_char_p, []),
         "divas_abi_version": (ctypes.c_int, []),
     }

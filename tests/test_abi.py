@@ -39,7 +39,7 @@ def test_library_exports_every_symbol(lib):
 
 
 def test_version_and_error(lib):
-    assert lib.divas_abi_version() == 7
+    assert lib.divas_abi_version() == 8
     assert isinstance(lib.divas_last_error(), bytes)
 
 
@@ -64,9 +64,18 @@ int main(void) {{ printf("%zu\\n", sizeof({cname})); {body} return 0; }}
                                            check=True).stdout.split()]
 
 
-@pytest.mark.parametrize("which", ["fuse", "trace", "record"])
+@pytest.mark.parametrize("which", ["fuse", "trace", "record", "scene", "render_cfg"])
 def test_struct_layout_matches_header(tmp_path, which):
     from paper_2601_04860_b200 import trace
+    if which in ("scene", "render_cfg"):
+        st, cname = ((_native.Scene, "divas_scene") if which == "scene"
+                     else (_native.RenderCfg, "divas_render_cfg"))
+        fields = [f[0] for f in st._fields_]
+        vals = _c_layout(tmp_path, cname, fields)
+        assert vals[0] == ctypes.sizeof(st)
+        for f, off in zip(fields, vals[1:]):
+            assert getattr(st, f).offset == off, f
+        return
     if which == "record":
         names = list(trace.RECORD_DTYPE.names)
         vals = _c_layout(tmp_path, "divas_pair_record", names)
@@ -92,3 +101,24 @@ def test_invalid_arguments_rejected_without_gpu(lib):
     assert b"grid" in lib.divas_last_error()
     assert lib.divas_refine(0, 1, 1, None, None, None, None, None, 0, None) == 1
     assert lib.divas_threshold(None, 10, 0.5, 0, None, None, None, None, 0, None) == 1
+
+
+def test_render_arguments_rejected_without_gpu(lib):
+    """Scene / config validation of the fixture producers (RenderConfig's own
+    checks, render.py:44-50) happens before any CUDA call."""
+    sc = _native.Scene()
+    sc.n_prims = _native.MAX_PRIMS + 1
+    cfg = _native.RenderCfg(16, 0.5, 6.0, 0.75, 1e-4)
+    assert lib.divas_render(ctypes.byref(sc), ctypes.byref(cfg), 1, None, 4, 4, *([None] * 7),
+                            None) == 1
+    assert b"primitives" in lib.divas_last_error()
+    sc.n_prims = 0
+    for bad in ((0, 0.5, 6.0, 0.75), (16, 6.0, 0.5, 0.75), (16, 0.5, 6.0, 0.0),
+                (16, 0.5, 6.0, 1.5)):
+        cfg = _native.RenderCfg(*bad, 1e-4)
+        assert lib.divas_render(ctypes.byref(sc), ctypes.byref(cfg), 1, None, 4, 4,
+                                *([None] * 7), None) == 1
+        assert lib.divas_march_rays(ctypes.byref(sc), ctypes.byref(cfg), 1, None, None, None,
+                                    None, None) == 1
+    o = (ctypes.c_double * 3)()
+    assert lib.divas_bake_density(ctypes.byref(sc), 0, o, 0.1, 0, o, o, None, None) == 1

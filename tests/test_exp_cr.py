@@ -1,0 +1,85 @@
+"""Pin the marcher's correctly rounded exp (csrc/exp_cr.cuh) on the CPU.
+
+The header is host + device code; here it is compiled with g++ (no FMA
+contraction) and checked on random and adversarial x in [-38, 0]:
+
+* against a 40-digit decimal exp rounded to the nearest double: every
+  result not flagged ``ambiguous`` is the correctly rounded value, and an
+  ambiguous one is the correctly rounded value or its flagged neighbour;
+* against the C library's exp (what the reference's numba math.exp calls):
+  equal whenever not ambiguous -- the premise of the marcher's certificate.
+"""
+
+import ctypes
+import math
+import os
+import subprocess
+from decimal import Decimal, getcontext
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "paper_2601_04860_b200", "csrc")
+
+
+@pytest.fixture(scope="module")
+def lib(tmp_path_factory):
+    d = tmp_path_factory.mktemp("expcr")
+    src = d / "shim.cpp"
+    src.write_text('#include "exp_cr.cuh"\n'
+                   'extern "C" double exp_cr_host(double x, int *amb, double *alt) {\n'
+                   '  bool a; double r = divas::exp_cr(x, a, *alt); *amb = a; return r; }\n'
+                   'extern "C" double libm_exp(double x) { return exp(x); }\n')
+    so = d / "libexpcr.so"
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
+                    f"-I{HDR}", str(src), "-o", str(so)], check=True)
+    lib = ctypes.CDLL(str(so))
+    lib.exp_cr_host.restype = ctypes.c_double
+    lib.exp_cr_host.argtypes = [ctypes.c_double, ctypes.POINTER(ctypes.c_int),
+                                ctypes.POINTER(ctypes.c_double)]
+    lib.libm_exp.restype = ctypes.c_double
+    lib.libm_exp.argtypes = [ctypes.c_double]
+    return lib
+
+
+def _xs():
+    rng = np.random.default_rng(7)
+    xs = list(-rng.uniform(0, 38, 4000))
+    xs += list(-np.exp(rng.uniform(np.log(1e-300), np.log(38.0), 2000)))    # tiny to large
+    xs += [-1e-300, -5e-324, -2.0 ** -60, -2.0 ** -53, -2.0 ** -30, -1e-11, -0.5, -math.log(2),
+           -1.4470486111111112, -0.0215, -38.0, -37.999999999999, -0.34657359027997264,
+           -0.3465735902799727]
+    # the marcher's own arguments: -sigma * dt for the reference scenes
+    for sigma in (46.0, 40.0, 4.0, 50.0, 1.5, 500.0, 30.0, 12.0, 8.0, 1e-9):
+        for dt in ((12.5 - 0.4) / 384, (6.0 - 0.5) / 256, (6.0 - 0.5) / 128, (7.0 - 0.3) / 200):
+            xs.append(-sigma * dt)
+    return xs
+
+
+def test_exp_cr_is_correctly_rounded(lib):
+    getcontext().prec = 40
+    amb_n = 0
+    for x in _xs():
+        a = ctypes.c_int()
+        alt = ctypes.c_double()
+        r = lib.exp_cr_host(x, ctypes.byref(a), ctypes.byref(alt))
+        cr = float(str(Decimal(x).exp()))
+        if a.value:
+            amb_n += 1
+            assert cr in (r, alt.value), x
+        else:
+            assert r == cr, (x, r, cr)
+    assert amb_n < 0.1 * len(_xs())
+
+
+def test_exp_cr_matches_libm_when_unambiguous(lib):
+    for x in _xs():
+        a = ctypes.c_int()
+        alt = ctypes.c_double()
+        r = lib.exp_cr_host(x, ctypes.byref(a), ctypes.byref(alt))
+        m = lib.libm_exp(x)
+        if not a.value:
+            assert r == m, (x, r, m)
+        else:
+            assert m in (r, alt.value), x

@@ -1,0 +1,225 @@
+"""Fixture producers on the device (divas_render / divas_march_rays /
+divas_bake_density) against the reference (golden vectors) and the oracle.
+
+Bar: the bake is bit-exact.  The marcher is bit-exact on every pixel it does
+not flag ``unsure`` -- the flag is the kernel's certificate that CUDA's exp
+and the C library's (each within 1 ulp) cannot have moved a decision or an
+f32 rounding there -- and flags at most 0.1 % of the pixels (tau_cw < 1; at
+tau_cw = 1 the cutoff itself is ulp-sensitive and may flag any ray); flagged pixels
+stay within one sample spacing in depth and 1e-6 in colour.  Plus the
+reference's own render tests (pkg/tests/test_render.py) restated.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+MAX_UNSURE = 1e-3
+
+
+def _bits(a):
+    a = np.asarray(a)
+    return a.view(np.uint32) if a.dtype == np.float32 else a
+
+
+def _render(sc, cams, cfg):
+    from paper_2601_04860_b200.render import render_views_device
+    o = render_views_device(sc, cams, cfg, unsure=True)
+    return {k: v.cpu().numpy() for k, v in o.items() if not k.startswith("_")}
+
+
+def _compare(o, ref, cfg, idx=0):
+    uns = o["unsure"][idx].astype(bool)
+    if cfg.tau_cw < 1.0:
+        # with tau_cw = 1 the cutoff is "cum rounds to exactly 1.0", which an
+        # ulp of exp can move by a step: such rays are legitimately flagged
+        assert uns.mean() <= MAX_UNSURE, uns.mean()
+    ok = ~uns
+    for k, v in ref.items():
+        got = o[k][idx]
+        if k == "rgb":
+            assert np.array_equal(_bits(got[ok]), _bits(v[ok])), k
+            assert np.all(np.abs(got[uns] - v[uns]) <= 1e-6)
+        else:
+            assert np.array_equal(_bits(got[ok]), _bits(v[ok])), k
+            if k != "n_samples":
+                dt = (cfg.far - cfg.near) / cfg.samples_per_ray
+                assert np.all(np.abs(got[uns] - v[uns]) <= dt + 1e-6), k
+    return int(uns.sum())
+
+
+@pytest.mark.parametrize("case", golden_io.render_cases(), ids=lambda c: c[0])
+def test_render_matches_reference(case):
+    _name, sc, cam, cfg, ref = case
+    o = _render(sc, [cam], cfg)
+    _compare(o, ref, cfg)
+
+
+def test_render_batched_views_match_single():
+    """Several cameras in one launch == one launch each (sop rig)."""
+    cases = [c for c in golden_io.render_cases() if c[0].endswith("sop")]
+    sc, cfg = cases[0][1], cases[0][3]
+    o = _render(sc, [c[2] for c in cases], cfg)
+    for i, c in enumerate(cases):
+        _compare(o, c[4], cfg, idx=i)
+
+
+def test_march_rays_match_reference():
+    from paper_2601_04860_b200.render import march_rays_device
+    per, rays, ref = golden_io.march_cases()
+    for i, (sc, cfg) in enumerate(per):
+        out, err, uns = march_rays_device(sc, rays[i][None], cfg)
+        out, err, uns = out.cpu().numpy()[0], err.cpu().numpy()[0], int(uns.cpu()[0])
+        assert uns == 0, i
+        assert np.array_equal(out[[3, 4, 6, 7]], ref[i][[3, 4, 6, 7]]), i   # depths, n exact
+        assert np.all(np.abs(out[[0, 1, 2, 5]] - ref[i][[0, 1, 2, 5]]) <= err), i
+        assert np.all(err <= 1e-9)
+
+
+@pytest.mark.parametrize("case", golden_io.bake_cases(), ids=lambda c: c[0])
+def test_bake_matches_reference(case):
+    from paper_2601_04860_b200.geometry import VoxelGrid
+    from paper_2601_04860_b200.scene import bake_density_grid
+    _name, sc, g, half, origin, ref = case
+    dg = bake_density_grid(sc, VoxelGrid(g, half, origin))
+    assert np.array_equal(_bits(dg.values), _bits(ref))
+
+
+def test_render_matches_oracle_larger():
+    """sphere_on_plane at 320x240 from 6 Fibonacci-like cameras (the
+    reference's render config: 384 samples per ray) against the oracle."""
+    import workloads
+    sc = golden_io.render_scene("sop")
+    cams = workloads.cameras("fib", 6, 320, 240)
+    cfg = golden_io.GoldCfg(384, 0.4, 12.5, 0.75, 1e-4)
+    o = _render(sc, cams, cfg)
+    total = 0
+    for i, c in enumerate(cams):
+        ref = oracle.render(sc.arrays(), c, cfg)
+        total += _compare(o, ref, cfg, idx=i)
+    assert o["n_samples"].min() > 0            # the room stops every ray
+
+
+def test_bake_matches_oracle_power_of_two_and_odd():
+    sc = golden_io.render_scene("mixed")
+    from paper_2601_04860_b200.geometry import VoxelGrid
+    from paper_2601_04860_b200.scene import bake_density_device
+    for g in (64, 37):
+        grid = VoxelGrid(g, 1.3, np.array([-1.3, -1.3, -4.3]))
+        sc.bounds = golden_io.Bounds(np.array([-5.0] * 3), np.array([5.0] * 3), False)
+        v = bake_density_device(sc, grid).cpu().numpy()
+        ref = oracle.bake(sc.arrays(), g, 1.3, grid.origin, sc.bounds)
+        assert np.array_equal(_bits(v), _bits(ref))
+        assert (v > 0).any()
+
+
+# ---- pkg/tests/test_render.py, restated against the device marcher ----------
+
+def _ref_scenes():
+    from paper_2601_04860_b200.geometry import SceneBounds
+    from paper_2601_04860_b200.scene import SceneModel, ScenePrimitive
+    bounds = SceneBounds((-5, -5, -5), (5, 5, 5))
+
+    def wall(depth=2.0, sigma=500.0):
+        return SceneModel((ScenePrimitive("box", {"center": (0, 0, -depth - 0.5),
+                                                  "half_extents": (4.0, 4.0, 0.5)},
+                                          density=sigma, color=(0.2, 0.8, 0.2), object_id=1),),
+                          bounds)
+
+    def sphere(sigma=4.0):
+        return SceneModel((ScenePrimitive("sphere", {"center": (0, 0, -3.0), "radius": 0.8},
+                                          density=sigma, color=(0.9, 0.1, 0.1), object_id=1),),
+                          bounds)
+    return wall, sphere, bounds
+
+
+def _front(res=64, f=1.6):
+    from paper_2601_04860_b200.geometry import Camera
+    return Camera(fx=f * res, fy=f * res, cx=res / 2, cy=res / 2, width=res, height=res,
+                  world_from_camera=np.eye(4))
+
+
+def test_reference_march_ray_cases():
+    from paper_2601_04860_b200.render import RenderConfig, march_ray
+    wall, sphere, bounds = _ref_scenes()
+    cfg = RenderConfig(samples_per_ray=256, near=0.5, far=6.0, tau_cw=0.75)
+    dt = (cfg.far - cfg.near) / cfg.samples_per_ray
+
+    class Ray:
+        def __init__(self, o, d):
+            d = np.asarray(d, np.float64)
+            self.origin, self.direction = np.asarray(o, np.float64), d / np.linalg.norm(d)
+    rec = march_ray(sphere(), Ray((0, 0, 0), (0, 1, 0)), cfg)       # misses everything
+    assert rec.n_samples == 0 and not rec.valid
+    assert rec.d_min == rec.d_max == rec.d_exp == 0.0
+    rec = march_ray(wall(2.0), Ray((0, 0, 0), (0, 0, -1)), cfg)     # opaque wall collapses
+    assert rec.valid
+    for v in (rec.d_min, rec.d_max, rec.d_exp, rec.z_surface):
+        assert abs(v - 2.0) <= dt + 1e-9
+    rec = march_ray(sphere(1.5), Ray((0, 0, 0), (0, 0, -1)), cfg)   # depth ordering
+    assert rec.d_min <= rec.d_exp <= rec.d_max
+
+
+def test_reference_render_view_cases():
+    from paper_2601_04860_b200.render import RenderConfig, render_view
+    from paper_2601_04860_b200.scene import SceneModel
+    wall, sphere, bounds = _ref_scenes()
+    cfg = RenderConfig(samples_per_ray=256, near=0.5, far=6.0, tau_cw=0.75)
+    vg = render_view(SceneModel((), bounds), _front(), cfg)         # empty scene
+    assert not vg.valid.any() and np.allclose(vg.rgb, 0.0)
+    vg = render_view(sphere(50.0), _front(), cfg)                   # depth profile
+    c = vg.d_exp.shape[0] // 2
+    assert abs(vg.d_exp[c, c] - (3.0 - 0.8)) < 0.05
+    assert vg.d_exp[vg.valid].max() > vg.d_exp[c, c] + 0.3
+    render_view(sphere(2.0), _front(), cfg).check()                 # invariants
+    prev = None                                                     # monotone cutoff
+    for tau in (0.3, 0.6, 0.9):
+        v = render_view(sphere(1.5), _front(),
+                        RenderConfig(samples_per_ray=128, near=0.5, far=6.0, tau_cw=tau))
+        if prev is not None:
+            both = prev.valid & v.valid
+            assert np.all(v.d_max[both] >= prev.d_max[both] - 1e-6)
+        prev = v
+    a = render_view(sphere(), _front(), cfg)                        # deterministic
+    b = render_view(sphere(), _front(), cfg)
+    for k in ("rgb", "d_min", "d_max", "d_exp", "n_samples", "z_surface"):
+        assert np.array_equal(getattr(a, k), getattr(b, k))
+
+
+def test_render_feeds_fusion_on_device():
+    """Rendered planes stay in HBM and fuse exactly like the oracle on them
+    (masks: refine of a constant-confidence mask)."""
+    import torch
+    from paper_2601_04860_b200.fusion import FusionParams
+    from paper_2601_04860_b200.geometry import VoxelGrid
+    from paper_2601_04860_b200.render import ViewGeometry, render_views_device
+    from paper_2601_04860_b200.scene import bake_density_device
+    import workloads
+    sc = golden_io.render_scene("sop")
+    sc.bounds = golden_io.Bounds(np.array([-4.9, -4.4, -4.9]), np.array([4.9, 5.5, 4.9]), False)
+    cams = workloads.cameras("fib", 4, 96, 72)
+    cfg = golden_io.GoldCfg(384, 0.4, 12.5, 0.75, 1e-4)
+    o = render_views_device(sc, cams, cfg)
+    grid = VoxelGrid(48, 1.2, np.array([0.0, 0.55, 0.0]) - 1.2)
+    dens = bake_density_device(sc, grid)
+    host = {k: v.cpu().numpy() for k, v in o.items() if not k.startswith("_")}
+    views = []
+    for i, c in enumerate(cams):
+        vg = ViewGeometry(c, host["rgb"][i], host["d_min"][i], host["d_max"][i],
+                          host["d_exp"][i], host["n_samples"][i], host["z_surface"][i])
+        m = np.where(host["n_samples"][i] > 0, 0.9, 0.0).astype(np.float32)
+        views.append((vg, oracle.refine(m, vg.z_surface, vg.n_samples)))
+    params = FusionParams()
+    from paper_2601_04860_b200.fusion import fuse
+    from paper_2601_04860_b200.scene import DensityGrid
+    dg = DensityGrid(grid, dens.cpu().numpy())
+    ref = oracle.fuse(grid, dg, views, params)
+    got = fuse(grid, dg, views, params)
+    p_ref = ref["p"].reshape(grid.resolution, grid.resolution, grid.resolution)
+    assert np.array_equal(got.probs >= 0.5, p_ref >= 0.5)
+    assert np.allclose(got.probs, p_ref, rtol=1e-12, atol=1e-15)
+    assert torch.count_nonzero(dens) > 0
