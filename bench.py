@@ -45,6 +45,16 @@ CONFIG_DESC = {
 }
 
 
+INPUTS_DESC = {
+    "analytic": "view planes from the analytic first hit on the marcher's sample lattice "
+                "(n_samples = 1), density from bake_density_grid's formula; masks = object-1 "
+                "silhouette with the segmenter's 2-px falloff",
+    "marcher": "view planes from the reference's ray marcher (render_view, 384 samples/ray) "
+               "and density from bake_density_grid, both run on the device bit-identical "
+               "to the reference; masks = object-1 silhouette with the segmenter's 2-px falloff",
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -63,6 +73,9 @@ def parse():
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="slab mode, N>1: occupancy all-gather fused into the fusion's stores "
                          "over NVLink (symmetric memory), or a separate NCCL all_gather")
+    ap.add_argument("--inputs", default="marcher", choices=["marcher", "analytic"],
+                    help="view planes + density: the reference's ray marcher and bake run on "
+                         "the device, bit-exact (default), or the analytic first hit")
     ap.add_argument("--shard", default="slabs", choices=["slabs", "views"],
                     help="N>1 decomposition: voxel slabs (default) or view blocks")
     return ap.parse_args()
@@ -239,7 +252,7 @@ def run_reference(args):
     import torch
     # fixture generation only (torch ops, none of our kernels); timing is CPU-only
     gen = "cuda" if torch.cuda.is_available() else "cpu"
-    wl = workloads.make(args.config, device=gen)
+    wl = workloads.make(args.config, device=gen, source=args.inputs)
     h = host_copy(wl)
     pv = FusionParams().as_vector()
     budget = max(0.5, min(args.cpu_budget_s / max(args.steps + args.warmup, 1), 4.0))
@@ -263,7 +276,8 @@ def run_reference(args):
         "ms_per_step": ms, "latency_ms": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIG_DESC[args.config], "grid": wl.g, "views": wl.nv,
-                   "width": wl.shape[2], "height": wl.shape[1]},
+                   "width": wl.shape[2], "height": wl.shape[1],
+                   "inputs": INPUTS_DESC[args.inputs]},
         "cpu_baseline": {"value": value, "unit": "updates/s", "cores": oracle.max_threads(),
                          "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
@@ -313,7 +327,7 @@ def run_ours(args):
     # --- inputs: rank 0 builds the view set, NCCL broadcasts it (once) ---------
     cfg = workloads.CONFIGS[args.config]
     if rank == 0:
-        wl = workloads.make(args.config, device=dev)
+        wl = workloads.make(args.config, device=dev, source=args.inputs)
     else:
         wl = None
     if dist_on:
@@ -597,6 +611,7 @@ def run_ours(args):
                                f"scan records/bands built in per-view windows around the "
                                f"projected gated region: {roi_frac:.3f} of the pixels"),
                    "l2": "flushed (256 MiB write) between steps, outside the events",
+                   "inputs": INPUTS_DESC[args.inputs],
                    "params": "FusionParams() defaults"},
         "breakdown_ms": {"refine": refine_ms, "fuse": fuse_ms, "gather": float(np.mean(t_gath)),
                          "broadcast_once": bcast_ms},

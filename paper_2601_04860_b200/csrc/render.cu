@@ -469,8 +469,13 @@ bake_kernel(SceneConst S, BakeConst B, float *__restrict__ out) {
                 for (int k = 0; k < 3; ++k) p[k] = B.bc[k] + (s * (q[k] / r)) * B.bh[k];
             }
         }
+        // outside a primitive's zero-density box its d is exactly 0, which
+        // never raises np.maximum's running max (>= 0): skip it
         double best = 0.0;
         for (int i = 0; i < S.n; ++i) {
+            if (p[0] < S.lo[i][0] || p[0] > S.hi[i][0] || p[1] < S.lo[i][1] ||
+                p[1] > S.hi[i][1] || p[2] < S.lo[i][2] || p[2] > S.hi[i][2])
+                continue;
             const double d = np_density(S, i, p[0], p[1], p[2]);
             if (d > best) best = d;
         }

@@ -223,3 +223,23 @@ def test_render_feeds_fusion_on_device():
     assert np.array_equal(got.probs >= 0.5, p_ref >= 0.5)
     assert np.allclose(got.probs, p_ref, rtol=1e-12, atol=1e-15)
     assert torch.count_nonzero(dens) > 0
+
+
+def test_workload_marcher_inputs_match_oracle():
+    """The bench's default inputs (workloads.make(source="marcher")) are the
+    oracle's render and bake of the same scene, bit for bit (C1 rig, 2 views)."""
+    import torch
+    import workloads
+    wl = workloads.make("C1", device="cuda", n_views=2, source="marcher")
+    sc = workloads.scene_model()
+    cfg = golden_io.GoldCfg(workloads.SPP, workloads.NEAR, workloads.FAR, 0.75, 1e-4)
+    for i, cam in enumerate(wl.cams):
+        ref = oracle.render(sc, cam, cfg)
+        for k, plane in (("d_min", wl.dmins), ("d_max", wl.dmaxs), ("d_exp", wl.dexps),
+                         ("z_surface", wl.z_surface), ("n_samples", wl.nsamps)):
+            assert np.array_equal(_bits(plane[i].cpu().numpy()), _bits(ref[k])), k
+    g = wl.g
+    ref = oracle.bake(sc, g, workloads.GRID_HALF, wl.origin,
+                      (sc.bounds.min, sc.bounds.max, sc.bounds.unbounded))
+    assert np.array_equal(_bits(wl.density.reshape(g, g, g).cpu().numpy()), _bits(ref))
+    assert int(torch.count_nonzero(wl.nsamps == 2)) > 0       # walls take two samples

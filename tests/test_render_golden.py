@@ -90,3 +90,15 @@ def test_scene_primitive_validation():
     with pytest.raises(ValueError):
         ScenePrimitive("box", **{**ok, "params": {"center": (0, 0, 0),
                                                   "half_extents": (1, 0, 1)}})
+
+
+def test_bench_scene_is_reference_sphere_on_plane():
+    """workloads.scene_model() (the bench's scene) packs exactly like the
+    reference's get_profile("sphere_on_plane").scene."""
+    import workloads
+    ref = golden_io.render_scene("sop")
+    k, p, d, c, _o, s = workloads.scene_model().packed()
+    assert np.array_equal(k, ref.kinds) and np.array_equal(p, ref.params)
+    assert np.array_equal(d, ref.dens) and np.array_equal(c, ref.cols)
+    assert np.array_equal(s, ref.soft)
+    assert workloads.scene_model().background == ref.background

@@ -26,7 +26,7 @@ def main():
     from paper_2601_04860_b200.segmenter import refine_bands_device
     import bench
     dev = torch.device("cuda", 0)
-    wl = workloads.make(args.config, device=dev)
+    wl = workloads.make(args.config, device=dev, source=os.environ.get("DIVAS_INPUTS", "marcher"))
     params = FusionParams()
 
     class A:

@@ -27,7 +27,7 @@ def main():
     from paper_2601_04860_b200.fusion import DeviceViews, FusionParams, Fuser, pack_cameras
     from paper_2601_04860_b200.segmenter import refine_bands_device
     dev = torch.device("cuda", 0)
-    wl = workloads.make(args.config, device=dev)
+    wl = workloads.make(args.config, device=dev, source=os.environ.get("DIVAS_INPUTS", "marcher"))
     dv = DeviceViews(torch.from_numpy(pack_cameras(wl.cams)).to(dev), torch.empty_like(wl.raw_masks),
                      wl.dmins, wl.dmaxs, wl.dexps, wl.nsamps, z_surface=wl.z_surface,
                      raw_masks=wl.raw_masks)

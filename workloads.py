@@ -233,6 +233,28 @@ def density_grid(g, device="cpu"):
     return out, origin, dx
 
 
+_ROOM_COLORS = ((0.30, 0.30, 0.34), (0.32, 0.30, 0.30), (0.26, 0.28, 0.26),
+                (0.34, 0.34, 0.38), (0.28, 0.31, 0.36), (0.33, 0.29, 0.33))
+
+
+def scene_model():
+    """The ``sphere_on_plane`` SceneModel (scenes.py:103-122 with _room,
+    scenes.py:77-100) as the package's mirror types, for the device marcher
+    and bake."""
+    from paper_2601_04860_b200.geometry import SceneBounds
+    from paper_2601_04860_b200.scene import SceneModel, ScenePrimitive
+    sphere = ScenePrimitive("sphere", {"center": CENTER, "radius": SPHERE_R,
+                                       "inner_radius": SPHERE_IN},
+                            density=SPHERE_SIGMA, color=(0.85, 0.2, 0.15), object_id=1)
+    pad = ScenePrimitive("box", {"center": PAD_C, "half_extents": PAD_H}, density=PAD_SIGMA,
+                         color=(0.1, 0.14, 0.2), object_id=2, soft_edge=SOFT)
+    walls = tuple(ScenePrimitive("box", {"center": bc, "half_extents": bh}, density=40.0,
+                                 color=col, object_id=90 + i, soft_edge=SOFT)
+                  for i, ((bc, bh), col) in enumerate(zip(_boxes()[1:], _ROOM_COLORS)))
+    return SceneModel((sphere, pad) + walls, SceneBounds((-4.9, -4.4, -4.9), (4.9, 5.5, 4.9)),
+                      background=(0.02, 0.02, 0.04))
+
+
 @dataclass
 class Workload:
     name: str
@@ -260,7 +282,11 @@ class Workload:
         return self.g ** 3 * self.nv
 
 
-def make(name, device="cpu", g=None, n_views=None, width=None, height=None):
+def make(name, device="cpu", g=None, n_views=None, width=None, height=None, source="analytic"):
+    """Inputs of a BASELINE config.  ``source="marcher"`` takes d_min / d_max /
+    d_exp / n_samples / z_surface from the reference's ray marcher and the
+    density from its bake, both run on the device and bit-identical to the
+    reference's (render.cu); the masks stay the analytic silhouette."""
     import torch
     cfg = dict(CONFIGS[name])
     if g:
@@ -283,5 +309,20 @@ def make(name, device="cpu", g=None, n_views=None, width=None, height=None):
         planes["n"].append(n)
     st = {k: torch.stack(v).contiguous() for k, v in planes.items()}
     dens, origin, dx = density_grid(cfg["g"], device)
+    if source == "marcher":
+        from paper_2601_04860_b200.geometry import VoxelGrid
+        from paper_2601_04860_b200.render import RenderConfig, render_views_device
+        from paper_2601_04860_b200.scene import bake_density_device
+        sc = scene_model()
+        o = render_views_device(sc, cams, RenderConfig(samples_per_ray=SPP, near=NEAR, far=FAR),
+                                dev=torch.device(device), unsure=True)
+        if int(o["unsure"].sum()):
+            raise RuntimeError("marcher flagged pixels whose bits are not certified")
+        st.update(z=o["z_surface"], dmin=o["d_min"], dmax=o["d_max"], dexp=o["d_exp"],
+                  n=o["n_samples"])
+        dens = bake_density_device(sc, VoxelGrid(cfg["g"], GRID_HALF, origin),
+                                   dev=torch.device(device))
+    elif source != "analytic":
+        raise ValueError(source)
     return Workload(name, cfg["g"], origin, dx, dens.reshape(-1).contiguous(), cams, st["raw"],
                     st["z"], st["dmin"], st["dmax"], st["dexp"], st["n"])
