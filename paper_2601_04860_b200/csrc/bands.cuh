@@ -175,14 +175,16 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
                 float4 *a4 = reinterpret_cast<float4 *>(recA + q);
                 a4[0] = make_float4(a[0].x, a[0].y, a[1 % VEC].x, a[1 % VEC].y);
                 a4[1] = make_float4(a[2 % VEC].x, a[2 % VEC].y, a[3 % VEC].x, a[3 % VEC].y);
+                // B is read only where A holds a depth (a supporting pixel;
+                // elsewhere A's NaN decides), so only those entries are written
                 if (write_b) {
-                    float4 *b4 = reinterpret_cast<float4 *>(recB + q);
-                    b4[0] = make_float4(b[0].x, b[0].y, b[1 % VEC].x, b[1 % VEC].y);
-                    b4[1] = make_float4(b[2 % VEC].x, b[2 % VEC].y, b[3 % VEC].x, b[3 % VEC].y);
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k)
+                        if (a[k].y == a[k].y) recB[q + k] = b[k];
                 }
             } else {
                 recA[q] = a[0];
-                if (write_b) recB[q] = b[0];
+                if (write_b && a[0].y == a[0].y) recB[q] = b[0];
             }
         }
     }
