@@ -27,20 +27,25 @@ struct BandParams {
 
 // Per-pixel scan records, two 8-byte planes per view (16 B/px in all):
 //   A = {refined mask, d_exp, or NaN when the pixel cannot support a thin
-//        candidate (mask <= 0.5 or n == 0)}
-//   B = {tau_d(n) as f32 (or -1e30 when it cannot support), n_samples bits}
-// A view whose supporting pixels all share one tau (the renderer's n is
-// constant per view, e.g. n = 1 on the reference's scenes) is scanned from
-// plane A alone (8 bytes per pixel, half the L1 traffic), with that tau from
-// the view's tau-range entry; other views read B as well.
+//        candidate (mask <= 0.5 or n == 0)}; the mask's sign bit flags a
+//        supporting pixel whose tau differs from the view's base tau(n_min)
+//        (readers take |mask|: refined masks are >= 0)
+//   B = {tau_d(n) as f32 (or -1e30 when it cannot support), n_samples bits},
+//        written only at supporting pixels (elsewhere A's NaN decides)
+// A view whose supporting pixels all share one tau is scanned from plane A
+// alone (8 bytes per pixel) with that tau from the view's tau-range entry;
+// one where few supporting pixels differ from the base tau is also scanned
+// from A alone, with the base tau, and an item that meets a flagged pixel is
+// recounted exactly; other views read B as well.
 // View v's records start at v * 2 * hm * wm float2: A plane, then B plane.
 constexpr float kIneligible = -1e30f;
 
-// Bands: per view nty * ntx tile entries, then one entry holding the view's
-// {min, max} key (order-preserving u32, as the z keys) of tau32 over the
-// supporting pixels the pass saw.
+// Bands: per view nty * ntx tile entries, then two 16-byte entries: the
+// view's {min, max} key (order-preserving u32, as the z keys) of tau32 over
+// the supporting pixels the pass saw, the count of flagged and of supporting
+// pixels; then {base tau32 bits (NaN: none), 0, 0, 0}.
 __host__ __device__ inline int64_t band_view_stride(int nty, int ntx) {
-    return (int64_t)nty * ntx + 1;
+    return (int64_t)nty * ntx + 2;
 }
 
 __device__ __forceinline__ uint32_t tau_key(float t) {   // t >= 0: order-preserving
@@ -55,8 +60,10 @@ static __global__ void band_init(double2 *__restrict__ bands, int nv, int nty, i
                                                    (int64_t)nty * ntx);
         e[0] = 0xffffffffu;
         e[1] = 0u;
-        e[2] = 0u;                                   // unused half of the entry
-        e[3] = 0u;
+        e[2] = 0u;                                   // flagged supporting pixels
+        e[3] = 0u;                                   // supporting pixels
+        e[4] = 0x7fc00000u;                          // base tau: none yet
+        e[5] = e[6] = e[7] = 0u;
     }
 }
 
@@ -79,7 +86,7 @@ __device__ __forceinline__ float band_px(float m, int32_t n, float d, const Band
 // a tile row and combine with shuffles.  REFINE: also produce the refined mask
 // from the raw one (segmenter.py:141-152) and band on the refined values.
 #ifndef DIVAS_BAND_MINB
-#define DIVAS_BAND_MINB 6
+#define DIVAS_BAND_MINB 5
 #endif
 template <int VEC, bool REFINE>
 __global__ void __launch_bounds__(256, DIVAS_BAND_MINB)
@@ -98,12 +105,18 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
     // plane B is needed only when the view's supporting pixels can differ in
     // tau: with the n range known (refine keys), one tau(n) for all -> skip it
     bool write_b = true;
+    float base = __int_as_float(0x7fc00000);         // tau(n_min); NaN without keys
     if (minmax) {
         const uint32_t n0 = minmax[kKeys * v + 2], n1 = minmax[kKeys * v + 3];
         double l0 = 0.0, h0 = 0.0;
         write_b = n0 <= n1 && band_px(1.0f, (int32_t)n0, 0.0f, B, l0, h0) !=
                                   band_px(1.0f, (int32_t)n1, 0.0f, B, l0, h0);
+        if (n0 <= n1) base = band_px(1.0f, (int32_t)n0, 0.0f, B, l0, h0);
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+            reinterpret_cast<uint32_t *>(bands + (int64_t)v * band_view_stride(B.nty, B.ntx) +
+                                         (int64_t)B.nty * B.ntx)[4] = __float_as_uint(base);
     }
+    uint32_t cnt = 0;              // supporting pixels (low 16 bits), flagged ones (high)
     // ROI (optional): the view's tile-aligned window {x0, y0, x1, y1}; the
     // grid covers the largest window, blocks past this view's window idle
     int rx0 = 0, rx1 = B.wm - 1, ty = (int)blockIdx.y;
@@ -164,7 +177,11 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
             for (int k = 0; k < VEC; ++k) {
                 const float t32 = band_px(m[k], n[k], d[k], B, lo, hi);
                 const bool sup = t32 >= 0.0f;
-                a[k] = make_float2(m[k], sup ? d[k] : __int_as_float(0x7fc00000));
+                // every pixel flags when base is NaN (no refine keys): then the
+                // flag path is never chosen (nflag = nsup)
+                const bool flag = sup && !(t32 == base);
+                cnt += sup ? (flag ? 0x10001u : 1u) : 0u;
+                a[k] = make_float2(flag ? -m[k] : m[k], sup ? d[k] : __int_as_float(0x7fc00000));
                 b[k] = make_float2(t32, __int_as_float(n[k]));
                 if (sup) {
                     tmin = min(tmin, tau_key(t32));
@@ -198,15 +215,22 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
         const int tx = x0 / kBandTile;
         bv[(int64_t)ty * B.ntx + tx] = make_double2(lo, hi);
     }
-    // the view's tau range: warp-reduce, one atomic pair per warp
-    for (int o = 16; o > 0; o >>= 1) {
-        tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
-        tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-    }
-    if ((threadIdx.x & 31) == 0 && tmin <= tmax) {
-        uint32_t *e = reinterpret_cast<uint32_t *>(bv + (int64_t)B.nty * B.ntx);
-        atomicMin(e, tmin);
-        atomicMax(e + 1, tmax);
+    // the view's tau range and flag counts: warp-reduce, atomics per warp
+    // (warps without a supporting pixel -- most of them -- skip it all)
+    // (a warp sees at most 32 x 8 x VEC <= 1024 pixels: the halves do not carry)
+    if (__any_sync(0xffffffffu, cnt != 0)) {
+        for (int o = 16; o > 0; o >>= 1) {
+            tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+            tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            uint32_t *e = reinterpret_cast<uint32_t *>(bv + (int64_t)B.nty * B.ntx);
+            atomicMin(e, tmin);
+            atomicMax(e + 1, tmax);
+            atomicAdd(e + 2, cnt >> 16);
+            atomicAdd(e + 3, cnt & 0xffffu);
+        }
     }
 }
 

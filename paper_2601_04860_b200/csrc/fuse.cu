@@ -858,7 +858,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     const float2 ra = __ldg(recA + q);                         // {m, d_exp or NaN}
     const int32_t ns = __ldg(M.nsamps + pix);
     if (ns <= 0) return false;                                 // valids[view, py, px] == 0
-    const float m = ra.x;
+    const float m = fabsf(ra.x);                              // sign: the tau flag
     PSTAT(2, 1);
 #if defined(DIVAS_ABL) && DIVAS_ABL >= 3
     K.t[kidx] = (double)m;
@@ -972,6 +972,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     const uint32_t *te = reinterpret_cast<const uint32_t *>(
         M.bands + (int64_t)view * band_view_stride(C.nty, C.ntx) + (int64_t)C.nty * C.ntx);
     const uint32_t tk0 = __ldg(te), tk1 = __ldg(te + 1);
+    const uint32_t nflag = __ldg(te + 2), nsup = __ldg(te + 3);
     const double xd = q.x_d;
     const float xd32 = (float)xd;
     const float Mg = (float)(9.5367431640625e-07 * (fabs(xd) + C.tau_max));   // 2^-20
@@ -991,10 +992,25 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
         for (int i = 0; i < npix; ++i) {
             DIVAS_BOUND(pp, recA, plane);
             const float2 r = __ldg(pp);
-            mmax = fmaxf(mmax, r.x);
+            mmax = fmaxf(mmax, fabsf(r.x));
             const float e = fabsf(xd32 - r.y) - tau;
             sup += (e <= -Mg) ? 1 : 0;
             unsure |= fabsf(e) < Mg;
+            ++pp;
+            if (--left == 0) { left = bw; pp += skip; }
+        }
+    } else if ((uint64_t)nflag * 32u <= nsup) {
+        // few supporting pixels differ from the base tau: scan with the base
+        // tau, a flagged pixel (negative mask) sends the item to the recount
+        const float tau = __uint_as_float(__ldg(te + 4));
+#pragma unroll 4
+        for (int i = 0; i < npix; ++i) {
+            DIVAS_BOUND(pp, recA, plane);
+            const float2 r = __ldg(pp);
+            mmax = fmaxf(mmax, fabsf(r.x));
+            const float e = fabsf(xd32 - r.y) - tau;
+            sup += (e <= -Mg) ? 1 : 0;
+            unsure |= (fabsf(e) < Mg) | (r.x < 0.0f);
             ++pp;
             if (--left == 0) { left = bw; pp += skip; }
         }
@@ -1004,7 +1020,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
             DIVAS_BOUND(pp, recA, plane);
             const float2 r = __ldg(pp);
             const float t32 = __ldg(pp + plane).x;
-            mmax = fmaxf(mmax, r.x);
+            mmax = fmaxf(mmax, fabsf(r.x));
             const float e = fabsf(xd32 - r.y) - t32;
             sup += (e <= -Mg) ? 1 : 0;
             unsure |= fabsf(e) < Mg;
