@@ -1129,21 +1129,27 @@ __device__ __forceinline__ void reduce_store(const FuseConst &C, const FuseOut &
 }
 
 // One voxel, lists in local memory (any count up to MAXV views).
+#ifndef DIVAS_RGROUP
+#define DIVAS_RGROUP 8
+#endif
+constexpr int kRGroup = DIVAS_RGROUP;          // contribution loads in flight per thread
 template <int MAXV>
 __device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &K,
                                              const FuseOut &O, const uint32_t *work,
                                              long long slot) {
+    const uint32_t vi = work[slot];                          // issued early
     double tw[MAXV], tmw[MAXV], tt[MAXV];
     int n_thick = 0, n_thin = 0;
     // contributions are fetched in groups of 4 (all loads in flight before
     // the first insertion), then inserted in view order as before
     for (int wd = 0; wd < C.w32; ++wd) {
         uint32_t bt = K.bits_thick[(int64_t)wd * C.cap + slot];
+        uint32_t bn = K.bits_thin[(int64_t)wd * C.cap + slot];     // both words in flight
         while (bt) {
-            double kw[4], km[4];
+            double kw[kRGroup], km[kRGroup];
             int c = 0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kRGroup; ++u) {
                 if (bt) {
                     const int view = wd * 32 + __ffs(bt) - 1;
                     bt &= bt - 1;
@@ -1153,7 +1159,7 @@ __device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kRGroup; ++u) {
                 if (u < c) {
                     int j = n_thick - 1;   // stable insertion by (w, m*w): fusion.py:389-407
                     while (j >= 0 && (tw[j] > kw[u] || (tw[j] == kw[u] && tmw[j] > km[u]))) {
@@ -1167,12 +1173,11 @@ __device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &
                 }
             }
         }
-        uint32_t bn = K.bits_thin[(int64_t)wd * C.cap + slot];
         while (bn) {
-            double kt[4];
+            double kt[kRGroup];
             int c = 0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kRGroup; ++u) {
                 if (bn) {
                     const int view = wd * 32 + __ffs(bn) - 1;
                     bn &= bn - 1;
@@ -1181,7 +1186,7 @@ __device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kRGroup; ++u) {
                 if (u < c) {
                     int j = n_thin - 1;    // fusion.py:373-386
                     while (j >= 0 && tt[j] > kt[u]) { tt[j + 1] = tt[j]; --j; }
@@ -1194,7 +1199,7 @@ __device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &
     double sw = 0.0, smw = 0.0, st = 0.0;
     for (int i = 0; i < n_thick; ++i) { sw += tw[i]; smw += tmw[i]; }
     for (int i = 0; i < n_thin; ++i) st += tt[i];
-    reduce_store(C, O, work[slot], n_thick, n_thin, sw, smw, st);
+    reduce_store(C, O, vi, n_thick, n_thin, sw, smw, st);
 }
 
 // dirty != NULL (incremental update of views [view_lo, view_hi)): only slots
