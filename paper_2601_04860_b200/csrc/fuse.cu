@@ -249,10 +249,46 @@ gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
     int cnt = 0;
     int64_t base;
     const BrickOrigin Bo = brick_origin(G, blockIdx.x);
+    const int64_t g = C.g, gg = g * g;
+    // interior brick (the common case): inside the grid, inside [lo, hi),
+    // quads aligned -- one float4 per quad, no per-quad bounds logic; round r
+    // of thread t is quad t + 256 r, i.e. 4 ix planes further
+    if ((g & 3) == 0 && Bo.ix + kBrick <= g && Bo.iy + kBrick <= g && Bo.iz + kBrick <= g &&
+        C.lo <= Bo.ix * gg && C.hi >= (Bo.ix + kBrick) * gg) {
+        const int t = (int)threadIdx.x;
+        base = ((Bo.ix + (t >> 6)) * g + Bo.iy + ((t >> 2) & 15)) * g + Bo.iz + 4 * (t & 3);
+        const uint8_t occ0 = (0.0 >= C.occ_thr) ? 1 : 0;
+        const double2 z2 = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int r = 0; r < kGateRounds; ++r)
-        cnt += __popc(gate_brick_quad(dens, C, O, Bo, r * kGateThreads + (int)threadIdx.x, false,
-                                      base));
+        for (int r = 0; r < kGateRounds; ++r, base += (kGateThreads / 64) * gg) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(dens + base));
+            if (O.probs) {
+                __stcs(reinterpret_cast<double2 *>(O.probs + base), z2);
+                __stcs(reinterpret_cast<double2 *>(O.probs + base) + 1, z2);
+            }
+            if (O.n_thick || O.n_thin || O.sw || O.smw || O.st) {   // stats outputs (rare)
+                if (O.n_thick) *reinterpret_cast<int4 *>(O.n_thick + base) = make_int4(0, 0, 0, 0);
+                if (O.n_thin) *reinterpret_cast<int4 *>(O.n_thin + base) = make_int4(0, 0, 0, 0);
+                double *sums[3] = {O.sw, O.smw, O.st};
+                for (int q = 0; q < 3; ++q)
+                    if (sums[q]) {
+                        reinterpret_cast<double2 *>(sums[q] + base)[0] = z2;
+                        reinterpret_cast<double2 *>(sums[q] + base)[1] = z2;
+                    }
+            }
+            const uchar4 o4 = make_uchar4(occ0, occ0, occ0, occ0);
+            if (O.occ) *reinterpret_cast<uchar4 *>(O.occ + base) = o4;
+            for (int p = 0; p < O.n_peers; ++p)
+                *reinterpret_cast<uchar4 *>(O.occ_peers[p] + base) = o4;
+            cnt += (int)density_gate(v.x, C) + (int)density_gate(v.y, C) +
+                   (int)density_gate(v.z, C) + (int)density_gate(v.w, C);
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < kGateRounds; ++r)
+            cnt += __popc(gate_brick_quad(dens, C, O, Bo, r * kGateThreads + (int)threadIdx.x,
+                                          false, base));
+    }
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = cnt;
     __syncthreads();
