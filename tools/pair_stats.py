@@ -14,7 +14,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 NAMES = ["pairs", "in_frustum", "valid_px", "thick_try", "thick_depth_ok", "thick_vote",
          "thin_gated", "band_tiles", "scan_items", "scan_pixels", "unsure_recounts",
          "thin_votes", "thick_exact_fallback", "corner_exact_fallback", "centre_uncertain",
-         "band_too_wide"]
+         "band_too_wide", "items_mmax_below_accept", "pixels_mmax_below_accept",
+         "items_zero_support", "pixels_zero_support"]
 
 
 def main():
