@@ -337,6 +337,14 @@ int divas_bake_density(const divas_scene *scene, int64_t g, const double origin[
 /* ---------------------------------------------------------------------- */
 const char *divas_last_error(void);
 
+/* Per view, the bounding box {x0, y0, x1, y1} (DEVICE int32 [nv][4]; empty:
+ * x1 = -1) of the pixels of DEVICE masks [nv][hm][wm] with mask >= thr: the
+ * upload window of the depth maps in refine_and_fuse (they are read only at
+ * pixels whose refined mask -- at most the raw one -- clears the thick or thin
+ * mask threshold, and at the 4-neighbours of those). */
+int divas_mask_bbox(int32_t nv, int64_t hm, int64_t wm, const float *masks, float thr,
+                    int32_t *bbox, void *stream);
+
 /* Host -> device copy of a pitched sub-rectangle (cudaMemcpy2DAsync): the
  * windowed upload of view planes in refine_and_fuse. */
 int divas_copy2d_h2d(void *dst, size_t dpitch, const void *src, size_t spitch,

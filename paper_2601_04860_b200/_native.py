@@ -28,7 +28,7 @@ EXPORTS = (
     "divas_overlay", "divas_vgrid_payload",
     "divas_last_error", "divas_abi_version", "divas_refine_bands_roi", "divas_refine_minmax",
     "divas_refine_bands_keys", "divas_copy2d_h2d", "divas_peer_put",
-    "divas_render", "divas_march_rays", "divas_bake_density",
+    "divas_render", "divas_march_rays", "divas_bake_density", "divas_mask_bbox",
 )
 
 _VP = ctypes.c_void_p
@@ -93,6 +93,7 @@ def _declare(lib):
                                                   I32, I32, _VP]),
         "divas_refine_minmax": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP]),
         "divas_copy2d_h2d": (ctypes.c_int, [_VP, S, _VP, S, S, S, _VP]),
+        "divas_mask_bbox": (ctypes.c_int, [I32, I64, I64, _VP, ctypes.c_float, _VP, _VP]),
         "divas_peer_put": (ctypes.c_int, [_VP, S, _VP, I32, S, _VP]),
         "divas_refine_bands_keys": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP,
                                                    ctypes.POINTER(D), D, _VP, _VP, _VP, _VP, S,

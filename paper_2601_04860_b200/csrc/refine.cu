@@ -294,3 +294,67 @@ extern "C" size_t divas_records_size(int32_t nv, int64_t hm, int64_t wm) {
 extern "C" size_t divas_bands_size(int32_t nv, int64_t hm, int64_t wm) {
     return band_bytes(nv, (int)hm, (int)wm);
 }
+
+// ---------------------------------------------------------------------------
+// Bounding box of the pixels whose mask is >= thr, per view: the upload
+// window of d_min / d_max / d_exp in refine_and_fuse.  Those maps are read
+// by the fusion only at pixels whose refined mask reaches mask_thr (thick
+// centres) or exceeds 0.5 (thin support) -- refined <= raw, so raw >= thr
+// with thr <= both -- and at the 4-neighbours of thick centres (gradient).
+// ---------------------------------------------------------------------------
+namespace divas {
+
+__global__ void bbox_init(int32_t *bbox, int nv) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nv) {
+        bbox[4 * i] = 0x7fffffff;
+        bbox[4 * i + 1] = 0x7fffffff;
+        bbox[4 * i + 2] = -1;
+        bbox[4 * i + 3] = -1;
+    }
+}
+
+// grid (blocks_per_view, nv); one pixel per thread per iteration
+__global__ void __launch_bounds__(kRefineThreads)
+mask_bbox(const float *__restrict__ masks, int64_t hm, int64_t wm, float thr,
+          int32_t *__restrict__ bbox) {
+    const int v = blockIdx.y;
+    const int64_t plane = hm * wm;
+    const float *m = masks + (int64_t)v * plane;
+    int x0 = 0x7fffffff, y0 = 0x7fffffff, x1 = -1, y1 = -1;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < plane;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (__ldg(m + i) >= thr) {
+            const int y = (int)(i / wm), x = (int)(i - (int64_t)y * wm);
+            x0 = min(x0, x); x1 = max(x1, x);
+            y0 = min(y0, y); y1 = max(y1, y);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+        y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+        x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+        y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+    }
+    if ((threadIdx.x & 31) == 0 && x1 >= 0) {
+        atomicMin(bbox + 4 * v, x0);
+        atomicMin(bbox + 4 * v + 1, y0);
+        atomicMax(bbox + 4 * v + 2, x1);
+        atomicMax(bbox + 4 * v + 3, y1);
+    }
+}
+
+}  // namespace divas
+
+extern "C" int divas_mask_bbox(int32_t nv, int64_t hm, int64_t wm, const float *masks, float thr,
+                               int32_t *bbox, void *stream) {
+    if (nv <= 0 || hm <= 0 || wm <= 0 || !masks || !bbox) {
+        set_error("divas_mask_bbox: bad arguments");
+        return DIVAS_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    bbox_init<<<(nv + 255) / 256, 256, 0, s>>>(bbox, nv);
+    dim3 grid(blocks_per_view(hm * wm, nv), nv);
+    mask_bbox<<<grid, kRefineThreads, 0, s>>>(masks, hm, wm, thr, bbox);
+    return check_launch("divas_mask_bbox");
+}

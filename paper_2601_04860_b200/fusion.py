@@ -644,19 +644,38 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     # records there; the planar refinement does not need it)
     full_names = ("raw", "z", "nsamps") if windows else ("raw", "z", "dexps", "nsamps")
     win_names = ("dmins", "dmaxs", "dexps") if windows else ("dmins", "dmaxs")
+    # raw masks first: their per-view bounding box narrows the depth maps'
+    # upload windows while z / n_samples keep the link busy
     with torch.cuda.stream(up):
         for v0, v1 in bounds_k:
+            upload_full("raw", v0, v1)
+        raw_done = torch.cuda.Event()
+        raw_done.record(up)
+        for v0, v1 in bounds_k:
             for k in full_names:
-                upload_full(k, v0, v1)
+                if k != "raw":
+                    upload_full(k, v0, v1)
     # the windows need the gated voxels' bounding box: one wait for the density
     # upload, while the full planes above keep the link busy
     rois = None
+    lib = _native.lib()
     if windows:
         from .sharding import slab_view_rois
         rois = slab_view_rois(dens, fuser.pv, g, np.asarray(grid.origin, dtype=np.float64),
                               fuser.dx, pack_cameras(cams), sizes)
+        # d_min / d_max / d_exp are read only where the refined mask reaches
+        # mask_thr or exceeds 0.5 (refined <= raw) and at those pixels'
+        # 4-neighbours: intersect each window with the mask's box + 1 px
+        thr = np.float32(min(float(fuser.pv[10]), 0.5))
+        if float(thr) > min(float(fuser.pv[10]), 0.5):
+            thr = np.nextafter(thr, np.float32(-np.inf))
+        bbox = torch.empty((nv, 4), dtype=torch.int32, device=dev)
+        cur.wait_event(raw_done)
+        _native.check(lib.divas_mask_bbox(nv, hm, wm, planes["raw"].data_ptr(), float(thr),
+                                          bbox.data_ptr(), _native.stream_handle()),
+                      "divas_mask_bbox")
+        mbox = bbox.cpu().numpy()
     keep = []
-    lib = _native.lib()
     with torch.cuda.stream(up):
         for v0, v1 in bounds_k:
             for k in win_names:
@@ -667,6 +686,13 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
                     h, w = sizes[i]
                     x0, y0, x1, y1 = (int(c) for c in rois.host[i])
                     x1, y1 = min(x1, w - 1), min(y1, h - 1)
+                    bx0, by0, bx1, by1 = (int(c) for c in mbox[i])
+                    if bx1 < 0:
+                        continue                  # no pixel can need a depth value
+                    x0, y0 = max(x0, bx0 - 1), max(y0, by0 - 1)
+                    x1, y1 = min(x1, bx1 + 1), min(y1, by1 + 1)
+                    if x1 < x0 or y1 < y0:
+                        continue
                     a = np.ascontiguousarray(srcs[i][k], np.float32)
                     keep.append(a)
                     h2d[0] += 4 * (x1 - x0 + 1) * (y1 - y0 + 1)

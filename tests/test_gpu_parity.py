@@ -378,3 +378,30 @@ def test_many_views_against_oracle(dev, reps):
     rel = np.abs(got["probs"] - ref["p"]) / np.maximum(np.abs(ref["p"]), 1e-300)
     assert rel.max(initial=0.0) <= REL_TOL
     assert int(ref["n_thin"].max()) > 32 or int(ref["n_thick"].max()) > 0
+
+
+@pytest.mark.parametrize("name", ["sop", "mixed"])
+def test_refine_and_fuse_depth_windows_poisoned(dev, name):
+    """refine_and_fuse uploads d_min / d_max / d_exp only inside each view's
+    box of raw mask >= 0.5 (+1 px, intersected with the gated window): NaN
+    everywhere else in the host maps changes no bit of the result."""
+    from paper_2601_04860_b200 import ConfidenceMask, FusionParams, refine_and_fuse
+    case = golden_io.scene_cases()[name]
+    grid, dens, views, bounds = reference_objects(case)
+    params = FusionParams(*[float(x) for x in case.pv[:13]], enable_thin=bool(case.pv[13]))
+    raws = [(vg, ConfidenceMask(m.values.copy())) for vg, m in views]
+    clean, masks = refine_and_fuse(grid, dens, raws, params, bounds=bounds)
+    poisoned = []
+    for vg, m in raws:
+        ys, xs = np.nonzero(m.values >= 0.5)
+        keep = np.zeros(m.values.shape, bool)
+        if len(ys):
+            keep[max(ys.min() - 1, 0):ys.max() + 2, max(xs.min() - 1, 0):xs.max() + 2] = True
+        vg2 = type(vg)(vg.camera, vg.rgb, *[np.where(keep, a, np.float32(np.nan)).astype(np.float32)
+                                            for a in (vg.d_min, vg.d_max, vg.d_exp)],
+                       vg.n_samples, vg.z_surface)
+        poisoned.append((vg2, m))
+    og, masks2 = refine_and_fuse(grid, dens, poisoned, params, bounds=bounds)
+    assert np.array_equal(og.probs, clean.probs)
+    for a, b in zip(masks, masks2):
+        assert np.array_equal(a.values, b.values)
