@@ -45,6 +45,14 @@ def main():
            "occupied": int(out["occ"].sum()),
            "n_samples_hist": {int(k): int(v) for k, v in zip(*np.unique(n.cpu().numpy(),
                                                                           return_counts=True))}}
+    # views whose supporting pixels (refined mask > 0.5, n > 0) do not share one n
+    sup = (refined > 0.5) & (n > 0)
+    varied = 0
+    for v in range(n.shape[0]):
+        vals = torch.unique(n[v][sup[v]])
+        varied += int(vals.numel() > 1)
+    res["views_varied_tau"] = varied
+    res["supporting_px_n_gt1"] = int(((n > 1) & sup).sum())
     print(json.dumps(res))
 
 
