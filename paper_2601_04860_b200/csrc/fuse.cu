@@ -40,6 +40,7 @@
 #include <cstdio>
 
 #include "bands.cuh"
+#include "exp_cr.cuh"
 
 namespace divas {
 
@@ -546,7 +547,7 @@ __device__ __forceinline__ bool thick_spatial(const FuseConst &C, const Cam &k, 
     double hd = 0.5 * (double)span;                                   // f32 site
     if (hd < C.eps) hd = C.eps;
     const double r = fabs(t_c - mu) / hd;
-    wd = exp(-C.alpha1 * r * r);
+    wd = exp_ref(-C.alpha1 * r * r);
     return true;
 }
 
@@ -813,7 +814,7 @@ __device__ __forceinline__ double depth_weight(const FuseConst &C, double t_c, f
     double hd = 0.5 * (double)span;
     if (hd < C.eps) hd = C.eps;
     const double r = fabs(t_c - mu) / hd;
-    return exp(-C.alpha1 * r * r);
+    return exp_ref(-C.alpha1 * r * r);
 }
 
 // The exact t_proj of the reference's chain (fusion.py:268-277).
@@ -1381,7 +1382,7 @@ __global__ void pair_trace_kernel(divas_trace_args A, FuseConst C) {
                 const double r = fabs(t_c - mu) / hd;
                 R.delta = delta; R.g = g; R.tau_spatial = tau_sp; R.tau_depth = tau_dp;
                 R.t_proj = t_proj; R.t_clamped = t_c; R.mu_d = mu; R.h_d = hd; R.r = r;
-                R.w_depth = exp(-C.alpha1 * r * r);
+                R.w_depth = exp_ref(-C.alpha1 * r * r);
                 R.stage = ok ? DIVAS_STAGE_PASSED
                              : (delta > tau_sp ? DIVAS_STAGE_SPATIAL : DIVAS_STAGE_DEPTH);
             }

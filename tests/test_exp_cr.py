@@ -7,7 +7,8 @@ contraction) and checked on random and adversarial x in [-38, 0]:
   result not flagged ``ambiguous`` is the correctly rounded value, and an
   ambiguous one is the correctly rounded value or its flagged neighbour;
 * against the C library's exp (what the reference's numba math.exp calls):
-  equal whenever not ambiguous -- the premise of the marcher's certificate.
+  equal whenever not ambiguous -- the premise of the marcher's certificate
+  and of the fusion's bit-exact thick depth weights (x down to -700).
 """
 
 import ctypes
@@ -46,10 +47,11 @@ def lib(tmp_path_factory):
 def _xs():
     rng = np.random.default_rng(7)
     xs = list(-rng.uniform(0, 38, 4000))
+    xs += list(-rng.uniform(38, 700, 1500))                                 # thick weights
     xs += list(-np.exp(rng.uniform(np.log(1e-300), np.log(38.0), 2000)))    # tiny to large
     xs += [-1e-300, -5e-324, -2.0 ** -60, -2.0 ** -53, -2.0 ** -30, -1e-11, -0.5, -math.log(2),
            -1.4470486111111112, -0.0215, -38.0, -37.999999999999, -0.34657359027997264,
-           -0.3465735902799727]
+           -0.3465735902799727, -700.0, -699.999999, -4.0, -1.0, -0.25]
     # the marcher's own arguments: -sigma * dt for the reference scenes
     for sigma in (46.0, 40.0, 4.0, 50.0, 1.5, 500.0, 30.0, 12.0, 8.0, 1e-9):
         for dt in ((12.5 - 0.4) / 384, (6.0 - 0.5) / 256, (6.0 - 0.5) / 128, (7.0 - 0.3) / 200):
