@@ -402,6 +402,12 @@ def run_ours(args):
                                "symmetric-memory buffer over NVLink, device barrier")
             except Exception as e:  # noqa: BLE001
                 gather_mode = f"nccl all_gather (symmetric memory unavailable: {type(e).__name__})"
+            # every rank must take the same path (the device barrier is collective)
+            ok = torch.tensor([1 if peer is not None else 0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0 and peer is not None:
+                peer = None
+                gather_mode = "nccl all_gather (symmetric memory unavailable on a peer rank)"
 
     # slab mode, several ranks: each rank takes the z min/max pass of its block
     # of views and the keys are all-gathered (the band pass needs every view's)
@@ -416,6 +422,10 @@ def run_ours(args):
             try:              # the keys' all-gather as NVLink stores + a device barrier
                 mm_peer = sharding.PeerGather((mm_rows, 4), torch.int32, dev)
             except Exception:  # noqa: BLE001
+                mm_peer = None
+            ok = torch.tensor([1 if mm_peer is not None else 0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0:
                 mm_peer = None
     roi = None
     if args.windows == "on" and not views_mode:
