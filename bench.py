@@ -242,6 +242,24 @@ def parity_check(wl, details, probs, n_thick, n_thin, refined_gpu):
 # reference arm
 # ---------------------------------------------------------------------------
 
+def _marcher_inputs_cpu(wl):
+    """Replace the analytic view planes / density of ``wl`` (CPU tensors) by
+    the oracle's render_view / bake_density_grid of the same scene."""
+    import oracle
+    import torch
+    import workloads
+    sc = workloads.scene_model()
+    cfg = (workloads.SPP, workloads.NEAR, workloads.FAR, 0.75, 1e-4)
+    for i, cam in enumerate(wl.cams):
+        o = oracle.render(sc, cam, cfg)
+        for plane, key in ((wl.dmins, "d_min"), (wl.dmaxs, "d_max"), (wl.dexps, "d_exp"),
+                           (wl.z_surface, "z_surface"), (wl.nsamps, "n_samples")):
+            plane[i].copy_(torch.from_numpy(o[key]))
+    b = sc.bounds
+    dens = oracle.bake(sc, wl.g, workloads.GRID_HALF, wl.origin, (b.min, b.max, b.unbounded))
+    wl.density.copy_(torch.from_numpy(dens.reshape(-1)))
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -250,9 +268,16 @@ def run_reference(args):
     import workloads
     from paper_2601_04860_b200.fusion import FusionParams
     import torch
-    # fixture generation only (torch ops, none of our kernels); timing is CPU-only
-    gen = "cuda" if torch.cuda.is_available() else "cpu"
-    wl = workloads.make(args.config, device=gen, source=args.inputs)
+    # Fixture generation, outside the timed region (which is CPU-only): with a
+    # GPU the device marcher / bake make the inputs (bit-identical to the
+    # reference's render_view / bake_density_grid, tests/test_gpu_render.py);
+    # without one, the oracle's restatement of the same functions does.
+    if torch.cuda.is_available():
+        wl = workloads.make(args.config, device="cuda", source=args.inputs)
+    else:
+        wl = workloads.make(args.config, device="cpu", source="analytic")
+        if args.inputs == "marcher":
+            _marcher_inputs_cpu(wl)
     h = host_copy(wl)
     pv = FusionParams().as_vector()
     budget = max(0.5, min(args.cpu_budget_s / max(args.steps + args.warmup, 1), 4.0))
