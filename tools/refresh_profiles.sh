@@ -9,6 +9,8 @@ timeout 600 python bench.py --impl reference > $P/bench_reference_C3.json 2> $P/
 for c in C1 C2 C5; do
   timeout 900 python bench.py --config $c --steps 20 --warmup 3 > $P/bench_$c.json 2> $P/bench_$c.err; echo "bench $c rc=$?"
 done
+timeout 300 python tools/time_render.py --config C3 > $P/render_C3.json 2> $P/render_C3.err; echo "render C3 rc=$?"
+timeout 300 python tools/time_render.py --config C5 --reps 3 > $P/render_C5.json 2> $P/render_C5.err; echo "render C5 rc=$?"
 timeout 300 python tools/profile_step.py --steps 2 > $P/step.log 2>&1; rc=$?; echo "step rc=$rc"
 if [ $rc -eq 0 ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" --csv \
