@@ -301,7 +301,8 @@ gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
 }
 
 // pass 2 (one CTA): exclusive scan of the tile counts in place; the total is
-// the gated count, beyond `cap` the overflow flag
+// the gated count, beyond `cap` the overflow flag.  Each thread scans 4
+// consecutive counts per round (a 16^3-brick grid of 256^3 is one round).
 __global__ void __launch_bounds__(1024)
 gate_scan(uint32_t *__restrict__ tiles, int64_t ntiles, int64_t cap, WsHeader *__restrict__ hdr) {
     __shared__ unsigned long long s_w[32];
@@ -309,10 +310,15 @@ gate_scan(uint32_t *__restrict__ tiles, int64_t ntiles, int64_t cap, WsHeader *_
     if (threadIdx.x == 0) s_carry = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t b = 0; b < ntiles; b += blockDim.x) {
-        const int64_t i = b + threadIdx.x;
-        const unsigned long long v = i < ntiles ? tiles[i] : 0ull;
-        unsigned long long incl = v;
+    for (int64_t b = 0; b < ntiles; b += 4 * (int64_t)blockDim.x) {
+        const int64_t i0 = b + 4 * (int64_t)threadIdx.x;
+        unsigned long long v[4], t = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            v[k] = i0 + k < ntiles ? tiles[i0 + k] : 0ull;
+            t += v[k];
+        }
+        unsigned long long incl = t;
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
@@ -330,9 +336,14 @@ gate_scan(uint32_t *__restrict__ tiles, int64_t ntiles, int64_t cap, WsHeader *_
         }
         __syncthreads();
         const unsigned long long carry = s_carry;
-        if (i < ntiles) tiles[i] = (uint32_t)(carry + s_w[warp] + incl - v);
+        unsigned long long run = carry + s_w[warp] + incl - t;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (i0 + k < ntiles) tiles[i0 + k] = (uint32_t)run;
+            run += v[k];
+        }
         __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) s_carry = carry + s_w[warp] + incl;
+        if (threadIdx.x == blockDim.x - 1) s_carry = run;
         __syncthreads();
     }
     if (threadIdx.x == 0) {
