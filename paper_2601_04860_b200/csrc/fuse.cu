@@ -372,10 +372,23 @@ gate_emit(const float *__restrict__ dens, FuseConst C, BrickGrid G,
     int lp[kGateRounds];
     int64_t qbase[kGateRounds];
     const BrickOrigin Bo = brick_origin(G, blockIdx.x);
+    const int64_t g = C.g, gg = g * g;
+    // interior brick: the lean quad walk of gate_tiles
+    const bool interior = (g & 3) == 0 && Bo.ix + kBrick <= g && Bo.iy + kBrick <= g &&
+                          Bo.iz + kBrick <= g && C.lo <= Bo.ix * gg &&
+                          C.hi >= (Bo.ix + kBrick) * gg;
+    const int t = (int)threadIdx.x;
+    const int64_t base0 = ((Bo.ix + (t >> 6)) * g + Bo.iy + ((t >> 2) & 15)) * g + Bo.iz + 4 * (t & 3);
 #pragma unroll
     for (int r = 0; r < kGateRounds; ++r) {
-        bits[r] = gate_brick_quad(dens, C, none, Bo, r * kGateThreads + (int)threadIdx.x, true,
-                                  qbase[r]);
+        if (interior) {
+            qbase[r] = base0 + (int64_t)r * (kGateThreads / 64) * gg;
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(dens + qbase[r]));
+            bits[r] = (density_gate(v.x, C) ? 1u : 0u) | (density_gate(v.y, C) ? 2u : 0u) |
+                      (density_gate(v.z, C) ? 4u : 0u) | (density_gate(v.w, C) ? 8u : 0u);
+        } else {
+            bits[r] = gate_brick_quad(dens, C, none, Bo, r * kGateThreads + t, true, qbase[r]);
+        }
         const int c = __popc(bits[r]);
         int incl = c;
         for (int o = 1; o < 32; o <<= 1) {
