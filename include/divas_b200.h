@@ -73,11 +73,16 @@ int divas_refine(int32_t nv, int64_t hm, int64_t wm,
  *   out      [nv][hm][wm] f32 refined masks as divas_refine (may be NULL);
  *   records  per view two [hm][wm] float2 planes (divas_records_size bytes):
  *            A = {refined mask, d_exp or NaN where the pixel cannot support a
- *            thin candidate}, B = {tau_d(n) as f32 or -1e30, n_samples bits};
+ *            thin candidate}; the mask's sign bit flags a supporting pixel
+ *            whose tau_d differs from the view's base tau_d(n_min) (readers
+ *            take |mask|); B = {tau_d(n) as f32, n_samples bits}, written
+ *            only at supporting pixels;
  *   bands    per view [ceil(hm/8)][ceil(wm/8)] {lo, hi} f64 per 8x8 tile (the
  *            depth interval in which a thin candidate can find support) and
- *            one more 16-byte entry: the {min, max} order-preserving u32 key
- *            of tau_d over the view's supporting pixels (divas_bands_size).
+ *            two more 16-byte entries: {min, max} order-preserving u32 keys
+ *            of tau_d over the view's supporting pixels, the counts of
+ *            flagged and of supporting pixels; {base tau_d f32 bits, 0, 0,
+ *            0} (divas_bands_size).
  * pv = FusionParams.as_vector() and dx_vox (the tolerances depend on them).
  * Views are independent: view k's slices start at k * divas_records_size(1,..)
  * / k * divas_bands_size(1,..) bytes, so a single view can be (re)built in
