@@ -30,7 +30,7 @@ struct BandParams {
 //        candidate (mask <= 0.5 or n == 0)}; the mask's sign bit flags a
 //        supporting pixel whose tau differs from the view's base tau(n_min)
 //        (readers take |mask|: refined masks are >= 0)
-//   B = {tau_d(n) as f32 (or -1e30 when it cannot support), n_samples bits},
+//   B = {tau_d(n) as f32, n_samples bits},
 //        written only at supporting pixels (elsewhere A's NaN decides)
 // A view whose supporting pixels all share one tau is scanned from plane A
 // alone (8 bytes per pixel) with that tau from the view's tau-range entry;
