@@ -728,11 +728,32 @@ __device__ __forceinline__ bool thin_bounds(const FuseConst &C, const Cam &k, do
 __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &M, const Cam &k,
                                             int view, double x_d, double xcam, double ycam,
                                             double Uc, double Vc) {
+#ifndef DIVAS_BANDR
+#define DIVAS_BANDR 1
+#endif
+#if DIVAS_BANDR
+    // per-axis extent of the cube in camera coordinates: the corners are
+    // (xcam, ycam, x_d) + h (+-R0 +-R1 +-R2) along the camera axes, so
+    // |dx| <= h (|r0| + |r3| + |r6|), |dy| <= h (|r1| + |r4| + |r7|),
+    // |dz| <= h (|r2| + |r5| + |r8|); the projected offset of a corner from
+    // the centre is fx (dx x_d - xcam dz) / (x_d (x_d + dz)), bounded below
+    // with dz = -Dz.  A margin far above every rounding (0.01 px) keeps the
+    // footprint box inside [Uc - Ru, Uc + Ru].
+    const double h = 0.5 * C.dx;
+    const double Dx = h * (fabs(k.r[0]) + fabs(k.r[3]) + fabs(k.r[6]));
+    const double Dy = h * (fabs(k.r[1]) + fabs(k.r[4]) + fabs(k.r[7]));
+    const double Dz = h * (fabs(k.r[2]) + fabs(k.r[5]) + fabs(k.r[8]));
+    if (!(x_d > 2.0 * Dz)) return false;
+    const double inv = rcp_fast1(x_d * (x_d - Dz)) * (1.0 + 1e-9);
+    const double Ru = k.fx * (Dx * x_d + fabs(xcam) * Dz) * inv * (1.0 + 1e-9) + 0.01;
+    const double Rv = k.fy * (Dy * x_d + fabs(ycam) * Dz) * inv * (1.0 + 1e-9) + 0.01;
+#else
     const double rho = C.cube_r;
     if (!(x_d > 2.0 * rho)) return false;
     const double inv = rcp_fast1(x_d * (x_d - rho)) * (1.0 + 1e-9);
     const double Ru = k.fx * rho * (x_d + fabs(xcam)) * inv + 2.0;
     const double Rv = k.fy * rho * (x_d + fabs(ycam)) * inv + 2.0;
+#endif
     const double fx0 = floor((Uc - Ru) * (1.0 / kBandTile)), fx1 = floor((Uc + Ru) * (1.0 / kBandTile));
     const double fy0 = floor((Vc - Rv) * (1.0 / kBandTile)), fy1 = floor((Vc + Rv) * (1.0 / kBandTile));
     const int tx0 = (int)fmax(fx0, 0.0), tx1 = (int)fmin(fx1, (double)(C.ntx - 1));
