@@ -15,7 +15,12 @@
 
 namespace divas {
 
-constexpr int kBandTile = 8;
+#ifndef DIVAS_BAND_TILE
+#define DIVAS_BAND_TILE 8
+#endif
+constexpr int kBandTile = DIVAS_BAND_TILE;        // 8 or 4
+// band test: boxes touching more tiles than this are not tested (scanned)
+constexpr int kBandMaxTiles = kBandTile == 8 ? 16 : 36;
 // per-view refine keys: z min, z max (order-preserving f32 keys), n min, n max
 // over the valid pixels (n > 0)
 constexpr int kKeys = 4;

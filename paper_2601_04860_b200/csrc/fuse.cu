@@ -759,7 +759,7 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     const int tx0 = (int)fmax(fx0, 0.0), tx1 = (int)fmin(fx1, (double)(C.ntx - 1));
     const int ty0 = (int)fmax(fy0, 0.0), ty1 = (int)fmin(fy1, (double)(C.nty - 1));
     if (tx1 < tx0 || ty1 < ty0) return false;
-    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > 16) { PSTAT(15, 1); return false; }
+    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > kBandMaxTiles) { PSTAT(15, 1); return false; }
     const double2 *bv = M.bands + (int64_t)view * band_view_stride(C.nty, C.ntx);
     // tiles in row-major order, four loads in flight per round trip (indices
     // past the last tile repeat it: always in range, never changes the answer)
