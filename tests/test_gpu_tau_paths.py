@@ -21,10 +21,13 @@ pytestmark = pytest.mark.gpu
 
 
 def _entries(bands, nv, hm, wm):
-    nty, ntx = (hm + 7) // 8, (wm + 7) // 8
-    stride = nty * ntx + 2
+    """Each view's two trailing 16-byte entries (tau keys, counts, base tau):
+    the per-view band block is divas_bands_size(1, hm, wm) bytes, tiles first."""
+    from paper_2601_04860_b200 import _native
+    stride = int(_native.lib().divas_bands_size(1, hm, wm)) // 16
+    ntiles = stride - 2
     b = bands.view(np.uint32).reshape(nv, stride * 4)
-    return b[:, nty * ntx * 4: nty * ntx * 4 + 8]
+    return b[:, ntiles * 4: ntiles * 4 + 8]
 
 
 @pytest.mark.parametrize("mode", ["const", "flagged", "planeB"])
