@@ -504,8 +504,7 @@ def run_ours(args):
         occ_full = None
         if dist_on and not views_mode:
             if peer is not None:
-                peer.barrier()
-                occ_full = peer.buf
+                occ_full = peer.barrier()
             else:
                 occ_full = sharding.gather_occupancy(out["occ"][lo:hi], slabs, g, rank)
         if ev is not None:

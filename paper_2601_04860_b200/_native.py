@@ -21,7 +21,8 @@ NPARAM = 14
 EXPORTS = (
     "divas_refine_workspace_size", "divas_refine", "divas_records_size", "divas_bands_size",
     "divas_refine_bands",
-    "divas_fuse_workspace_size", "divas_fuse", "divas_gate_count", "divas_fuse_gated_count",
+    "divas_fuse_workspace_size", "divas_fuse_workspace_size_ext", "divas_fuse", "divas_gate_count",
+    "divas_fuse_gated_count",
     "divas_fuse_overflow", "divas_fuse_ws_regions",
     "divas_gradient_maps", "divas_pair_trace",
     "divas_threshold_workspace_size", "divas_threshold",
@@ -99,11 +100,12 @@ def _declare(lib):
                                                    ctypes.POINTER(D), D, _VP, _VP, _VP, _VP, S,
                                                    _VP, I32, I32, _VP]),
         "divas_fuse_workspace_size": (S, [I64, I32, I32, I32]),
+        "divas_fuse_workspace_size_ext": (S, [I64, I32, I32, I32, I32]),
         "divas_fuse": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, S, _VP]),
         "divas_gate_count": (ctypes.c_int, [ctypes.POINTER(FuseArgs), _VP, _VP]),
         "divas_fuse_gated_count": (_VP, [_VP]),
         "divas_fuse_overflow": (_VP, [_VP]),
-        "divas_fuse_ws_regions": (None, [I64, I32, I32, I32, ctypes.POINTER(S)]),
+        "divas_fuse_ws_regions": (None, [I64, I32, I32, I32, I32, ctypes.POINTER(S)]),
         "divas_gradient_maps": (ctypes.c_int, [I32, I32, I32, _VP, _VP, _VP, _VP, D, D, I32, _VP,
                                                _VP]),
         "divas_pair_trace": (ctypes.c_int, [_VP, _VP]),
@@ -124,7 +126,11 @@ def _declare(lib):
         "divas_abi_version": (ctypes.c_int, []),
     }
     for name, (res, args) in sig.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None and os.environ.get("DIVAS_LIB"):
+            continue      # experiment builds of older revisions (tools/ab.sh)
+        if fn is None:
+            raise RuntimeError(f"{LIB_PATH} does not export {name}: rebuild the library")
         fn.restype = res
         fn.argtypes = args
 
@@ -144,10 +150,12 @@ def lib():
     return _lib
 
 
-def ws_regions(cap, nv_cap, hm, wm):
-    """Byte offsets {work, bits_thick, bits_thin, w, mw, t, total} of a fuse workspace."""
+def ws_regions(cap, nv_cap, hm, wm, internal_aux=False):
+    """Byte offsets {work, bits_thick, bits_thin, w, mw, t, total} of a fuse
+    workspace (``internal_aux``: room for records / bands built by divas_fuse)."""
     out = (ctypes.c_size_t * 7)()
-    lib().divas_fuse_ws_regions(int(cap), int(nv_cap), int(hm), int(wm), out)
+    lib().divas_fuse_ws_regions(int(cap), int(nv_cap), int(hm), int(wm), int(bool(internal_aux)),
+                                out)
     return dict(zip(("work", "bits_thick", "bits_thin", "w", "mw", "t", "total"), list(out)))
 
 

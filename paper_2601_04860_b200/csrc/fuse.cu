@@ -578,10 +578,20 @@ __device__ __forceinline__ bool thick_spatial(const FuseConst &C, const Cam &k, 
 // ---------------------------------------------------------------------------
 // certified fast projection
 // ---------------------------------------------------------------------------
-// Reciprocal accurate to ~1 ulp: f32 seed + two Newton steps in f64.  Only
-// used inside certified approximations (never for an output bit).
+// f32 reciprocal seed on the MUFU (rcp.approx: relative error < 2^-22 after
+// the f64 -> f32 rounding of the argument); subnormal / overflowing arguments
+// give inf / 0, which the callers' range guards keep out of every decision.
+__device__ __forceinline__ double rcp_seed(double d) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)d));
+    return (double)r;
+}
+
+// Reciprocal accurate to ~1 ulp: seed + two Newton steps in f64.  Only used
+// inside certified approximations (never for an output bit); callers pass
+// 1e-30 < d < 1e30.
 __device__ __forceinline__ double rcp_fast(double d) {
-    double r = (double)__frcp_rn((float)d);
+    double r = rcp_seed(d);
     double e = fma(-d, r, 1.0);
     r = fma(r, e, r);
     e = fma(-d, r, 1.0);
@@ -643,12 +653,16 @@ __device__ __forceinline__ double tau_thin(const FuseConst &C, int32_t n) {
     return (2.0 * C.gamma + b) * C.dx;
 }
 
-// Reciprocal for certified bounds: f32 seed + one Newton step (rel. error
-// ~2^-46, far inside kCertRel).
+// Reciprocal for certified bounds: seed + one Newton step (rel. error
+// < 2^-43, far inside kCertRel); 1e-30 < d < 1e30.
 __device__ __forceinline__ double rcp_fast1(double d) {
-    const double r = (double)__frcp_rn((float)d);
+    const double r = rcp_seed(d);
     return fma(r, fma(-d, r, 1.0), r);
 }
+
+// branch-free min / max of finite doubles (fmin / fmax carry NaN handling)
+__device__ __forceinline__ double dmin2(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double dmax2(double a, double b) { return b > a ? b : a; }
 
 // _thin_pair (fusion.py:306-370): footprint bounds from the 8 projected
 // corners.  floor(fl(umin * w)) = min_j floor(fl(u_j * w)) (floor and
@@ -669,25 +683,33 @@ __device__ __forceinline__ bool thin_bounds(const FuseConst &C, const Cam &k, do
     const double eabs = 4e-15 * S;
     const double rho = C.cube_r;
     const double dmn = d_c - rho;                  // every corner is at least this deep
-    if (dmn > 2.0 * eabs && d_c < 1e30) {
-        const double ax = half * R[0], bx = half * R[3], cx_ = half * R[6];
-        const double ay = half * R[1], by = half * R[4], cy_ = half * R[7];
+    if (dmn > 2.0 * eabs && dmn > 1e-30 && d_c < 1e30) {
+        // corner j = (sx, sy, sz) of half * (+-R col) offsets; corners j and
+        // 7 - j are opposite (negated offsets), so four offset triples give
+        // all eight: with p = a + b, m = a - b the sz = -1 corners are
+        // -p - c, m - c, -m - c, p - c
         const double az = half * R[2], bz = half * R[5], cz_ = half * R[8];
+        const double fax = k.fx * (half * R[0]), fbx = k.fx * (half * R[3]), fcx = k.fx * (half * R[6]);
+        const double fay = k.fy * (half * R[1]), fby = k.fy * (half * R[4]), fcy = k.fy * (half * R[7]);
+        const double pz = az + bz, mz = az - bz, pu = fax + fbx, mu = fax - fbx;
+        const double pv = fay + fby, mv = fay - fby;
+        const double Z[4] = {-pz - cz_, mz - cz_, -mz - cz_, pz - cz_};
+        const double Uo[4] = {-pu - fcx, mu - fcx, -mu - fcx, pu - fcx};
+        const double Vo[4] = {-pv - fcy, mv - fcy, -mv - fcy, pv - fcy};
         const double FX = k.fx * x_c, FY = k.fy * y_c;
-        const double fax = k.fx * ax, fbx = k.fx * bx, fcx = k.fx * cx_;
-        const double fay = k.fy * ay, fby = k.fy * by, fcy = k.fy * cy_;
-        double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300;
+        double umin = 0.0, umax = 0.0, vmin = 0.0, vmax = 0.0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const double sx = (j & 1) ? 1.0 : -1.0;
-            const double sy = (j & 2) ? 1.0 : -1.0;
-            const double sz = (j & 4) ? 1.0 : -1.0;
-            const double dj = d_c - (sx * az + sy * bz + sz * cz_);
-            const double r = rcp_fast1(dj);
-            const double U = (FX + (sx * fax + sy * fbx + sz * fcx)) * r;
-            const double V = (FY + (sx * fay + sy * fby + sz * fcy)) * r;
-            umin = fmin(umin, U); umax = fmax(umax, U);
-            vmin = fmin(vmin, V); vmax = fmax(vmax, V);
+        for (int j = 0; j < 4; ++j) {
+            const double r1 = rcp_fast1(d_c - Z[j]), r2 = rcp_fast1(d_c + Z[j]);
+            const double U1 = (FX + Uo[j]) * r1, U2 = (FX - Uo[j]) * r2;
+            const double V1 = (FY + Vo[j]) * r1, V2 = (FY - Vo[j]) * r2;
+            const bool uu = U1 < U2, vv = V1 < V2;
+            const double ulo = uu ? U1 : U2, uhi = uu ? U2 : U1;
+            const double vlo = vv ? V1 : V2, vhi = vv ? V2 : V1;
+            umin = j ? dmin2(umin, ulo) : ulo;
+            umax = j ? dmax2(umax, uhi) : uhi;
+            vmin = j ? dmin2(vmin, vlo) : vlo;
+            vmax = j ? dmax2(vmax, vhi) : vhi;
         }
         const double idm = rcp_fast1(dmn) * (1.0 + 1e-9);
         const double mx = fabs(x_c) + rho, my = fabs(y_c) + rho;
@@ -743,14 +765,16 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     const double Dx = h * (fabs(k.r[0]) + fabs(k.r[3]) + fabs(k.r[6]));
     const double Dy = h * (fabs(k.r[1]) + fabs(k.r[4]) + fabs(k.r[7]));
     const double Dz = h * (fabs(k.r[2]) + fabs(k.r[5]) + fabs(k.r[8]));
-    if (!(x_d > 2.0 * Dz)) return false;
-    const double inv = rcp_fast1(x_d * (x_d - Dz)) * (1.0 + 1e-9);
+    const double den = x_d * (x_d - Dz);
+    if (!(x_d > 2.0 * Dz && den > 1e-30 && den < 1e30)) return false;
+    const double inv = rcp_fast1(den) * (1.0 + 1e-9);
     const double Ru = k.fx * (Dx * x_d + fabs(xcam) * Dz) * inv * (1.0 + 1e-9) + 0.01;
     const double Rv = k.fy * (Dy * x_d + fabs(ycam) * Dz) * inv * (1.0 + 1e-9) + 0.01;
 #else
     const double rho = C.cube_r;
-    if (!(x_d > 2.0 * rho)) return false;
-    const double inv = rcp_fast1(x_d * (x_d - rho)) * (1.0 + 1e-9);
+    const double den = x_d * (x_d - rho);
+    if (!(x_d > 2.0 * rho && den > 1e-30 && den < 1e30)) return false;
+    const double inv = rcp_fast1(den) * (1.0 + 1e-9);
     const double Ru = k.fx * rho * (x_d + fabs(xcam)) * inv + 2.0;
     const double Rv = k.fy * rho * (x_d + fabs(ycam)) * inv + 2.0;
 #endif
@@ -915,16 +939,22 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     const double ycam = k.r[1] * relx + k.r[4] * rely + k.r[7] * relz;
 
     // frustum + pixel: certified from one reciprocal, exact chain otherwise
-    const double r = rcp_fast(x_d);
-    const double A = k.fx * xcam * r;
-    const double B = k.fy * ycam * r;
+    double A, B;
     long long px, py;
-    const int cu = cert_axis(A + k.cx, kCertRel * (fabs(A) + fabs(k.cx) + 1.0), k.w, px);
-    const int cv = cert_axis(k.cy - B, kCertRel * (fabs(B) + fabs(k.cy) + 1.0), k.h, py);
-    if (cu == 0 || cv == 0) return false;
+    int cu = 2, cv = 2;
+    if (x_d > 1e-30 && x_d < 1e30) {
+        const double r = rcp_fast(x_d);
+        A = k.fx * xcam * r;
+        B = k.fy * ycam * r;
+        cu = cert_axis(A + k.cx, kCertRel * (fabs(A) + fabs(k.cx) + 1.0), k.w, px);
+        cv = cert_axis(k.cy - B, kCertRel * (fabs(B) + fabs(k.cy) + 1.0), k.h, py);
+        if (cu == 0 || cv == 0) return false;
+    }
     if (cu == 2 || cv == 2) {
-        const double u = (k.fx * (xcam / x_d) + k.cx) / k.w;
-        const double v = (k.cy - k.fy * (ycam / x_d)) / k.h;
+        A = k.fx * (xcam / x_d);
+        B = k.fy * (ycam / x_d);
+        const double u = (A + k.cx) / k.w;
+        const double v = (k.cy - B) / k.h;
         if (u < 0.0 || u >= 1.0 || v < 0.0 || v >= 1.0) return false;
         px = pixel_index(u, (long long)k.w);
         py = pixel_index(v, (long long)k.h);
@@ -1019,6 +1049,57 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     return true;
 }
 
+// Footprint scan of one box, row by row (groups of four records at constant
+// offsets, then a pair and a single for the row's remainder).  Per record
+// {m, D}: m_max in f32 (widening is exact and monotone: fmaxf equals the
+// reference's f64 `if mv > m_max`; NaN never wins), e = |f32(x_d) - D| - tau
+// decides support when |e| >= Mg (see thin_item), and the smallest |e| tells
+// whether any record fell inside the margin.  MODE 0: one tau per view
+// (plane A alone); 1: the base tau, a flagged record (negative m) also makes
+// the item unsure; 2: per-record tau from plane B.  Returns "unsure".
+template <int MODE>
+__device__ __forceinline__ bool scan_box(const float2 *__restrict__ rp, int wm, int64_t plane,
+                                         int bw, int bh, float xd32, float tau, float Mg,
+                                         int &sup, float &mmax) {
+    float emin = __int_as_float(0x7f800000);   // +inf
+    float fmin_ = 0.0f;                         // most negative m (MODE 1 flags)
+    auto pix = [&](float2 r, float t) {
+        mmax = fmaxf(mmax, fabsf(r.x));
+        const float e = fabsf(xd32 - r.y) - (MODE == 2 ? t : tau);
+        sup += (e <= -Mg) ? 1 : 0;
+        emin = fminf(emin, fabsf(e));
+        if (MODE == 1) fmin_ = fminf(fmin_, r.x);
+    };
+    const int rem = bw & 3;
+    const int full = bw - rem;
+    for (int y = 0; y < bh; ++y, rp += wm) {
+        int c = 0;
+        for (; c < full; c += 4) {
+            const float2 *q = rp + c;
+            float2 r[4];
+            float t[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                r[j] = __ldg(q + j);
+                t[j] = MODE == 2 ? __ldg(q + j + plane).x : 0.0f;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pix(r[j], t[j]);
+        }
+        const float2 *q = rp + c;
+        if (rem & 2) {
+            const float2 r0 = __ldg(q), r1 = __ldg(q + 1);
+            const float t0 = MODE == 2 ? __ldg(q + plane).x : 0.0f;
+            const float t1 = MODE == 2 ? __ldg(q + 1 + plane).x : 0.0f;
+            pix(r0, t0);
+            pix(r1, t1);
+            q += 2;
+        }
+        if (rem & 1) pix(__ldg(q), MODE == 2 ? __ldg(q + plane).x : 0.0f);
+    }
+    return emin < Mg || (MODE == 1 && fmin_ < 0.0f);
+}
+
 // Corner projections + footprint scan of one queued thin candidate.
 __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, const FuseMaps &M,
                                           const Contrib &K, int view,
@@ -1061,68 +1142,30 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     const int bw = (int)(xe - xs) + 1;
     const int npix = bw * ((int)(ye - ys) + 1);
     PSTAT(9, npix);
+    const int bh = (int)(ye - ys) + 1;
     int sup = 0;
     float mmax = 0.0f;
-    bool unsure = false;
-    // a running record pointer: +1 per pixel, + (wm - bw) at the end of a row
-    const int64_t skip = (int64_t)C.wm - bw;
-    const float2 *__restrict__ pp = rp;
-    int left = bw;
+    bool unsure;
     if (tk0 >= tk1) {   // one tau for every supporting pixel of the view (or none)
-        const float tau = __uint_as_float(tk0);
-#pragma unroll 4
-        for (int i = 0; i < npix; ++i) {
-            DIVAS_BOUND(pp, recA, plane);
-            const float2 r = __ldg(pp);
-            mmax = fmaxf(mmax, fabsf(r.x));
-            const float e = fabsf(xd32 - r.y) - tau;
-            sup += (e <= -Mg) ? 1 : 0;
-            unsure |= fabsf(e) < Mg;
-            ++pp;
-            if (--left == 0) { left = bw; pp += skip; }
-        }
+        unsure = scan_box<0>(rp, C.wm, plane, bw, bh, xd32, __uint_as_float(tk0), Mg, sup, mmax);
     } else if ((uint64_t)nflag * 32u <= nsup) {
         // few supporting pixels differ from the base tau: scan with the base
         // tau, a flagged pixel (negative mask) sends the item to the recount
-        const float tau = __uint_as_float(__ldg(te + 4));
-#pragma unroll 4
-        for (int i = 0; i < npix; ++i) {
-            DIVAS_BOUND(pp, recA, plane);
-            const float2 r = __ldg(pp);
-            mmax = fmaxf(mmax, fabsf(r.x));
-            const float e = fabsf(xd32 - r.y) - tau;
-            sup += (e <= -Mg) ? 1 : 0;
-            unsure |= (fabsf(e) < Mg) | (r.x < 0.0f);
-            ++pp;
-            if (--left == 0) { left = bw; pp += skip; }
-        }
+        unsure = scan_box<1>(rp, C.wm, plane, bw, bh, xd32, __uint_as_float(__ldg(te + 4)), Mg,
+                             sup, mmax);
     } else {
-#pragma unroll 4
-        for (int i = 0; i < npix; ++i) {
-            DIVAS_BOUND(pp, recA, plane);
-            const float2 r = __ldg(pp);
-            const float t32 = __ldg(pp + plane).x;
-            mmax = fmaxf(mmax, fabsf(r.x));
-            const float e = fabsf(xd32 - r.y) - t32;
-            sup += (e <= -Mg) ? 1 : 0;
-            unsure |= fabsf(e) < Mg;
-            ++pp;
-            if (--left == 0) { left = bw; pp += skip; }
-        }
+        unsure = scan_box<2>(rp, C.wm, plane, bw, bh, xd32, 0.0f, Mg, sup, mmax);
     }
     if (unsure) PSTAT(10, 1);
     if (unsure) {   // some pixel within the margin: recount with the reference's f64 test
         sup = 0;
-        pp = rp;
         const int32_t *np = M.nsamps + (int64_t)view * plane + ys * (int64_t)C.wm + xs;
-        left = bw;
-        for (int i = 0; i < npix; ++i) {
-            const float2 r = __ldg(pp);
-            sup += (r.y == r.y && fabs(xd - (double)r.y) <= tau_thin(C, __ldg(np))) ? 1 : 0;
-            ++pp;
-            ++np;
-            if (--left == 0) { left = bw; pp += skip; np += skip; }
-        }
+        const float2 *__restrict__ pp = rp;
+        for (int y = 0; y < bh; ++y, pp += C.wm, np += C.wm)
+            for (int c = 0; c < bw; ++c) {
+                const float2 r = __ldg(pp + c);
+                sup += (r.y == r.y && fabs(xd - (double)r.y) <= tau_thin(C, __ldg(np + c))) ? 1 : 0;
+            }
     }
     const double m_max = (double)mmax;
     const double p_cov = sup == 0 ? 0.0 : (double)sup / (double)npix;
@@ -1519,7 +1562,10 @@ struct WsLayout {
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static WsLayout ws_layout(int64_t cap, int32_t nv_cap, int32_t hm, int32_t wm) {
+// internal_aux: reserve the scan-record / band regions that divas_fuse builds
+// when the caller supplies no records (args->records == NULL); callers that
+// pass divas_refine_bands output need neither (C3: ~390 MB less).
+static WsLayout ws_layout(int64_t cap, int32_t nv_cap, int32_t hm, int32_t wm, bool internal_aux) {
     const size_t c = (size_t)(cap > 0 ? cap : 1);
     const size_t w32 = (size_t)((nv_cap + 31) / 32);
     WsLayout L;
@@ -1532,8 +1578,8 @@ static WsLayout ws_layout(int64_t cap, int32_t nv_cap, int32_t hm, int32_t wm) {
     L.t = off;          off = align256(off + (size_t)nv_cap * c * 8);
     L.dirty = off;      off = align256(off + c);
     L.gtiles = off;     off = align256(off + (size_t)kGateTileMax * 4);
-    L.rec = off;        off = align256(off + record_bytes(nv_cap, hm, wm));
-    L.bands = off;      off = align256(off + band_bytes(nv_cap, hm, wm));
+    L.rec = off;        off = align256(off + (internal_aux ? record_bytes(nv_cap, hm, wm) : 0));
+    L.bands = off;      off = align256(off + (internal_aux ? band_bytes(nv_cap, hm, wm) : 0));
     L.total = off;
     return L;
 }
@@ -1564,7 +1610,9 @@ static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     C.rho_thin = pv[5]; C.thin_pct = pv[6]; C.alpha1 = pv[7]; C.thin_accept = pv[8];
     C.eps = pv[9]; C.mask_thr = pv[10]; C.thin_floor = pv[11]; C.kappa = pv[12];
     C.enable_thin = pv[13] != 0.0;
-    C.band_ok = C.thin_pct > 0.0 ? 1 : 0;
+    // zero support => p_cov = 0 => t = 0 (thin_pct > 0) < thin_accept: no vote.
+    // Needs thin_accept > 0 too (FusionParams enforces it; raw vectors may not)
+    C.band_ok = (C.thin_pct > 0.0 && C.thin_accept > 0.0) ? 1 : 0;
     C.ntx = (a->wm + kBandTile - 1) / kBandTile;
     C.nty = (a->hm + kBandTile - 1) / kBandTile;
     C.cube_r = 0.8660254037844387 * a->dx_vox * (1.0 + 1e-9);
@@ -1626,9 +1674,15 @@ static void launch_aux(const divas_fuse_args *a, int v0, int cnt, float2 *rec, d
 
 using namespace divas;
 
+extern "C" size_t divas_fuse_workspace_size_ext(int64_t max_gated, int32_t nv_cap, int32_t hm,
+                                                int32_t wm, int32_t internal_aux) {
+    return ws_layout(max_gated, nv_cap > 0 ? nv_cap : 1, hm > 0 ? hm : 1, wm > 0 ? wm : 1,
+                     internal_aux != 0).total;
+}
+
 extern "C" size_t divas_fuse_workspace_size(int64_t max_gated, int32_t nv_cap, int32_t hm,
                                             int32_t wm) {
-    return ws_layout(max_gated, nv_cap > 0 ? nv_cap : 1, hm > 0 ? hm : 1, wm > 0 ? wm : 1).total;
+    return divas_fuse_workspace_size_ext(max_gated, nv_cap, hm, wm, 1);
 }
 
 extern "C" const int64_t *divas_fuse_gated_count(const void *workspace) {
@@ -1649,6 +1703,12 @@ static int validate(const divas_fuse_args *a, const char *who) {
         return DIVAS_EINVAL;
     }
     if (nvox > 0xffffffffLL) { set_error("%s: grid too large for 32-bit slots", who); return DIVAS_EINVAL; }
+    const int64_t nb = (a->g + kBrick - 1) / kBrick;   // gate bricks of the full grid
+    if (nb * nb * nb > kGateTileMax) {
+        set_error("%s: grid of %lld^3 has more than %lld gate bricks", who, (long long)a->g,
+                  (long long)kGateTileMax);
+        return DIVAS_EINVAL;
+    }
     if (!a->density) { set_error("%s: null density", who); return DIVAS_EINVAL; }
     return DIVAS_OK;
 }
@@ -1704,7 +1764,7 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         }
     }
     const int64_t cap = a->max_gated > 0 ? a->max_gated : (a->vox_hi - a->vox_lo);
-    const WsLayout L = ws_layout(cap, nv_cap, a->hm, a->wm);
+    const WsLayout L = ws_layout(cap, nv_cap, a->hm, a->wm, a->records == nullptr);
     if (workspace_bytes < L.total) {
         set_error("divas_fuse: workspace too small (%zu < %zu)", workspace_bytes, L.total);
         return DIVAS_EWORKSPACE;
@@ -1787,9 +1847,9 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
 }
 
 extern "C" void divas_fuse_ws_regions(int64_t max_gated, int32_t nv_cap, int32_t hm, int32_t wm,
-                                      size_t out[7]) {
+                                      int32_t internal_aux, size_t out[7]) {
     const WsLayout L = ws_layout(max_gated, nv_cap > 0 ? nv_cap : 1, hm > 0 ? hm : 1,
-                                 wm > 0 ? wm : 1);
+                                 wm > 0 ? wm : 1, internal_aux != 0);
     out[0] = L.work; out[1] = L.bits_thick; out[2] = L.bits_thin;
     out[3] = L.w; out[4] = L.mw; out[5] = L.t; out[6] = L.total;
 }

@@ -364,7 +364,11 @@ class Fuser:
             out["occ"] = occ
         lib = _native.lib()
         nvc = max(int(nv_cap or views.nv), views.nv)
-        wsb = lib.divas_fuse_workspace_size(cap, nvc, views.hm, views.wm)
+        if hasattr(lib, "divas_fuse_workspace_size_ext"):
+            wsb = lib.divas_fuse_workspace_size_ext(cap, nvc, views.hm, views.wm,
+                                                    1 if aux is None else 0)
+        else:                                   # experiment builds of older revisions
+            wsb = lib.divas_fuse_workspace_size(cap, nvc, views.hm, views.wm)
         if workspace is None or workspace.numel() < wsb:
             workspace = torch.empty(wsb, dtype=torch.uint8, device=dev)
         out["workspace"] = workspace

@@ -200,14 +200,24 @@ def gather_occupancy(occ_slab, slabs, g: int, rank: int, group=None):
 class PeerOccupancy:
     """The slab all-gather fused into the fusion's stores.
 
-    A [G^3] uint8 occupancy buffer in symmetric memory on every rank
+    Two [G^3] uint8 occupancy buffers in symmetric memory on every rank
     (``torch.distributed._symmetric_memory``: NVLink peer mappings of each
     rank's allocation).  ``Fuser.run(occ_peers=self.peers)`` makes the gate and
-    reduce kernels store each voxel's occupancy byte into EVERY rank's buffer
-    (zeros of the slab as coalesced 4-byte stores, the gated voxels' p >= thr
-    bytes as they are reduced), so after ``barrier()`` each rank holds the
-    full grid without a separate collective.  Raises if symmetric memory is
-    unavailable (the caller falls back to ``gather_occupancy``).
+    reduce kernels store each voxel's occupancy byte into EVERY rank's current
+    buffer (zeros of the slab as coalesced 4-byte stores, the gated voxels'
+    p >= thr bytes as they are reduced), so after ``barrier()`` each rank holds
+    the full grid in ``buf`` without a separate collective.
+
+    Contract (no write-after-read race across ranks): step k writes buffer
+    k % 2 and ``barrier()`` flips to the other buffer for step k + 1.  A fast
+    rank can start writing step k + 1 while a slow rank still reads step k's
+    result -- they touch different buffers.  It can write buffer k % 2 again
+    only in step k + 2, after the step-(k+1) barrier, which every rank reaches
+    only after its own step-(k+1) work on the stream; so a step's ``buf`` is
+    valid until the caller's next-but-one step, provided it is read on the
+    fusion stream (or copied) before the next step's barrier.
+    Raises if symmetric memory is unavailable (the caller falls back to
+    ``gather_occupancy``).
     """
 
     def __init__(self, nvox: int, device, group=None):
@@ -215,17 +225,35 @@ class PeerOccupancy:
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm
         group = group or dist.group.WORLD
-        self.buf = symm.empty(nvox, dtype=torch.uint8, device=device)
-        self.hdl = symm.rendezvous(self.buf, group)
-        self.world = int(self.hdl.world_size)
-        ptrs = [int(p) for p in self.hdl.buffer_ptrs]
-        self.ptr_table = torch.tensor(ptrs, dtype=torch.int64, device=device)
-        self.peers = (int(self.ptr_table.data_ptr()), self.world)
+        self.bufs, self.hdls, self.tables = [], [], []
+        for _ in range(2):
+            b = symm.empty(nvox, dtype=torch.uint8, device=device)
+            h = symm.rendezvous(b, group)
+            self.bufs.append(b)
+            self.hdls.append(h)
+            self.tables.append(torch.tensor([int(p) for p in h.buffer_ptrs], dtype=torch.int64,
+                                            device=device))
+        self.world = int(self.hdls[0].world_size)
+        self.cur = 0
+
+    @property
+    def buf(self):
+        """The buffer the current step stores into (the full grid after barrier())."""
+        return self.bufs[self.cur]
+
+    @property
+    def peers(self):
+        """(device pointer of the current buffer's per-rank pointer table, world)."""
+        return (int(self.tables[self.cur].data_ptr()), self.world)
 
     def barrier(self):
         """Device-side barrier on the current stream: every rank's stores of
-        this step have landed in every buffer after it."""
-        self.hdl.barrier(channel=0)
+        this step have landed in every rank's ``buf`` after it.  Returns that
+        buffer and flips to the other one for the next step."""
+        done = self.cur
+        self.hdls[done].barrier(channel=0)
+        self.cur ^= 1
+        return self.bufs[done]
 
 
 class PeerGather:

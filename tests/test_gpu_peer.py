@@ -61,12 +61,18 @@ def test_peer_occupancy_symmetric_memory_world1():
                             world_size=1, device_id=dev)
     try:
         peer = sharding.PeerOccupancy(case.g ** 3, dev)
-        peer.buf.fill_(9)
-        fuser.run(dens, dv, occ=None, occ_peers=peer.peers)
-        peer.barrier()
-        torch.cuda.synchronize()
-        assert peer.world == 1
-        assert torch.equal(peer.buf, occ_full)
+        for b in peer.bufs:
+            b.fill_(9)
+        # two steps: each writes its own buffer (double-buffered, no WAR race)
+        for step in range(2):
+            first = peer.buf
+            fuser.run(dens, dv, occ=None, occ_peers=peer.peers)
+            got = peer.barrier()
+            torch.cuda.synchronize()
+            assert got.data_ptr() == first.data_ptr()
+            assert peer.buf.data_ptr() != first.data_ptr()
+            assert peer.world == 1
+            assert torch.equal(got, occ_full)
     finally:
         dist.destroy_process_group()
 
