@@ -184,7 +184,23 @@ typedef struct divas_fuse_args {
                                     into the gate (zeros) and reduce (p >=
                                     occ_thr) stores.  Independent of `occ`.    */
     int32_t n_peers;
+    uint64_t *fallbacks;         /* NULL, or device [DIVAS_NFALLBACK] counters:
+                                    how often each certified shortcut could
+                                    not decide and the reference's exact chain
+                                    ran (DIVAS_FB_*; accumulated, never reset) */
 } divas_fuse_args;
+
+/* Fallback counters of divas_fuse_args.fallbacks (exact-chain evaluations). */
+#define DIVAS_FB_CENTRE      0   /* centre pixel / frustum: exact u, v chain     */
+#define DIVAS_FB_THICK       1   /* thick spatial test: exact _thick_pair chain  */
+#define DIVAS_FB_THICK_T     2   /* thick weight: exact t_proj for the clamp     */
+#define DIVAS_FB_CORNERS     3   /* thin footprint: exact 8-corner chain         */
+#define DIVAS_FB_RECOUNT     4   /* thin support: f64 recount of the footprint   */
+#define DIVAS_FB_THIN_GATE   5   /* thin gate dx * max(fx, fy) / x_d >= 1 in f64 */
+#define DIVAS_FB_BAND_WIDE   6   /* band test skipped: box wider than its tiles  */
+#define DIVAS_FB_TILE_SKIP   7   /* (not a fallback) pair tiles rejected whole by
+                                    the tile-level band test                    */
+#define DIVAS_NFALLBACK      8
 
 /* Workspace bytes for divas_fuse with slot capacity `max_gated`, `nv_cap`
  * views of padded size hm x wm (~ max_gated * (4 + nv_cap * 24.25) bytes for

@@ -50,7 +50,7 @@ class FuseArgs(ctypes.Structure):
         ("st", _VP), ("occ", _VP), ("occ_thr", ctypes.c_double), ("max_gated", ctypes.c_int64),
         ("records", _VP), ("bands", _VP), ("nv_cap", ctypes.c_int32), ("mode", ctypes.c_int32),
         ("view_lo", ctypes.c_int32), ("view_hi", ctypes.c_int32),
-        ("occ_peers", _VP), ("n_peers", ctypes.c_int32),
+        ("occ_peers", _VP), ("n_peers", ctypes.c_int32), ("fallbacks", _VP),
     ]
 
 MAX_PRIMS = 128
@@ -70,6 +70,11 @@ class RenderCfg(ctypes.Structure):
                 ("far_", ctypes.c_double), ("tau_cw", ctypes.c_double),
                 ("min_weight", ctypes.c_double)]
 
+
+# fallback counters (divas_fuse_args.fallbacks), DIVAS_FB_* in the header
+FALLBACKS = ("centre", "thick", "thick_t", "corners", "recount", "thin_gate", "band_wide",
+             "tile_skip")
+NFALLBACK = 8
 
 FUSE_FULL = 0
 STEP_GATE, STEP_CLEAR_ALL, STEP_CLEAR_VIEWS, STEP_PAIRS, STEP_REDUCE = 1, 2, 4, 8, 16

@@ -1,5 +1,6 @@
 // bands.cuh -- per-view 8x8-tile depth bands for exact thin-path rejection.
 //
+// (The bands also cover pixels with m == 0.5: band_px.)
 // A footprint pixel p supports a thin candidate at depth x_d iff
 //   mask_p > 0.5 && n_p > 0 && |fl(x_d - D_p)| <= tau(n_p)          (fusion.py:361-367)
 // which implies  D_p - tau(1 + 2^-52) <= x_d <= D_p + tau(1 + 2^-52).  A tile's
@@ -72,9 +73,15 @@ static __global__ void band_init(double2 *__restrict__ bands, int nv, int nty, i
     }
 }
 
+// A pixel widens its tile's band when m >= 0.5 and n > 0 (thin support needs
+// m > 0.5, the thick gate m >= mask_thr = 0.5: the band covers both, so a
+// tile whose band misses x_d can neither support a thin candidate nor hold a
+// thick centre pixel that passes the depth test, tau_depth <= tau_thin);
+// returns the pixel's tau as f32 when it can support (m > 0.5), else
+// kIneligible.
 __device__ __forceinline__ float band_px(float m, int32_t n, float d, const BandParams &B,
                                          double &lo, double &hi) {
-    if (m > 0.5f && n > 0) {
+    if (m >= 0.5f && n > 0) {
         double b = B.beta * (double)n;
         if (b > B.bmax) b = B.bmax;
         const double t = (2.0 * B.gamma + b) * B.dx;
@@ -82,7 +89,7 @@ __device__ __forceinline__ float band_px(float m, int32_t n, float d, const Band
         const double mg = 1e-12 * (fabs(D) + t);
         lo = fmin(lo, D - t - mg);
         hi = fmax(hi, D + t + mg);
-        return (float)t;
+        return m > 0.5f ? (float)t : kIneligible;
     }
     return kIneligible;
 }

@@ -61,7 +61,14 @@ struct FuseConst {
     int unbounded;
     double occ_thr;
     int gshift;          // log2(g) when g is a power of two, else -1
+    unsigned long long *fallbacks;   // exact-chain counters (DIVAS_FB_*), or NULL
+    int cull;            // tile-level band rejection allowed (tile_culled)
 };
+
+// Count one exact-chain evaluation (rare sites only; no-op without counters).
+__device__ __forceinline__ void fallback(const FuseConst &C, int i) {
+    if (C.fallbacks) atomicAdd(C.fallbacks + i, 1ull);
+}
 
 // (ix, iy, iz) of a flat voxel index: shifts for power-of-two grids
 __device__ __forceinline__ void voxel_coords(const FuseConst &C, uint32_t vi, uint32_t &ix,
@@ -722,6 +729,7 @@ __device__ __forceinline__ bool thin_bounds(const FuseConst &C, const Cam &k, do
             return true;
     }
     PSTAT(13, 1);
+    fallback(C, DIVAS_FB_CORNERS);
     // exact corner chain (fusion.py:315-341)
     double umn = 1e30, umx = -1e30, vmn = 1e30, vmx = -1e30;
 #pragma unroll 1
@@ -783,7 +791,11 @@ __device__ __forceinline__ bool band_reject(const FuseConst &C, const FuseMaps &
     const int tx0 = (int)fmax(fx0, 0.0), tx1 = (int)fmin(fx1, (double)(C.ntx - 1));
     const int ty0 = (int)fmax(fy0, 0.0), ty1 = (int)fmin(fy1, (double)(C.nty - 1));
     if (tx1 < tx0 || ty1 < ty0) return false;
-    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > kBandMaxTiles) { PSTAT(15, 1); return false; }
+    if ((tx1 - tx0 + 1) * (ty1 - ty0 + 1) > kBandMaxTiles) {
+        PSTAT(15, 1);
+        fallback(C, DIVAS_FB_BAND_WIDE);
+        return false;
+    }
     const double2 *bv = M.bands + (int64_t)view * band_view_stride(C.nty, C.ntx);
     // tiles in row-major order, four loads in flight per round trip (indices
     // past the last tile repeat it: always in range, never changes the answer)
@@ -960,7 +972,10 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
         py = pixel_index(v, (long long)k.h);
     }
     PSTAT(1, 1);
-    if (cu == 2 || cv == 2) PSTAT(14, 1);
+    if (cu == 2 || cv == 2) {
+        PSTAT(14, 1);
+        fallback(C, DIVAS_FB_CENTRE);
+    }
     const int64_t plane = (int64_t)C.hm * C.wm;
     const int64_t vplane = (int64_t)view * plane;
     const int64_t q = py * (int64_t)C.wm + px;
@@ -1006,6 +1021,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
             double wd = 0.0;
             if (ok == 1) {
                 if (need_t) {
+                    fallback(C, DIVAS_FB_THICK_T);
                     const double u = (k.fx * (xcam / x_d) + k.cx) / k.w;
                     const double v = (k.cy - k.fy * (ycam / x_d)) / k.h;
                     t_c = exact_tproj(k, xc0, xc1, xc2, u, v);
@@ -1015,6 +1031,7 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
                 wd = depth_weight(C, t_c, dmin, dmax);
             } else if (ok == 2) {                  // exact reference chain
                 PSTAT(12, 1);
+                fallback(C, DIVAS_FB_THICK);
                 const double u = (k.fx * (xcam / x_d) + k.cx) / k.w;
                 const double v = (k.cy - k.fy * (ycam / x_d)) / k.h;
                 ok = thick_spatial(C, k, xc0, xc1, xc2, u, v, dmin, dmax, gr, wd) ? 1 : 0;
@@ -1037,7 +1054,10 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
         const double fmax = k.fx > k.fy ? k.fx : k.fy;
         const double a = C.dx * fmax;
         if (a < x_d * (1.0 - 1e-12)) return false;
-        if (!(a > x_d * (1.0 + 1e-12)) && !(a / x_d >= 1.0)) return false;
+        if (!(a > x_d * (1.0 + 1e-12))) {
+            fallback(C, DIVAS_FB_THIN_GATE);
+            if (!(a / x_d >= 1.0)) return false;
+        }
     }
     PSTAT(6, 1);
     if (C.band_ok && band_reject(C, M, k, view, x_d, xcam, ycam, A + k.cx, k.cy - B))
@@ -1057,16 +1077,25 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
 // whether any record fell inside the margin.  MODE 0: one tau per view
 // (plane A alone); 1: the base tau, a flagged record (negative m) also makes
 // the item unsure; 2: per-record tau from plane B.  Returns "unsure".
+// -1 when a <= b, else 0 (NaN compares false): one FSET, so a count is one
+// add per record instead of a compare, an increment and a select
+__device__ __forceinline__ int le_mask(float a, float b) {
+    int m;
+    asm("set.le.s32.f32 %0, %1, %2;" : "=r"(m) : "f"(a), "f"(b));
+    return m;
+}
+
 template <int MODE>
 __device__ __forceinline__ bool scan_box(const float2 *__restrict__ rp, int wm, int64_t plane,
                                          int bw, int bh, float xd32, float tau, float Mg,
                                          int &sup, float &mmax) {
     float emin = __int_as_float(0x7f800000);   // +inf
     float fmin_ = 0.0f;                         // most negative m (MODE 1 flags)
+    const float nMg = -Mg;
     auto pix = [&](float2 r, float t) {
         mmax = fmaxf(mmax, fabsf(r.x));
         const float e = fabsf(xd32 - r.y) - (MODE == 2 ? t : tau);
-        sup += (e <= -Mg) ? 1 : 0;
+        sup -= le_mask(e, nMg);                  // e <= -Mg (NaN: no)
         emin = fminf(emin, fabsf(e));
         if (MODE == 1) fmin_ = fminf(fmin_, r.x);
     };
@@ -1147,16 +1176,20 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     float mmax = 0.0f;
     bool unsure;
     if (tk0 >= tk1) {   // one tau for every supporting pixel of the view (or none)
-        unsure = scan_box<0>(rp, C.wm, plane, bw, bh, xd32, __uint_as_float(tk0), Mg, sup, mmax);
+        unsure = scan_box<0>(rp, C.wm, plane, bw, bh, xd32, __uint_as_float(tk0), Mg,
+                             sup, mmax);
     } else if ((uint64_t)nflag * 32u <= nsup) {
         // few supporting pixels differ from the base tau: scan with the base
         // tau, a flagged pixel (negative mask) sends the item to the recount
-        unsure = scan_box<1>(rp, C.wm, plane, bw, bh, xd32, __uint_as_float(__ldg(te + 4)), Mg,
-                             sup, mmax);
+        unsure = scan_box<1>(rp, C.wm, plane, bw, bh, xd32, __uint_as_float(__ldg(te + 4)),
+                             Mg, sup, mmax);
     } else {
         unsure = scan_box<2>(rp, C.wm, plane, bw, bh, xd32, 0.0f, Mg, sup, mmax);
     }
-    if (unsure) PSTAT(10, 1);
+    if (unsure) {
+        PSTAT(10, 1);
+        fallback(C, DIVAS_FB_RECOUNT);
+    }
     if (unsure) {   // some pixel within the margin: recount with the reference's f64 test
         sup = 0;
         const int32_t *np = M.nsamps + (int64_t)view * plane + ys * (int64_t)C.wm + xs;
@@ -1211,18 +1244,143 @@ __device__ __forceinline__ void pair_tile(const FuseConst &C, const Cam &k,
     for (int i = threadIdx.x; i < nq; i += blockDim.x) thin_item(C, k, M, K, view, s_q[i]);
 }
 
+// Tile-level rejection (exact): can ANY pair of this tile (one view x the
+// tile's gated voxels) contribute?  A thick vote needs its centre pixel p with
+// m >= mask_thr >= 0.5, n > 0 and |x_d - D_p| <= tau_depth(n) <= tau_thin(n);
+// a thin vote (band_ok) needs support, i.e. a footprint pixel with m > 0.5,
+// n > 0 and |x_d - D_p| <= tau_thin(n).  Either way x_d lies in the depth band
+// of p's 8x8 tile (bands.cuh covers every pixel with m >= 0.5).  Every centre
+// pixel and footprint of the tile's voxels lies in the projection of their
+// bounding box (convex, in front of the camera: inside the hull of its 8
+// corners' projections, padded by a pixel), and their x_d in the corners'
+// depth range (depth is affine), so when that range meets no band of the
+// covered tiles no pair can vote: the tile is skipped.  Run by warp 0;
+// bb = {min ix, iy, iz, max ix, iy, iz} of the tile's voxels.
+__device__ __forceinline__ bool tile_culled(const FuseConst &C, const Cam &k,
+                                            const FuseMaps &M, int view, const unsigned *bb) {
+    const int lane = threadIdx.x & 31;
+    double xc = 0.0, yc = 0.0, d = 1.0, sc = 0.0;
+    if (lane < 8) {
+        const double px = C.origin0 + (double)(bb[0] + (lane & 1 ? bb[3] - bb[0] + 1 : 0)) * C.dx;
+        const double py = C.origin1 + (double)(bb[1] + (lane & 2 ? bb[4] - bb[1] + 1 : 0)) * C.dx;
+        const double pz = C.origin2 + (double)(bb[2] + (lane & 4 ? bb[5] - bb[2] + 1 : 0)) * C.dx;
+        const double rx = px - k.p0, ry = py - k.p1, rz = pz - k.p2;
+        d = -(k.r[2] * rx + k.r[5] * ry + k.r[8] * rz);
+        xc = k.r[0] * rx + k.r[3] * ry + k.r[6] * rz;
+        yc = k.r[1] * rx + k.r[4] * ry + k.r[7] * rz;
+        sc = fabs(px) + fabs(py) + fabs(pz) + fabs(k.p0) + fabs(k.p1) + fabs(k.p2);
+    }
+    const double mg = 1e-9 * (sc + 1.0);
+    const bool behind = lane < 8 ? d < -mg : true;
+    const bool front = lane < 8 ? d > mg : true;
+    if (__all_sync(0xffffffffu, behind)) return true;       // every voxel centre is behind
+    if (!__all_sync(0xffffffffu, front)) return false;      // straddles the camera plane
+    double u = lane < 8 ? k.fx * (xc / d) + k.cx : 0.0;      // pixel coordinates
+    double v = lane < 8 ? k.cy - k.fy * (yc / d) : 0.0;
+    double umn = lane < 8 ? u : 1e300, umx = lane < 8 ? u : -1e300;
+    double vmn = lane < 8 ? v : 1e300, vmx = lane < 8 ? v : -1e300;
+    double dlo = lane < 8 ? d - mg : 1e300, dhi = lane < 8 ? d + mg : -1e300;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+        umn = dmin2(umn, __shfl_xor_sync(0xffffffffu, umn, o));
+        umx = dmax2(umx, __shfl_xor_sync(0xffffffffu, umx, o));
+        vmn = dmin2(vmn, __shfl_xor_sync(0xffffffffu, vmn, o));
+        vmx = dmax2(vmx, __shfl_xor_sync(0xffffffffu, vmx, o));
+        dlo = dmin2(dlo, __shfl_xor_sync(0xffffffffu, dlo, o));
+        dhi = dmax2(dhi, __shfl_xor_sync(0xffffffffu, dhi, o));
+    }
+    umn = __shfl_sync(0xffffffffu, umn, 0); umx = __shfl_sync(0xffffffffu, umx, 0);
+    vmn = __shfl_sync(0xffffffffu, vmn, 0); vmx = __shfl_sync(0xffffffffu, vmx, 0);
+    dlo = __shfl_sync(0xffffffffu, dlo, 0); dhi = __shfl_sync(0xffffffffu, dhi, 0);
+    const double W = k.w, H = k.h;
+    if (!(umx > -2.0 && umn < W + 2.0 && vmx > -2.0 && vmn < H + 2.0)) {
+        // the projection misses the image: every centre is out of the frustum,
+        // unless a NaN / inf slipped through (then do not skip)
+        return umx <= -2.0 || umn >= W + 2.0 || vmx <= -2.0 || vmn >= H + 2.0;
+    }
+    const int x0 = (int)fmax(floor(umn) - 1.0, 0.0), x1 = (int)fmin(floor(umx) + 1.0, W - 1.0);
+    const int y0 = (int)fmax(floor(vmn) - 1.0, 0.0), y1 = (int)fmin(floor(vmx) + 1.0, H - 1.0);
+    const int tx0 = x0 / kBandTile, tx1 = min(x1 / kBandTile, C.ntx - 1);
+    const int ty0 = y0 / kBandTile, ty1 = min(y1 / kBandTile, C.nty - 1);
+    const int nx = tx1 - tx0 + 1, nt = nx * (ty1 - ty0 + 1);
+    if (nx < 1 || nt < 1 || nt > 256) return false;
+    const double2 *bv = M.bands + (int64_t)view * band_view_stride(C.nty, C.ntx);
+    bool hit = false;
+    for (int i = lane; i < nt; i += 32) {
+        const int ty = ty0 + i / nx, tx = tx0 + i % nx;
+        const double2 b = __ldg(bv + (int64_t)ty * C.ntx + tx);
+        hit |= dhi >= b.x && dlo <= b.y;
+    }
+    return !__any_sync(0xffffffffu, hit);
+}
+
+// Pre-pass of fuse_pairs: one CTA per tile of 256 slots; the bounding box of
+// the tile's voxels once, then each warp runs tile_culled for its share of the
+// views.  skip[(view - view0) * ntiles + tile] = 1: the pair CTA exits at once.
+// Tiles whose voxels spread over more than 32 voxels on an axis (a slot run
+// that wraps to another brick row) are never skipped (their rectangles would
+// cover too many band tiles to be worth testing).
+__global__ void __launch_bounds__(kPairThreads)
+tile_cull(FuseConst C, const double *__restrict__ cams, FuseMaps M,
+          const uint32_t *__restrict__ work, const WsHeader *__restrict__ hdr, int nviews,
+          uint8_t *__restrict__ skip) {
+    __shared__ unsigned s_bb[6];
+    const long long n = min((long long)hdr->count, (long long)C.cap);
+    const long long block0 = (long long)blockIdx.x * blockDim.x;
+    const long long ntiles = gridDim.x;
+    if (block0 >= n) return;                         // fuse_pairs exits on its own
+    if (threadIdx.x == 0) {
+        s_bb[0] = s_bb[1] = s_bb[2] = 0xffffffffu;
+        s_bb[3] = s_bb[4] = s_bb[5] = 0u;
+    }
+    __syncthreads();
+    const long long slot = block0 + threadIdx.x;
+    unsigned ix = 0xffffffffu, iy = 0xffffffffu, iz = 0xffffffffu;
+    unsigned jx = 0u, jy = 0u, jz = 0u;
+    if (slot < n) {
+        voxel_coords(C, __ldg(work + slot), ix, iy, iz);
+        jx = ix; jy = iy; jz = iz;
+    }
+    ix = __reduce_min_sync(0xffffffffu, ix); iy = __reduce_min_sync(0xffffffffu, iy);
+    iz = __reduce_min_sync(0xffffffffu, iz); jx = __reduce_max_sync(0xffffffffu, jx);
+    jy = __reduce_max_sync(0xffffffffu, jy); jz = __reduce_max_sync(0xffffffffu, jz);
+    if ((threadIdx.x & 31) == 0 && ix != 0xffffffffu) {
+        atomicMin(&s_bb[0], ix); atomicMin(&s_bb[1], iy); atomicMin(&s_bb[2], iz);
+        atomicMax(&s_bb[3], jx); atomicMax(&s_bb[4], jy); atomicMax(&s_bb[5], jz);
+    }
+    __syncthreads();
+    unsigned bb[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) bb[i] = s_bb[i];
+    const bool compact = bb[3] - bb[0] < 32 && bb[4] - bb[1] < 32 && bb[5] - bb[2] < 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int v = warp; v < nviews; v += kPairThreads / 32) {
+        bool cull = false;
+        if (compact) {
+            Cam k;
+            load_cam(cams + (int64_t)(C.view0 + v) * kCamStride, k);
+            cull = tile_culled(C, k, M, C.view0 + v, bb);
+        }
+        if (lane == 0) {
+            skip[(int64_t)v * ntiles + blockIdx.x] = cull ? 1 : 0;
+            if (cull) fallback(C, DIVAS_FB_TILE_SKIP);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
 fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
            FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
-           const WsHeader *__restrict__ hdr, int nviews) {
+           const WsHeader *__restrict__ hdr, int nviews, const uint8_t *__restrict__ skip) {
     __shared__ QItem s_q[kQueue];
     __shared__ int s_nq;
     const long long n = min((long long)hdr->count, (long long)C.cap);
     const int view = C.view0 + (int)blockIdx.y;
-    if (threadIdx.x == 0) s_nq = 0;
-    __syncthreads();
     const long long block0 = (long long)blockIdx.x * blockDim.x;
     if (block0 >= n) return;                                   // whole CTA idle
+    if (skip && __ldg(skip + (int64_t)blockIdx.y * gridDim.x + blockIdx.x)) return;
+    if (threadIdx.x == 0) s_nq = 0;
+    __syncthreads();
     Cam k;
     load_cam(cams + (int64_t)view * kCamStride, k);
     pair_tile(C, k, dens, M, K, work, n, block0, view, s_q, &s_nq);
@@ -1557,7 +1715,7 @@ __global__ void clear_view_bits(Contrib K, int64_t cap, int view_lo, int view_hi
 // workspace layout
 // ---------------------------------------------------------------------------
 struct WsLayout {
-    size_t work, bits_thick, bits_thin, w, mw, t, dirty, gtiles, rec, bands, total;
+    size_t work, bits_thick, bits_thin, w, mw, t, dirty, gtiles, skip, rec, bands, total;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -1578,6 +1736,7 @@ static WsLayout ws_layout(int64_t cap, int32_t nv_cap, int32_t hm, int32_t wm, b
     L.t = off;          off = align256(off + (size_t)nv_cap * c * 8);
     L.dirty = off;      off = align256(off + c);
     L.gtiles = off;     off = align256(off + (size_t)kGateTileMax * 4);
+    L.skip = off;       off = align256(off + (size_t)nv_cap * ((c + kPairThreads - 1) / kPairThreads));
     L.rec = off;        off = align256(off + (internal_aux ? record_bytes(nv_cap, hm, wm) : 0));
     L.bands = off;      off = align256(off + (internal_aux ? band_bytes(nv_cap, hm, wm) : 0));
     L.total = off;
@@ -1613,6 +1772,9 @@ static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     // zero support => p_cov = 0 => t = 0 (thin_pct > 0) < thin_accept: no vote.
     // Needs thin_accept > 0 too (FusionParams enforces it; raw vectors may not)
     C.band_ok = (C.thin_pct > 0.0 && C.thin_accept > 0.0) ? 1 : 0;
+    // tile skipping needs every voting pixel inside the bands (m >= 0.5):
+    // thick gate mask_thr >= 0.5, and thin votes only with support
+    C.cull = (C.mask_thr >= 0.5 && (C.band_ok || !C.enable_thin)) ? 1 : 0;
     C.ntx = (a->wm + kBandTile - 1) / kBandTile;
     C.nty = (a->hm + kBandTile - 1) / kBandTile;
     C.cube_r = 0.8660254037844387 * a->dx_vox * (1.0 + 1e-9);
@@ -1621,6 +1783,7 @@ static void fill_const(FuseConst &C, const divas_fuse_args *a, int64_t cap) {
     C.bh0 = a->bh[0]; C.bh1 = a->bh[1]; C.bh2 = a->bh[2];
     C.unbounded = a->unbounded;
     C.occ_thr = a->occ_thr;
+    C.fallbacks = (unsigned long long *)a->fallbacks;
 }
 
 static void launch_gate_count(const FuseConst &C, const float *dens, WsHeader *hdr,
@@ -1823,8 +1986,15 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
                 __atomic_fetch_or(&carve_set, bit, __ATOMIC_RELAXED);
             }
         }
-        fuse_pairs<<<dim3((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)(v1 - v0)),
-                     kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr, v1 - v0);
+        const dim3 pg((unsigned)std::max<int64_t>(cap_blocks, 1), (unsigned)(v1 - v0));
+        uint8_t *skip = nullptr;
+        if (C.cull) {       // tile-level band rejection first (exact, see tile_culled)
+            skip = (uint8_t *)(ws + L.skip);
+            tile_cull<<<pg.x, kPairThreads, 0, s>>>(C, a->cams, M, work, hdr, v1 - v0, skip);
+            if ((rc = check_launch("divas_fuse(tile_cull)"))) return rc;
+        }
+        fuse_pairs<<<pg, kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr, v1 - v0,
+                                               skip);
         if ((rc = check_launch("divas_fuse(pairs)"))) return rc;
     }
     if (steps & DIVAS_STEP_REDUCE) {

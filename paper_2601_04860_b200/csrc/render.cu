@@ -10,16 +10,13 @@
 // (-fmad=false), except the two sites where numpy goes through BLAS (see
 // np_density): there the fused chains OpenBLAS computes are restated with
 // explicit fma().  The only operation whose bits could differ from the
-// reference is exp inside the marcher's alpha = 1 - exp(-sigma * dt): it is
-// evaluated correctly rounded (exp_cr), which is what the C library returns
-// unless the exact value lies within a hundredth of an ulp of a rounding
-// midpoint.  In that rare case alpha may be either neighbour, and the marcher
-// carries a rigorous absolute bound of how far each running quantity
-// (transmittance, cumulative weight, weighted sums, colour) can be from the
-// reference's; a pixel is flagged `unsure` when a decision (new peak, the
-// min-weight and cutoff crossings) lies within that bound of its threshold or
-// an f32 output could round differently.  Every pixel that is not flagged is
-// bit-identical to the reference.
+// reference could be exp inside the marcher's alpha = 1 - exp(-sigma * dt):
+// it is glibc's exp restated bit for bit (exp_glibc, exp_cr.cuh), so alpha is
+// the reference's.  The marcher still carries the machinery of an absolute
+// bound on how far each running quantity can be from the reference's (an
+// earlier correctly-rounded exp could differ in the last bit near rounding
+// midpoints) and flags a pixel `unsure` when a decision lies within that
+// bound; with the exact exp every bound is 0 and no pixel is flagged.
 #include <algorithm>
 #include <cmath>
 
@@ -201,11 +198,7 @@ __device__ __forceinline__ void march(const SceneConst &S, const MarchConst &R, 
             if (x < -38.0) {
                 a = 1.0;          // exp(x) < 2^-54: 1 - exp(x) rounds to 1 for any exp
             } else {
-                bool amb;
-                double alt;
-                const double e = exp_cr(x, amb, alt);
-                a = 1.0 - e;
-                if (amb) Ea = fabs(a - (1.0 - alt));   // 0 when both round alike
+                a = 1.0 - exp_glibc(x);   // the C library's exp, bit for bit: Ea = 0
             }
             if (ET + Ea > 0.0 && T < 1e-280) unsure = true;   // subnormal: no rel. bound
         }

@@ -326,7 +326,7 @@ class Fuser:
     def run(self, density, views: DeviceViews, probs=None, stats=False, occ=False,
             occ_thr=0.5, vox_range=None, workspace=None, stream=None, max_gated=None,
             aux=None, nv_cap=None, incremental=None, steps=None, view_range=None,
-            occ_peers=None):
+            occ_peers=None, fallbacks=None):
         """Enqueue ``divas_fuse``.  ``aux``: ViewAux from ``refine_bands_device``
         (else built in the workspace).  ``incremental=(v0, v1)``: re-evaluate
         only views [v0, v1) against the state a previous full ``run`` left in
@@ -336,7 +336,10 @@ class Fuser:
         ``occ_peers``: (device pointer of an array of n buffer pointers, n) --
         the occupancy of the range is also stored into every listed [G^3]
         buffer (``sharding.PeerOccupancy``: the slab all-gather fused into the
-        fusion's own stores over NVLink)."""
+        fusion's own stores over NVLink).  ``fallbacks``: a CUDA int64 tensor of
+        ``_native.NFALLBACK`` counters that accumulate how often each certified
+        shortcut handed a pair to the reference's exact chain
+        (``_native.FALLBACKS`` names them)."""
         import ctypes
         import torch
         g = self.g
@@ -390,6 +393,11 @@ class Fuser:
         a.nv_cap = nvc
         if occ_peers is not None:
             a.occ_peers, a.n_peers = int(occ_peers[0]), int(occ_peers[1])
+        if fallbacks is not None:
+            if (fallbacks.dtype != torch.int64 or not fallbacks.is_cuda or
+                    fallbacks.numel() < _native.NFALLBACK):
+                raise ValueError("fallbacks must be a CUDA int64 tensor of NFALLBACK counters")
+            a.fallbacks = _native.ptr(fallbacks)
         if incremental is not None:
             a.mode = _native.FUSE_INCREMENTAL
             a.view_lo, a.view_hi = int(incremental[0]), int(incremental[1])

@@ -72,6 +72,12 @@ def fuzz_cases(limit=None):
     return [_case(d, f"t{t:03d}") for t in range(n)]
 
 
+def stress_cases():
+    """Adversarial lattice and dense (rho = 5) instances (make_stress_golden.py)."""
+    d = _npz("stress.npz")
+    return [_case(d, str(n)) for n in d["names"]]
+
+
 def scene_cases():
     d = _npz("scene.npz")
     return {k: _case(d, k) for k in ("sop", "small", "g1", "mixed")}

@@ -29,9 +29,23 @@ def lib(tmp_path_factory):
     d = tmp_path_factory.mktemp("expcr")
     src = d / "shim.cpp"
     src.write_text('#include "exp_cr.cuh"\n'
+                   '#include <stdlib.h>\n'
                    'extern "C" double exp_cr_host(double x, int *amb, double *alt) {\n'
                    '  bool a; double r = divas::exp_cr(x, a, *alt); *amb = a; return r; }\n'
-                   'extern "C" double libm_exp(double x) { return exp(x); }\n')
+                   'extern "C" double libm_exp(double x) { return exp(x); }\n'
+                   'extern "C" double glibc_exp_host(double x) { return divas::exp_glibc(x); }\n'
+                   '/* n random arguments per family (seeded), count bit mismatches vs libm */\n'
+                   'extern "C" long glibc_exp_sweep(long n, long seed) {\n'
+                   '  srand48(seed); long bad = 0;\n'
+                   '  for (long i = 0; i < n; ++i) { double x;\n'
+                   '    switch (i % 5) { case 0: x = -drand48() * 745.5; break;\n'
+                   '      case 1: x = -drand48() * drand48() * 4.0; break;\n'
+                   '      case 2: x = (drand48() - 0.5) * 1500.0; break;\n'
+                   '      case 3: x = -708.0 - drand48() * 38.0; break;\n'
+                   '      default: x = -exp(-drand48() * 700.0); }\n'
+                   '    double a = exp(x), b = divas::exp_glibc(x);\n'
+                   '    if (memcmp(&a, &b, 8) != 0) ++bad; }\n'
+                   '  return bad; }\n')
     so = d / "libexpcr.so"
     subprocess.run(["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC",
                     f"-I{HDR}", str(src), "-o", str(so)], check=True)
@@ -41,6 +55,10 @@ def lib(tmp_path_factory):
                                 ctypes.POINTER(ctypes.c_double)]
     lib.libm_exp.restype = ctypes.c_double
     lib.libm_exp.argtypes = [ctypes.c_double]
+    lib.glibc_exp_host.restype = ctypes.c_double
+    lib.glibc_exp_host.argtypes = [ctypes.c_double]
+    lib.glibc_exp_sweep.restype = ctypes.c_long
+    lib.glibc_exp_sweep.argtypes = [ctypes.c_long, ctypes.c_long]
     return lib
 
 
@@ -85,3 +103,15 @@ def test_exp_cr_matches_libm_when_unambiguous(lib):
             assert r == m, (x, r, m)
         else:
             assert m in (r, alt.value), x
+
+
+def test_exp_glibc_equals_libm_bit_for_bit(lib):
+    """exp_glibc (what the kernels call) restates the C library's exp: equal
+    bits on the adversarial list, the subnormal / overflow tails and 5e6
+    random arguments (the lattice case that exposed the correctly rounded
+    exp: exp(-0.180413167127756), 0.50008 ulp from glibc's result)."""
+    for x in _xs() + [-0.180413167127756, 0.0, -0.0, 1e-17, -745.13, -746.0, 709.7, 710.0,
+                      -1100.0, float("-inf"), float("inf")]:
+        assert lib.glibc_exp_host(x) == lib.libm_exp(x) or (x != x), x
+    for seed in (1, 2):
+        assert lib.glibc_exp_sweep(2_500_000, seed) == 0

@@ -1,4 +1,6 @@
-"""Incremental session fusion (C4) == full recompute, bit for bit."""
+"""Incremental session fusion (C4) == full recompute == the CPU oracle's
+refine + fuse of the resulting view set, bit for bit (the reference session
+recomputes everything on every update, session.py:212-215)."""
 
 import numpy as np
 import pytest
@@ -22,6 +24,18 @@ def scene():
     return grid, dens, pairs, params, bounds
 
 
+def _oracle(grid, dens, pairs, params, bounds):
+    """The CPU oracle on the same (view, raw mask) set: refine_mask then fuse
+    of the refined set -- the reference session's full recompute
+    (session.py:204-215)."""
+    import oracle
+    from paper_2601_04860_b200 import ConfidenceMask
+    refined = [(vg, ConfidenceMask(oracle.refine(np.asarray(m.values, np.float32), vg.z_surface,
+                                                 vg.n_samples), refined=True))
+               for vg, m in pairs]
+    return oracle.fuse(grid, dens, refined, params, bounds)["p"]
+
+
 def _full(grid, dens, pairs, params, bounds):
     from paper_2601_04860_b200 import refine_and_fuse
     og, _m = refine_and_fuse(grid, dens, pairs, params, bounds=bounds, return_refined=False)
@@ -37,6 +51,7 @@ def test_add_views_one_by_one(scene):
         assert s.add_view(vg, m) == k
         got = s.occupancy_grid().probs
         assert np.array_equal(got, _full(grid, dens, pairs[:k + 1], params, bounds)), k
+        assert np.array_equal(got, _oracle(grid, dens, pairs[:k + 1], params, bounds)), k
 
 
 def test_replace_mask_equals_recompute(scene):
@@ -53,6 +68,7 @@ def test_replace_mask_equals_recompute(scene):
         s.replace_mask(i, new)
         cur[i] = (cur[i][0], new)
         assert np.array_equal(s.occupancy_grid().probs, _full(grid, dens, cur, params, bounds))
+        assert np.array_equal(s.occupancy_grid().probs, _oracle(grid, dens, cur, params, bounds))
     s.refuse()
     assert np.array_equal(s.occupancy_grid().probs, _full(grid, dens, cur, params, bounds))
     with pytest.raises(ValueError):
@@ -95,6 +111,7 @@ def test_replace_mask_device_graph_replay(scene, graph):
         s.replace_mask_device(i, torch.from_numpy(vals).to(s.dev), graph=graph)
         cur[i] = (cur[i][0], ConfidenceMask(vals))
         assert np.array_equal(s.occupancy_grid().probs, _full(grid, dens, cur, params, bounds))
+        assert np.array_equal(s.occupancy_grid().probs, _oracle(grid, dens, cur, params, bounds))
     assert (len(s._graphs) == 3) == graph
     s.add_views(pairs[4:5])
     cur.append(pairs[4])

@@ -24,6 +24,18 @@ def test_oracle_matches_reference_fuzz(case):
     assert np.array_equal(r["p"], case.p)
 
 
+@pytest.mark.parametrize("case", golden_io.stress_cases(), ids=lambda c: c.name)
+def test_oracle_matches_reference_stress(case):
+    """Adversarial lattice (exact pixel edges, frustum borders, depth-test and
+    gate equalities) and dense rho = 5 instances: bit-exact, with and without
+    the density early-out."""
+    r = _run(case)
+    assert np.array_equal(r["p"], case.p)
+    r2 = _run(case, early_out=False)
+    for k in ("p", "n_thick", "n_thin"):
+        assert np.array_equal(r[k], r2[k]), k
+
+
 @pytest.mark.parametrize("name", ["sop", "small", "g1", "mixed"])
 def test_oracle_matches_reference_scenes(name):
     case = golden_io.scene_cases()[name]
