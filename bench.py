@@ -242,71 +242,168 @@ def parity_check(wl, details, probs, n_thick, n_thin, refined_gpu):
 # reference arm
 # ---------------------------------------------------------------------------
 
-def _marcher_inputs_cpu(wl):
-    """Replace the analytic view planes / density of ``wl`` (CPU tensors) by
-    the oracle's render_view / bake_density_grid of the same scene."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _reference_fixture(config, inputs):
+    """The workload of ``config`` as host arrays, made WITHOUT the repo's CUDA
+    library: the survey's camera rig (workloads.cameras), view planes from the
+    oracle's restatement of the reference's ``render_view`` and density from
+    its ``bake_density_grid`` (both bit-identical to the reference on its
+    golden vectors, tests/test_render_golden.py, and to this arm's device
+    marcher, tests/test_gpu_render.py), masks = the same analytic silhouette
+    (CPU torch, device-independent ops; workloads.render_maps)."""
     import oracle
-    import torch
     import workloads
+    cfg = workloads.CONFIGS[config]
+    cams = workloads.cameras(cfg["views"], cfg["n"], cfg["w"], cfg["h"])
     sc = workloads.scene_model()
-    cfg = (workloads.SPP, workloads.NEAR, workloads.FAR, 0.75, 1e-4)
-    for i, cam in enumerate(wl.cams):
-        o = oracle.render(sc, cam, cfg)
-        for plane, key in ((wl.dmins, "d_min"), (wl.dmaxs, "d_max"), (wl.dexps, "d_exp"),
-                           (wl.z_surface, "z_surface"), (wl.nsamps, "n_samples")):
-            plane[i].copy_(torch.from_numpy(o[key]))
-    b = sc.bounds
-    dens = oracle.bake(sc, wl.g, workloads.GRID_HALF, wl.origin, (b.min, b.max, b.unbounded))
-    wl.density.copy_(torch.from_numpy(dens.reshape(-1)))
+    rcfg = (workloads.SPP, workloads.NEAR, workloads.FAR, 0.75, 1e-4)
+    planes = []
+    for cam in cams:
+        dmin, dmax, dexp, n, z, core, _ = workloads.render_maps(cam, "cpu")
+        raw = workloads.silhouette_mask(core).numpy()
+        if inputs == "marcher":
+            o = oracle.render(sc, cam, rcfg)
+            pl = dict(d_min=o["d_min"], d_max=o["d_max"], d_exp=o["d_exp"],
+                      n_samples=o["n_samples"], z_surface=o["z_surface"])
+        else:
+            pl = dict(d_min=dmin.numpy(), d_max=dmax.numpy(), d_exp=dexp.numpy(),
+                      n_samples=n.numpy(), z_surface=z.numpy())
+        planes.append((raw, pl))
+    g = cfg["g"]
+    origin = np.asarray(workloads.CENTER) - workloads.GRID_HALF
+    if inputs == "marcher":
+        b = sc.bounds
+        dens = oracle.bake(sc, g, workloads.GRID_HALF, origin, (b.min, b.max, b.unbounded))
+    else:
+        dens = workloads.density_grid(g, "cpu")[0].numpy()
+    return cams, planes, dens.reshape(g, g, g), origin
+
+
+def _native_libs():
+    """Shared objects of this repo mapped into the process (which code ran)."""
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")}
+    except OSError:
+        return None
+    return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT + os.sep))
+
+
+def probs_digest(p):
+    """sha256 of the fused probability grid (f64, C order): both arms print it."""
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(p, dtype=np.float64).tobytes()).hexdigest()
 
 
 def run_reference(args):
+    """The reference's own CPU path, unmodified: ``divas.segmenter.refine_mask``
+    for every view + ``divas.fusion.fuse(..., workers=nproc)`` (numba prange
+    over all host cores) + the ``probs >= 0.5`` threshold (ablation.py:109),
+    from ``baseline/_ref`` (pip-installed /root/reference/pkg).  Every step is
+    one full update of the whole grid: nothing is sampled or extrapolated.
+    Without ``baseline/_ref`` the oracle port (C, pthreads) runs the same full
+    update instead (``cpu_baseline.kind`` says which)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle
+    ncpu = os.cpu_count() or 1
+    have_ref = os.path.isdir(os.path.join(REF_DIR, "divas"))
+    if have_ref:
+        # before numba is first imported (divas/_nb.py caps it at 16 otherwise)
+        os.environ["NUMBA_NUM_THREADS"] = str(ncpu)
+        os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "divas_ref_numba_cache"))
+        sys.path.insert(0, REF_DIR)
+    t_fix = time.perf_counter()
+    cams, planes, dens, origin = _reference_fixture(args.config, args.inputs)
+    t_fix = time.perf_counter() - t_fix
+    g, nv = dens.shape[0], len(cams)
+    H, W = planes[0][0].shape
     import workloads
-    from paper_2601_04860_b200.fusion import FusionParams
-    import torch
-    # Fixture generation, outside the timed region (which is CPU-only): with a
-    # GPU the device marcher / bake make the inputs (bit-identical to the
-    # reference's render_view / bake_density_grid, tests/test_gpu_render.py);
-    # without one, the oracle's restatement of the same functions does.
-    if torch.cuda.is_available():
-        wl = workloads.make(args.config, device="cuda", source=args.inputs)
+    if have_ref:
+        from divas import fusion as F, segmenter as S
+        from divas.geometry import Camera, VoxelGrid
+        from divas.render import ViewGeometry
+        from divas.scene import DensityGrid
+        grid = VoxelGrid(g, workloads.GRID_HALF, origin)
+        dgrid = DensityGrid(grid, dens)
+        params = F.FusionParams()
+        views, raws = [], []
+        for cam, (raw, pl) in zip(cams, planes):
+            c = Camera(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height,
+                       cam.world_from_camera)
+            views.append(ViewGeometry(c, None, pl["d_min"], pl["d_max"], pl["d_exp"],
+                                      pl["n_samples"], pl["z_surface"]))
+            raws.append(S.ConfidenceMask(raw))
+
+        def update():
+            refined = [S.refine_mask(m, vg) for m, vg in zip(raws, views)]
+            og = F.fuse(grid, dgrid, list(zip(views, refined)), params, workers=ncpu)
+            return og.probs, og.probs >= 0.5
+
+        threads = ncpu
+        kind = "reference"
+        what = ("divas.segmenter.refine_mask x%d views + divas.fusion.fuse(workers=%d) + "
+                "probs >= 0.5, the unmodified reference (baseline/_ref, numba %s)")
+        import numba
+        what = what % (nv, ncpu, numba.__version__)
     else:
-        wl = workloads.make(args.config, device="cpu", source="analytic")
-        if args.inputs == "marcher":
-            _marcher_inputs_cpu(wl)
-    h = host_copy(wl)
-    pv = FusionParams().as_vector()
-    budget = max(0.5, min(args.cpu_budget_s / max(args.steps + args.warmup, 1), 4.0))
-    # one sample definition shared by every step
-    _t, det = oracle_sample(wl, h, pv, budget)
-    slabs = det["slabs"]
-    for _ in range(args.warmup):
-        oracle_sample(wl, h, pv, budget, slabs=slabs)
+        import oracle
+        from paper_2601_04860_b200.fusion import FusionParams
+        pv = FusionParams().as_vector()
+        threads = oracle.max_threads()
+        cams_a = np.stack([np.concatenate([c.rotation.reshape(9), c.position,
+                                           [c.fx, c.fy, c.cx, c.cy, float(c.width),
+                                            float(c.height)]]) for c in cams])
+        st = {k: np.stack([pl[k] for _r, pl in planes]) for k in planes[0][1]}
+        raw_all = np.stack([r for r, _pl in planes])
+        dflat = dens.reshape(-1)
+        dx = 2.0 * workloads.GRID_HALF / g
+
+        def update():
+            refined = np.stack([oracle.refine(raw_all[v], st["z_surface"][v], st["n_samples"][v])
+                                for v in range(nv)])
+            packed = (cams_a[:, :9].reshape(nv, 3, 3), cams_a[:, 9:12], cams_a[:, 12:18], refined,
+                      st["d_min"], st["d_max"], st["d_exp"], st["n_samples"],
+                      (st["n_samples"] > 0).astype(np.uint8))
+            r = oracle.fuse_packed(g, origin, dx, dflat, packed, pv, np.zeros(3), np.ones(3), 0,
+                                   early_out=False, nthreads=threads)
+            return r["p"], r["p"] >= 0.5
+
+        kind = "port"
+        what = (f"oracle (C restatement of segmenter.py:129-152 + fusion.py:410-509, every "
+                f"voxel-view pair projected), {threads} threads: baseline/_ref is not installed")
+    for _ in range(max(args.warmup, 1)):              # the first call JIT-compiles numba
+        update()
     times = []
+    probs = None
     for _ in range(args.steps):
-        t, _d = oracle_sample(wl, h, pv, budget, slabs=slabs)
-        times.append(t)
+        t0 = time.perf_counter()
+        probs, _occ = update()
+        times.append(time.perf_counter() - t0)
     ms = 1e3 * float(np.mean(times))
-    value = wl.updates() / (ms / 1e3)
-    sample = (f"refine of all {wl.nv} views + fuse of {len(slabs)}/{wl.g} ix-slabs "
-              f"(every voxel-view pair projected, as fusion.py:505-509), extrapolated to the "
-              f"full grid")
+    value = g ** 3 * nv / (ms / 1e3)
     line = {
         "impl": "reference", "metric": "voxel-view updates/s", "value": value,
         "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "latency_ms": ms, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": ms, "latency_ms": ms, "ms_min": 1e3 * min(times),
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_DESC[args.config], "grid": wl.g, "views": wl.nv,
-                   "width": wl.shape[2], "height": wl.shape[1],
-                   "inputs": INPUTS_DESC[args.inputs]},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": oracle.max_threads(),
-                         "kind": "port", "sample": sample},
+        "config": {"workload": CONFIG_DESC[args.config], "grid": g, "views": nv,
+                   "width": W, "height": H,
+                   "inputs": INPUTS_DESC[args.inputs].replace(
+                       "run on the device", "run by the oracle's C restatement on the host"),
+                   "step": "refine all views + fuse the whole grid + threshold, every step",
+                   "fixture_s": round(t_fix, 1)},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": kind,
+                         "sample": what + "; the full update every step (no extrapolation)",
+                         "cpu_count": ncpu},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "probs_sha256": probs_digest(probs),
+        "occupied": int((probs >= 0.5).sum()),
+        "native_so_loaded": _native_libs(),
     }
     print(json.dumps(line), flush=True)
 
@@ -589,6 +686,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     gated = int(Fuser.gated_count({"workspace": ws}).item())
     extra = {}
+    if world == 1:
+        # the timed step's grid, digested as the reference arm digests its own
+        extra["probs_sha256"] = probs_digest(probs.cpu().numpy())
+        extra["occupied"] = int((probs >= 0.5).sum().item())
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         h = host_copy(wl)

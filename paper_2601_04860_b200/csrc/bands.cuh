@@ -49,7 +49,9 @@ constexpr float kIneligible = -1e30f;
 // Bands: per view nty * ntx tile entries, then two 16-byte entries: the
 // view's {min, max} key (order-preserving u32, as the z keys) of tau32 over
 // the supporting pixels the pass saw, the count of flagged and of supporting
-// pixels; then {base tau32 bits (NaN: none), 0, 0, 0}.
+// pixels; then {base tau32 bits (NaN: none), min and max n_samples over the
+// supporting pixels, base n (0: none)}.  A supporting pixel is flagged when
+// its f64 tau differs from the base tau(n_min) (exact, not by the f32 key).
 __host__ __device__ inline int64_t band_view_stride(int nty, int ntx) {
     return (int64_t)nty * ntx + 2;
 }
@@ -69,7 +71,9 @@ static __global__ void band_init(double2 *__restrict__ bands, int nv, int nty, i
         e[2] = 0u;                                   // flagged supporting pixels
         e[3] = 0u;                                   // supporting pixels
         e[4] = 0x7fc00000u;                          // base tau: none yet
-        e[5] = e[6] = e[7] = 0u;
+        e[5] = 0xffffffffu;                          // n range of the supporting pixels
+        e[6] = 0u;
+        e[7] = 0u;                                   // base n: none yet
     }
 }
 
@@ -80,7 +84,7 @@ static __global__ void band_init(double2 *__restrict__ bands, int nv, int nty, i
 // returns the pixel's tau as f32 when it can support (m > 0.5), else
 // kIneligible.
 __device__ __forceinline__ float band_px(float m, int32_t n, float d, const BandParams &B,
-                                         double &lo, double &hi) {
+                                         double &lo, double &hi, double &t64) {
     if (m >= 0.5f && n > 0) {
         double b = B.beta * (double)n;
         if (b > B.bmax) b = B.bmax;
@@ -89,9 +93,15 @@ __device__ __forceinline__ float band_px(float m, int32_t n, float d, const Band
         const double mg = 1e-12 * (fabs(D) + t);
         lo = fmin(lo, D - t - mg);
         hi = fmax(hi, D + t + mg);
+        t64 = t;
         return m > 0.5f ? (float)t : kIneligible;
     }
     return kIneligible;
+}
+__device__ __forceinline__ float band_px(float m, int32_t n, float d, const BandParams &B,
+                                         double &lo, double &hi) {
+    double t64;
+    return band_px(m, n, d, B, lo, hi, t64);
 }
 
 // One thread per VEC-pixel column chunk and 8 rows; TPW = 8 / VEC threads form
@@ -118,16 +128,22 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
     // tau: with the n range known (refine keys), one tau(n) for all -> skip it
     bool write_b = true;
     float base = __int_as_float(0x7fc00000);         // tau(n_min); NaN without keys
+    double base64 = __longlong_as_double(0x7ff8000000000000LL);   // the same in f64
     if (minmax) {
         const uint32_t n0 = minmax[kKeys * v + 2], n1 = minmax[kKeys * v + 3];
-        double l0 = 0.0, h0 = 0.0;
+        double l0 = 0.0, h0 = 0.0, t1 = 0.0;
         write_b = n0 <= n1 && band_px(1.0f, (int32_t)n0, 0.0f, B, l0, h0) !=
                                   band_px(1.0f, (int32_t)n1, 0.0f, B, l0, h0);
-        if (n0 <= n1) base = band_px(1.0f, (int32_t)n0, 0.0f, B, l0, h0);
-        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-            reinterpret_cast<uint32_t *>(bands + (int64_t)v * band_view_stride(B.nty, B.ntx) +
-                                         (int64_t)B.nty * B.ntx)[4] = __float_as_uint(base);
+        if (n0 <= n1) base = band_px(1.0f, (int32_t)n0, 0.0f, B, l0, h0, t1);
+        if (n0 <= n1) base64 = t1;
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+            uint32_t *e = reinterpret_cast<uint32_t *>(bands + (int64_t)v * band_view_stride(B.nty, B.ntx) +
+                                                       (int64_t)B.nty * B.ntx);
+            e[4] = __float_as_uint(base);
+            e[7] = n0 <= n1 ? n0 : 0u;
+        }
     }
+    uint32_t nlo = 0xffffffffu, nhi = 0u;            // n range of the supporting pixels
     uint32_t cnt = 0;              // supporting pixels (low 16 bits), flagged ones (high)
     // ROI (optional): the view's tile-aligned window {x0, y0, x1, y1}; the
     // grid covers the largest window, blocks past this view's window idle
@@ -187,17 +203,20 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
             float2 a[VEC], b[VEC];
 #pragma unroll
             for (int k = 0; k < VEC; ++k) {
-                const float t32 = band_px(m[k], n[k], d[k], B, lo, hi);
+                double t64 = 0.0;
+                const float t32 = band_px(m[k], n[k], d[k], B, lo, hi, t64);
                 const bool sup = t32 >= 0.0f;
                 // every pixel flags when base is NaN (no refine keys): then the
                 // flag path is never chosen (nflag = nsup)
-                const bool flag = sup && !(t32 == base);
+                const bool flag = sup && !(t64 == base64);
                 cnt += sup ? (flag ? 0x10001u : 1u) : 0u;
                 a[k] = make_float2(flag ? -m[k] : m[k], sup ? d[k] : __int_as_float(0x7fc00000));
                 b[k] = make_float2(t32, __int_as_float(n[k]));
                 if (sup) {
                     tmin = min(tmin, tau_key(t32));
                     tmax = max(tmax, tau_key(t32));
+                    nlo = min(nlo, (uint32_t)n[k]);
+                    nhi = max(nhi, (uint32_t)n[k]);
                 }
             }
             if (VEC == 4) {
@@ -234,6 +253,8 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
         for (int o = 16; o > 0; o >>= 1) {
             tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
             tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+            nlo = min(nlo, __shfl_xor_sync(0xffffffffu, nlo, o));
+            nhi = max(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
             cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         }
         if ((threadIdx.x & 31) == 0) {
@@ -242,6 +263,8 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
             atomicMax(e + 1, tmax);
             atomicAdd(e + 2, cnt >> 16);
             atomicAdd(e + 3, cnt & 0xffffu);
+            atomicMin(e + 5, nlo);
+            atomicMax(e + 6, nhi);
         }
     }
 }

@@ -1129,6 +1129,87 @@ __device__ __forceinline__ bool scan_box(const float2 *__restrict__ rp, int wm, 
     return emin < Mg || (MODE == 1 && fmin_ < 0.0f);
 }
 
+// Exact f32 support interval of a thin candidate with one tau (MODE 0 / 1):
+// a record depth D (f32, widened exactly) supports x_d iff the reference's
+// f64 test |x_d - D| <= tau holds (fusion.py:361-367).  fl(x_d - D) is
+// monotone in D, so the f32 depths that pass form one interval [lo, hi]; its
+// ends lie within an ulp of fl32(x_d -+ tau) and are found by evaluating the
+// reference's own test on the neighbouring f32 values.  The scan then decides
+// each pixel with two f32 compares, exactly (NaN depth -- an ineligible
+// pixel -- fails both).  Returns false (the caller recounts in f64) when the
+// interval reaches non-positive depths or an end does not settle.
+__device__ __forceinline__ float f32_up(float f) {      // next f32 above f > 0
+    return __int_as_float(__float_as_int(f) + 1);
+}
+__device__ __forceinline__ float f32_down(float f) {    // next f32 below f > 0
+    return __int_as_float(__float_as_int(f) - 1);
+}
+__device__ __forceinline__ bool support_interval(double xd, double tau, float &lo, float &hi) {
+    // straight-line (no data-dependent loop: lanes must enter the scan
+    // together): fl32(x_d +- tau) is within an ulp of each end, so the end is
+    // one of its neighbours; the next neighbour outward must fail the test
+    auto ok = [&](float D) { return fabs(xd - (double)D) <= tau; };
+    const double a = xd - tau, b = xd + tau;
+    const float h0 = __double2float_rn(b), l0 = __double2float_rn(a);
+    const float hm = f32_down(h0), hp = f32_up(h0), hq = f32_up(hp);
+    const float lp = f32_up(l0), lm = f32_down(l0), lq = f32_down(lm);
+    const bool okhm = ok(hm), okh0 = ok(h0), okhp = ok(hp), okhq = ok(hq);
+    const bool oklp = ok(lp), okl0 = ok(l0), oklm = ok(lm), oklq = ok(lq);
+    hi = okhp ? hp : (okh0 ? h0 : hm);
+    lo = oklm ? lm : (okl0 ? l0 : lp);
+    // each side's candidates lie on its own side of x_d (there the test is
+    // monotone in D), the inner ones pass, the outer ones fail
+    return a > 1e-30 && b < 1e30 && lq > 0.0f && (double)hm > xd && (double)lp < xd && okhm &&
+           oklp && !okhq && !oklq;
+}
+
+// -1 when lo <= D <= hi, else 0 (NaN: 0), branch-free: one FSETP + one FSET
+__device__ __forceinline__ int in_mask(float D, float lo, float hi) {
+    int m;
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %1, %2;\n\tset.le.and.s32.f32 %0, %1, %3, p;\n\t}"
+        : "=r"(m) : "f"(D), "f"(lo), "f"(hi));
+    return m;
+}
+
+// Footprint scan with an exact interval (MODE 0: one tau per view; MODE 1:
+// the base tau, and a flagged record -- negative m, its tau differs -- makes
+// the item unsure).  Same row walk as scan_box.  Returns "unsure" (MODE 1
+// flags only).
+template <int MODE>
+__device__ __forceinline__ bool scan_exact(const float2 *__restrict__ rp, int wm, int bw, int bh,
+                                           float lo, float hi, int &sup, float &mmax) {
+    float fmin_ = 0.0f;
+    auto pix = [&](float2 r) {
+        mmax = fmaxf(mmax, fabsf(r.x));
+        sup -= in_mask(r.y, lo, hi);
+        if (MODE == 1) fmin_ = fminf(fmin_, r.x);
+    };
+    const int rem = bw & 3;
+    const int full = bw - rem;
+#pragma unroll 1
+    for (int y = 0; y < bh; ++y, rp += wm) {
+        int c = 0;
+#pragma unroll 1
+        for (; c < full; c += 4) {
+            const float2 *q = rp + c;
+            float2 r[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) r[j] = __ldg(q + j);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pix(r[j]);
+        }
+        const float2 *q = rp + c;
+        if (rem & 2) {
+            const float2 r0 = __ldg(q), r1 = __ldg(q + 1);
+            pix(r0);
+            pix(r1);
+            q += 2;
+        }
+        if (rem & 1) pix(__ldg(q));
+    }
+    return MODE == 1 && fmin_ < 0.0f;
+}
+
 // Corner projections + footprint scan of one queued thin candidate.
 __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, const FuseMaps &M,
                                           const Contrib &K, int view,
@@ -1175,12 +1256,35 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     int sup = 0;
     float mmax = 0.0f;
     bool unsure;
-    if (tk0 >= tk1) {   // one tau for every supporting pixel of the view (or none)
-        unsure = scan_box<0>(rp, C.wm, plane, bw, bh, xd32, __uint_as_float(tk0), Mg,
-                             sup, mmax);
-    } else if ((uint64_t)nflag * 32u <= nsup) {
+    const bool one_tau = tk0 >= tk1;                  // one tau for every supporting pixel
+    const bool few_flags = !one_tau && (uint64_t)nflag * 32u <= nsup;
+    float ilo = 0.0f, ihi = 0.0f;
+    bool exact_ok = false;
+    // the exact interval needs the f64 tau the reference uses: tau_thin(n)
+    // from the n range of the view's supporting pixels (one f64 tau when its
+    // ends agree), or the base n whose f64 tau every unflagged pixel shares
+    const uint32_t nlo = __ldg(te + 5), nhi = __ldg(te + 6), nbase = __ldg(te + 7);
+#ifndef DIVAS_EXACT_SCAN
+#define DIVAS_EXACT_SCAN 1
+#endif
+    const bool single = DIVAS_EXACT_SCAN &&
+                        (nlo > nhi || tau_thin(C, (int32_t)nlo) == tau_thin(C, (int32_t)nhi));
+    if (!DIVAS_EXACT_SCAN) {
+    } else if (single) {                                      // (no supporting pixel: any tau)
+        exact_ok = support_interval(xd, tau_thin(C, nlo > nhi ? 1 : (int32_t)nlo), ilo, ihi);
+    } else if (few_flags && nbase > 0) {
+        exact_ok = support_interval(xd, tau_thin(C, (int32_t)nbase), ilo, ihi);
+    }
+    if (exact_ok && single) {
+        unsure = scan_exact<0>(rp, C.wm, bw, bh, ilo, ihi, sup, mmax);
+    } else if (exact_ok) {
         // few supporting pixels differ from the base tau: scan with the base
         // tau, a flagged pixel (negative mask) sends the item to the recount
+        unsure = scan_exact<1>(rp, C.wm, bw, bh, ilo, ihi, sup, mmax);
+    } else if (one_tau) {
+        unsure = scan_box<0>(rp, C.wm, plane, bw, bh, xd32, __uint_as_float(tk0), Mg,
+                             sup, mmax);
+    } else if (few_flags) {
         unsure = scan_box<1>(rp, C.wm, plane, bw, bh, xd32, __uint_as_float(__ldg(te + 4)),
                              Mg, sup, mmax);
     } else {

@@ -12,7 +12,7 @@ import tempfile
 from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB = os.path.join(ROOT, "paper_2601_04860_b200", "_lib", "libdivas_b200.so")
+LIB = os.environ.get("SASS_LIB") or os.path.join(ROOT, "paper_2601_04860_b200", "_lib", "libdivas_b200.so")
 
 
 def line_map(kernel):
@@ -63,7 +63,7 @@ def main():
     tot = sum(v[0] for v in agg.values()) or 1
     tst = sum(v[1] for v in agg.values()) or 1
     srcs = {}
-    for (f, ln), (ex, st) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:40]:
+    for (f, ln), (ex, st) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:int(os.environ.get("TOP", "40"))]:
         path = os.path.join(ROOT, "paper_2601_04860_b200", "csrc", f)
         if f not in srcs and os.path.exists(path):
             srcs[f] = open(path).read().splitlines()

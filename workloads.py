@@ -147,15 +147,19 @@ def render_maps(cam, device="cpu"):
     xc = (ix + 0.5 - cam.cx) / cam.fx
     yc = (cam.cy - (iy + 0.5)) / cam.fy
     R = torch.tensor(cam.rotation, dtype=torch.float64, device=device)
+    # elementwise IEEE ops only (no matmul / norm kernels, whose FMA use and
+    # reduction order differ between devices): the same bits on the CPU and
+    # the GPU, so the reference arm (CPU) sees this arm's exact masks
     d = torch.stack([R[0, 0] * xc + R[0, 1] * yc - R[0, 2], R[1, 0] * xc + R[1, 1] * yc - R[1, 2],
                      R[2, 0] * xc + R[2, 1] * yc - R[2, 2]], dim=-1)
-    d = d / torch.linalg.norm(d, dim=-1, keepdim=True)
+    nrm = torch.sqrt(d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1] + d[..., 2] * d[..., 2])
+    d = d / nrm.unsqueeze(-1)
     o = torch.tensor(cam.position, dtype=torch.float64, device=device)
     inf = torch.full((h, w), float("inf"), dtype=torch.float64, device=device)
     # sphere (outer surface entry; hollow interior only matters past the cutoff)
-    oc = o - torch.tensor(CENTER, dtype=torch.float64, device=device)
-    b = d @ oc
-    disc = b * b - (oc @ oc - SPHERE_R ** 2)
+    oc = [float(cam.position[j]) - CENTER[j] for j in range(3)]
+    b = d[..., 0] * oc[0] + d[..., 1] * oc[1] + d[..., 2] * oc[2]
+    disc = b * b - ((oc[0] * oc[0] + oc[1] * oc[1] + oc[2] * oc[2]) - SPHERE_R ** 2)
     t_s = torch.where(disc >= 0, -b - torch.sqrt(disc.clamp(min=0)), inf)
     t_s = torch.where(t_s > NEAR, t_s, inf)
     t_best, obj = t_s, torch.where(torch.isfinite(t_s), 1, 0)
