@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="slab mode, N>1: occupancy all-gather fused into the fusion's stores "
                          "over NVLink (symmetric memory), or a separate NCCL all_gather")
+    ap.add_argument("--overlap", default="on", choices=["on", "off"],
+                    help="run the density gate on a side stream concurrently with the refine")
     ap.add_argument("--inputs", default="marcher", choices=["marcher", "analytic"],
                     help="view planes + density: the reference's ray marcher and bake run on "
                          "the device, bit-exact (default), or the analytic first hit")
@@ -555,10 +557,31 @@ def run_ours(args):
                                       [(H, W)] * nv, vox_range=(lo, hi))
     roi_frac = roi.fraction(H, W) if roi is not None else 1.0
 
-    def step(ev=None, check=False):
+    # the density gate (rho stream, zero fill of p / occupancy, slot list) does
+    # not depend on the refined masks: it runs on a side stream concurrently
+    # with the refine + band pass, and the pair / reduce launches wait for it
+    overlap = args.overlap == "on" and not views_mode
+    side = torch.cuda.Stream(dev) if overlap else None
+    gate_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
+                for _ in range(max(args.steps, 1))]
+
+    def step(ev=None, check=False, k=0):
         nonlocal ws, bands
         if ev is not None:
             ev[0].record(stream)
+        fkw = dict(probs=probs, occ=occ_buf if (peer is None or check) else None,
+                   vox_range=(lo, hi), aux=bands, max_gated=cap,
+                   occ_peers=peer.peers if peer is not None else None)
+        if overlap:
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                if ev is not None:
+                    gate_evs[k][0].record(side)
+                ws = fuser.run(wl.density, dv, workspace=ws, stream=side,
+                               steps=_native.STEP_GATE | _native.STEP_CLEAR_ALL,
+                               **fkw)["workspace"]
+                if ev is not None:
+                    gate_evs[k][1].record(side)
         if views_mode:
             if v1 > v0:
                 refine_bands_device(dv.raw_masks[v0:v1], dv.z_surface[v0:v1], dv.nsamps[v0:v1],
@@ -590,11 +613,14 @@ def run_ours(args):
             fuser.run(wl.density, dv, steps=pairs, view_range=(v0, max(v1, v0 + 1)), **kw)
             plan.exchange(ws, rank)
             out = fuser.run(wl.density, dv, steps=_native.STEP_REDUCE, **kw)
+        elif overlap:
+            stream.wait_stream(side)
+            fkw["aux"] = bands
+            out = fuser.run(wl.density, dv, workspace=ws, steps=_native.STEP_PAIRS |
+                            _native.STEP_REDUCE, view_range=(0, nv), **fkw)
         else:
-            out = fuser.run(wl.density, dv, probs=probs,
-                            occ=occ_buf if (peer is None or check) else None,
-                            vox_range=(lo, hi), workspace=ws, aux=bands, max_gated=cap,
-                            occ_peers=peer.peers if peer is not None else None)
+            fkw["aux"] = bands
+            out = fuser.run(wl.density, dv, workspace=ws, **fkw)
         ws = out["workspace"]
         if ev is not None:
             ev[2].record(stream)
@@ -644,12 +670,21 @@ def run_ours(args):
             dist.barrier()
         for k in range(K):
             flush.zero_()
-            step(evs[k])
+            step(evs[k], k=k)
         torch.cuda.synchronize()
         if dist_on:
             dist.barrier()
     t_ref = [a.elapsed_time(b) for a, b, _c, _d in evs]
-    t_fuse = [b.elapsed_time(c) for _a, b, c, _d in evs]
+    # fuse = the gate's own duration (side stream, concurrent with the refine)
+    # + pairs / reduce after both streams joined; without overlap one span
+    t_gate = [gate_evs[k][0].elapsed_time(gate_evs[k][1]) for k in range(K)] if overlap else None
+    if overlap:
+        t_fuse = []
+        for k, (a, b, c, _d) in enumerate(evs):
+            join = max(a.elapsed_time(b), a.elapsed_time(gate_evs[k][1]))
+            t_fuse.append(t_gate[k] + (a.elapsed_time(c) - join))
+    else:
+        t_fuse = [b.elapsed_time(c) for _a, b, c, _d in evs]
     t_gath = [c.elapsed_time(d) for _a, _b, c, d in evs]
     t_step = [a.elapsed_time(d) for a, _b, _c, d in evs]
     ms_local = float(np.mean(t_step))
@@ -660,6 +695,21 @@ def run_ours(args):
         ms = float(t.item())
     updates = g ** 3 * nv
     value = updates / (ms / 1e3)
+    overlapped = None
+    if overlap:
+        # the operators' own durations, without the gate / refine contention:
+        # K more steps with the overlap off (the roofline is quoted on these)
+        overlapped = {"refine_ms": float(np.mean(t_ref)), "fuse_ms": float(np.mean(t_fuse)),
+                      "gate_ms": float(np.mean(t_gate))}
+        overlap = False
+        torch.cuda.synchronize()
+        for k in range(K):
+            flush.zero_()
+            step(evs[k], k=k)
+        torch.cuda.synchronize()
+        t_ref = [a.elapsed_time(b) for a, b, _c, _d in evs]
+        t_fuse = [b.elapsed_time(c) for _a, b, c, _d in evs]
+        overlap = True
 
     # --- roofline of the dominant operator --------------------------------------
     peak, peak_kind = measured_peak()
@@ -722,8 +772,8 @@ def run_ours(args):
             extra["incremental"] = run_incremental(args, wl, params, dev, probs)
             extra["incremental"]["full_recompute_ms_for_comparison"] = ms
 
-    # refine: init, minmax, band_pass; fuse: gate_tiles, gate_scan, gate_emit, pairs, reduce
-    launches_per_step = 3 + 5
+    # refine: init, minmax, band_pass; fuse: gate_tiles, gate_scan, gate_emit, tile_cull, pairs, reduce
+    launches_per_step = 3 + 6
     line = {
         "metric": "voxel-view updates/s", "value": value, "unit": "updates/s",
         "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms,
@@ -733,6 +783,9 @@ def run_ours(args):
                    "width": W, "height": H,
                    "parallelism": (f"{args.shard} x{world}" if dist_on else "1 GPU"),
                    "slabs": slabs, "slab_policy": args.slabs,
+                   "overlap": ("density gate on a side stream, concurrent with refine + band pass "
+                               "in the timed steps; breakdown_ms / roofline from K more steps "
+                               "with the operators run back to back" if overlap else None),
                    "step": ("refine+aux(own views) + gate + bcast(gated list) + pairs(own views)"
                             " + all-gather(contributions) + reduce" if views_mode else
                             "refine+aux(all views; records in windows) + fuse(slab, threshold fused)"
@@ -749,6 +802,7 @@ def run_ours(args):
                    "inputs": INPUTS_DESC[args.inputs],
                    "params": "FusionParams() defaults"},
         "breakdown_ms": {"refine": refine_ms, "fuse": fuse_ms, "gather": float(np.mean(t_gath)),
+                         "timed_step_with_overlap": overlapped,
                          "broadcast_once": bcast_ms},
         "gated_voxels": gated,
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,

@@ -210,13 +210,30 @@ __device__ __forceinline__ BrickOrigin brick_origin(const BrickGrid &G, uint32_t
     return BrickOrigin{G.ix0 + (int64_t)bx * kBrick, (int64_t)by * kBrick, (int64_t)bz * kBrick};
 }
 
+// Slot order inside a brick (the order gate_emit lists gated voxels in):
+// quad j (0..1023; a quad = 4 voxels along iz) -> brick-local quad coordinates
+// (qx, qy, qz) in 0..15 x 0..15 x 0..3.  Consecutive runs are compact blocks:
+// 8 quads (a warp's 32 slots when all are gated) = 2 x 4 x 4 voxels, 64 quads
+// (a pair CTA's 256 slots) = 8 x 8 x 4 voxels, consecutive 64-quad tiles step
+// along iz.  Compact blocks keep a pair CTA's footprints overlapping (L1
+// reuse) and its bounding box small (tile_cull).
+__device__ __forceinline__ void brick_quad_xyz(int j, int &qx, int &qy, int &qz) {
+    const int T = j >> 6, u = j & 63;                 // 8x8x1-quad tile, quad in tile
+    const int w8 = u >> 3, v = u & 7;                 // 2x4-quad chunk, quad in chunk
+    qx = 8 * (T >> 3) + 2 * (w8 >> 1) + (v >> 2);
+    qy = 8 * ((T >> 2) & 1) + 4 * (w8 & 1) + (v & 3);
+    qz = T & 3;
+}
+
 __device__ __forceinline__ unsigned gate_brick_quad(const float *__restrict__ dens,
                                                     const FuseConst &C, const FuseOut &O,
                                                     const BrickOrigin &Bo, int j,
                                                     bool count_only, int64_t &base_out) {
-    const int64_t ix = Bo.ix + (j >> 6);
-    const int64_t iy = Bo.iy + ((j >> 2) & 15);
-    const int64_t iz = Bo.iz + 4 * (j & 3);
+    int qx, qy, qz;
+    brick_quad_xyz(j, qx, qy, qz);
+    const int64_t ix = Bo.ix + qx;
+    const int64_t iy = Bo.iy + qy;
+    const int64_t iz = Bo.iz + 4 * qz;
     const int64_t g = C.g;
     base_out = (ix * g + iy) * g + iz;
     if (ix >= g || iy >= g || iz >= g) return 0u;
@@ -385,11 +402,12 @@ gate_emit(const float *__restrict__ dens, FuseConst C, BrickGrid G,
                           Bo.iz + kBrick <= g && C.lo <= Bo.ix * gg &&
                           C.hi >= (Bo.ix + kBrick) * gg;
     const int t = (int)threadIdx.x;
-    const int64_t base0 = ((Bo.ix + (t >> 6)) * g + Bo.iy + ((t >> 2) & 15)) * g + Bo.iz + 4 * (t & 3);
 #pragma unroll
     for (int r = 0; r < kGateRounds; ++r) {
         if (interior) {
-            qbase[r] = base0 + (int64_t)r * (kGateThreads / 64) * gg;
+            int qx, qy, qz;
+            brick_quad_xyz(r * kGateThreads + t, qx, qy, qz);
+            qbase[r] = ((Bo.ix + qx) * g + Bo.iy + qy) * g + Bo.iz + 4 * qz;
             const float4 v = __ldg(reinterpret_cast<const float4 *>(dens + qbase[r]));
             bits[r] = (density_gate(v.x, C) ? 1u : 0u) | (density_gate(v.y, C) ? 2u : 0u) |
                       (density_gate(v.z, C) ? 4u : 0u) | (density_gate(v.w, C) ? 8u : 0u);
