@@ -1376,32 +1376,48 @@ __device__ __forceinline__ void pair_tile(const FuseConst &C, const Cam &k,
 // bounding box (convex, in front of the camera: inside the hull of its 8
 // corners' projections, padded by a pixel), and their x_d in the corners'
 // depth range (depth is affine), so when that range meets no band of the
-// covered tiles no pair can vote: the tile is skipped.  Run by warp 0;
-// bb = {min ix, iy, iz, max ix, iy, iz} of the tile's voxels.
-__device__ __forceinline__ bool tile_culled(const FuseConst &C, const Cam &k,
-                                            const FuseMaps &M, int view, const unsigned *bb) {
-    const int lane = threadIdx.x & 31;
-    double xc = 0.0, yc = 0.0, d = 1.0, sc = 0.0;
-    if (lane < 8) {
-        const double px = C.origin0 + (double)(bb[0] + (lane & 1 ? bb[3] - bb[0] + 1 : 0)) * C.dx;
-        const double py = C.origin1 + (double)(bb[1] + (lane & 2 ? bb[4] - bb[1] + 1 : 0)) * C.dx;
-        const double pz = C.origin2 + (double)(bb[2] + (lane & 4 ? bb[5] - bb[2] + 1 : 0)) * C.dx;
-        const double rx = px - k.p0, ry = py - k.p1, rz = pz - k.p2;
-        d = -(k.r[2] * rx + k.r[5] * ry + k.r[8] * rz);
-        xc = k.r[0] * rx + k.r[3] * ry + k.r[6] * rz;
-        yc = k.r[1] * rx + k.r[4] * ry + k.r[7] * rz;
-        sc = fabs(px) + fabs(py) + fabs(pz) + fabs(k.p0) + fabs(k.p1) + fabs(k.p2);
+// covered tiles no pair can vote: the tile is skipped.
+//
+// One warp tests four views at once: lanes 8s .. 8s+7 project the 8 corners
+// of bb = {min ix, iy, iz, max ix, iy, iz} into view v0 + s (a reciprocal
+// instead of the division: the pixel window is padded by a pixel and the
+// depth range by 1e-9 relative, far above its error), then the 32 lanes walk
+// each view's covered band tiles in turn.  cull[s] = the verdict for v0 + s.
+__device__ __forceinline__ void tile_culled4(const FuseConst &C, const double *__restrict__ cams,
+                                             const FuseMaps &M, int v0, int nviews,
+                                             const unsigned *bb, bool cull[4]) {
+    const int lane = threadIdx.x & 31, sub = lane >> 3, c = lane & 7;
+    const int vl = v0 + sub;
+    const bool has = vl < nviews;
+    double xc = 0.0, yc = 0.0, d = 1.0, sc = 0.0, fx = 1.0, fy = 1.0, cx = 0.0, cy = 0.0;
+    double W = 1.0, H = 1.0;
+    if (has) {
+        const double *k = cams + (int64_t)(C.view0 + vl) * kCamStride;
+        const double px = C.origin0 + (double)(bb[0] + (c & 1 ? bb[3] - bb[0] + 1 : 0)) * C.dx;
+        const double py = C.origin1 + (double)(bb[1] + (c & 2 ? bb[4] - bb[1] + 1 : 0)) * C.dx;
+        const double pz = C.origin2 + (double)(bb[2] + (c & 4 ? bb[5] - bb[2] + 1 : 0)) * C.dx;
+        const double p0 = __ldg(k + 9), p1 = __ldg(k + 10), p2 = __ldg(k + 11);
+        const double rx = px - p0, ry = py - p1, rz = pz - p2;
+        d = -(__ldg(k + 2) * rx + __ldg(k + 5) * ry + __ldg(k + 8) * rz);
+        xc = __ldg(k + 0) * rx + __ldg(k + 3) * ry + __ldg(k + 6) * rz;
+        yc = __ldg(k + 1) * rx + __ldg(k + 4) * ry + __ldg(k + 7) * rz;
+        sc = fabs(px) + fabs(py) + fabs(pz) + fabs(p0) + fabs(p1) + fabs(p2);
+        fx = __ldg(k + 12); fy = __ldg(k + 13); cx = __ldg(k + 14); cy = __ldg(k + 15);
+        W = __ldg(k + 16); H = __ldg(k + 17);
     }
     const double mg = 1e-9 * (sc + 1.0);
-    const bool behind = lane < 8 ? d < -mg : true;
-    const bool front = lane < 8 ? d > mg : true;
-    if (__all_sync(0xffffffffu, behind)) return true;       // every voxel centre is behind
-    if (!__all_sync(0xffffffffu, front)) return false;      // straddles the camera plane
-    double u = lane < 8 ? k.fx * (xc / d) + k.cx : 0.0;      // pixel coordinates
-    double v = lane < 8 ? k.cy - k.fy * (yc / d) : 0.0;
-    double umn = lane < 8 ? u : 1e300, umx = lane < 8 ? u : -1e300;
-    double vmn = lane < 8 ? v : 1e300, vmx = lane < 8 ? v : -1e300;
-    double dlo = lane < 8 ? d - mg : 1e300, dhi = lane < 8 ? d + mg : -1e300;
+    // every corner of the group behind / in front (8-lane groups: masks per group)
+    const unsigned gmask = 0xffu << (8 * sub);
+    const unsigned behind = __ballot_sync(0xffffffffu, !has || d < -mg) & gmask;
+    const unsigned front = __ballot_sync(0xffffffffu, has && d > mg) & gmask;
+    const bool all_behind = behind == gmask, all_front = front == gmask;
+    double u = 0.0, v = 0.0;
+    if (all_front && d > 1e-30 && d < 1e30) {
+        const double r = rcp_fast(d);
+        u = fx * (xc * r) + cx;
+        v = cy - fy * (yc * r);
+    }
+    double umn = u, umx = u, vmn = v, vmx = v, dlo = d - mg, dhi = d + mg;
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) {
         umn = dmin2(umn, __shfl_xor_sync(0xffffffffu, umn, o));
@@ -1411,37 +1427,52 @@ __device__ __forceinline__ bool tile_culled(const FuseConst &C, const Cam &k,
         dlo = dmin2(dlo, __shfl_xor_sync(0xffffffffu, dlo, o));
         dhi = dmax2(dhi, __shfl_xor_sync(0xffffffffu, dhi, o));
     }
-    umn = __shfl_sync(0xffffffffu, umn, 0); umx = __shfl_sync(0xffffffffu, umx, 0);
-    vmn = __shfl_sync(0xffffffffu, vmn, 0); vmx = __shfl_sync(0xffffffffu, vmx, 0);
-    dlo = __shfl_sync(0xffffffffu, dlo, 0); dhi = __shfl_sync(0xffffffffu, dhi, 0);
-    const double W = k.w, H = k.h;
-    if (!(umx > -2.0 && umn < W + 2.0 && vmx > -2.0 && vmn < H + 2.0)) {
+    // per view: 0 = test the band tiles, 1 = culled, 2 = keep
+    int state = 0, tx0 = 0, ty0 = 0, nx = 0, nt = 0;
+    if (!has || all_behind) {
+        state = 1;                                     // (no view / every centre behind)
+    } else if (!all_front) {
+        state = 2;                                     // straddles the camera plane
+    } else if (!(umx > -2.0 && umn < W + 2.0 && vmx > -2.0 && vmn < H + 2.0)) {
         // the projection misses the image: every centre is out of the frustum,
         // unless a NaN / inf slipped through (then do not skip)
-        return umx <= -2.0 || umn >= W + 2.0 || vmx <= -2.0 || vmn >= H + 2.0;
+        state = (umx <= -2.0 || umn >= W + 2.0 || vmx <= -2.0 || vmn >= H + 2.0) ? 1 : 2;
+    } else {
+        const int x0 = (int)fmax(floor(umn) - 1.0, 0.0), x1 = (int)fmin(floor(umx) + 1.0, W - 1.0);
+        const int y0 = (int)fmax(floor(vmn) - 1.0, 0.0), y1 = (int)fmin(floor(vmx) + 1.0, H - 1.0);
+        tx0 = x0 / kBandTile;
+        ty0 = y0 / kBandTile;
+        nx = min(x1 / kBandTile, C.ntx - 1) - tx0 + 1;
+        nt = nx * (min(y1 / kBandTile, C.nty - 1) - ty0 + 1);
+        if (nx < 1 || nt < 1 || nt > 256) state = 2;
     }
-    const int x0 = (int)fmax(floor(umn) - 1.0, 0.0), x1 = (int)fmin(floor(umx) + 1.0, W - 1.0);
-    const int y0 = (int)fmax(floor(vmn) - 1.0, 0.0), y1 = (int)fmin(floor(vmx) + 1.0, H - 1.0);
-    const int tx0 = x0 / kBandTile, tx1 = min(x1 / kBandTile, C.ntx - 1);
-    const int ty0 = y0 / kBandTile, ty1 = min(y1 / kBandTile, C.nty - 1);
-    const int nx = tx1 - tx0 + 1, nt = nx * (ty1 - ty0 + 1);
-    if (nx < 1 || nt < 1 || nt > 256) return false;
-    const double2 *bv = M.bands + (int64_t)view * band_view_stride(C.nty, C.ntx);
-    bool hit = false;
-    for (int i = lane; i < nt; i += 32) {
-        const int ty = ty0 + i / nx, tx = tx0 + i % nx;
-        const double2 b = __ldg(bv + (int64_t)ty * C.ntx + tx);
-        hit |= dhi >= b.x && dlo <= b.y;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {                       // the four views' band walks
+        const int st = __shfl_sync(0xffffffffu, state, 8 * s);
+        if (st != 0) { cull[s] = st == 1; continue; }
+        const int ntx = __shfl_sync(0xffffffffu, nx, 8 * s);
+        const int ntt = __shfl_sync(0xffffffffu, nt, 8 * s);
+        const int bx = __shfl_sync(0xffffffffu, tx0, 8 * s);
+        const int by = __shfl_sync(0xffffffffu, ty0, 8 * s);
+        const double lo_ = __shfl_sync(0xffffffffu, dlo, 8 * s);
+        const double hi_ = __shfl_sync(0xffffffffu, dhi, 8 * s);
+        const double2 *bv = M.bands + (int64_t)(C.view0 + v0 + s) * band_view_stride(C.nty, C.ntx);
+        bool hit = false;
+        for (int i = lane; i < ntt; i += 32) {
+            const int ty = by + i / ntx, tx = bx + i % ntx;
+            const double2 b = __ldg(bv + (int64_t)ty * C.ntx + tx);
+            hit |= hi_ >= b.x && lo_ <= b.y;
+        }
+        cull[s] = !__any_sync(0xffffffffu, hit);
     }
-    return !__any_sync(0xffffffffu, hit);
 }
 
 // Pre-pass of fuse_pairs: one CTA per tile of 256 slots; the bounding box of
-// the tile's voxels once, then each warp runs tile_culled for its share of the
-// views.  skip[(view - view0) * ntiles + tile] = 1: the pair CTA exits at once.
-// Tiles whose voxels spread over more than 32 voxels on an axis (a slot run
-// that wraps to another brick row) are never skipped (their rectangles would
-// cover too many band tiles to be worth testing).
+// the tile's voxels once, then each warp tests four views at a time
+// (tile_culled4).  skip[(view - view0) * ntiles + tile] = 1: the pair CTA
+// exits at once.  Tiles whose voxels spread over more than 32 voxels on an
+// axis (a slot run that wraps to another brick) are never skipped (their
+// rectangles would cover too many band tiles to be worth testing).
 __global__ void __launch_bounds__(kPairThreads)
 tile_cull(FuseConst C, const double *__restrict__ cams, FuseMaps M,
           const uint32_t *__restrict__ work, const WsHeader *__restrict__ hdr, int nviews,
@@ -1476,16 +1507,15 @@ tile_cull(FuseConst C, const double *__restrict__ cams, FuseMaps M,
     for (int i = 0; i < 6; ++i) bb[i] = s_bb[i];
     const bool compact = bb[3] - bb[0] < 32 && bb[4] - bb[1] < 32 && bb[5] - bb[2] < 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int v = warp; v < nviews; v += kPairThreads / 32) {
-        bool cull = false;
-        if (compact) {
-            Cam k;
-            load_cam(cams + (int64_t)(C.view0 + v) * kCamStride, k);
-            cull = tile_culled(C, k, M, C.view0 + v, bb);
-        }
-        if (lane == 0) {
-            skip[(int64_t)v * ntiles + blockIdx.x] = cull ? 1 : 0;
-            if (cull) fallback(C, DIVAS_FB_TILE_SKIP);
+    for (int v0 = 4 * warp; v0 < nviews; v0 += 4 * (kPairThreads / 32)) {
+        bool cull[4] = {false, false, false, false};
+        if (compact) tile_culled4(C, cams, M, v0, nviews, bb, cull);
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            if (lane == s && v0 + s < nviews) {
+                skip[(int64_t)(v0 + s) * ntiles + blockIdx.x] = cull[s] ? 1 : 0;
+                if (cull[s]) fallback(C, DIVAS_FB_TILE_SKIP);
+            }
         }
     }
 }
