@@ -98,6 +98,25 @@ __device__ __forceinline__ float band_px(float m, int32_t n, float d, const Band
     }
     return kIneligible;
 }
+// band_px with the tile hull in f32 and directed rounding (band_pass2): the
+// interval [D - tau(1 + 2^-52), D + tau(1 + 2^-52)] that can hold a
+// supporting x_d lies inside [RD(D - T), RU(D + T)], T = one f32 ulp above
+// RU(tau) -- a hull wider than the f64 one by about an f32 ulp, which the
+// band tests only ever read as a conservative bound.
+__device__ __forceinline__ float band_px32(float m, int32_t n, float d, const BandParams &B,
+                                           float &lo, float &hi, double &t64) {
+    if (m >= 0.5f && n > 0) {
+        double b = B.beta * (double)n;
+        if (b > B.bmax) b = B.bmax;
+        const double t = (2.0 * B.gamma + b) * B.dx;
+        const float T = __int_as_float(__float_as_int(__double2float_ru(t)) + 1);
+        lo = fminf(lo, __fsub_rd(d, T));
+        hi = fmaxf(hi, __fadd_ru(d, T));
+        t64 = t;
+        return m > 0.5f ? __double2float_rn(t) : kIneligible;
+    }
+    return kIneligible;
+}
 __device__ __forceinline__ float band_px(float m, int32_t n, float d, const BandParams &B,
                                          double &lo, double &hi) {
     double t64;
@@ -258,6 +277,173 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
             cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         }
         if ((threadIdx.x & 31) == 0) {
+            uint32_t *e = reinterpret_cast<uint32_t *>(bv + (int64_t)B.nty * B.ntx);
+            atomicMin(e, tmin);
+            atomicMax(e + 1, tmax);
+            atomicAdd(e + 2, cnt >> 16);
+            atomicAdd(e + 3, cnt & 0xffffu);
+            atomicMin(e + 5, nlo);
+            atomicMax(e + 6, nhi);
+        }
+    }
+}
+
+// Row-split variant of band_pass<4, *> (128-bit loads only): a thread owns a
+// 4-pixel chunk of TWO rows and issues all eight of its 16-byte loads (mask,
+// n, d_exp, z of both rows) before any arithmetic, so four times as many
+// threads keep loads in flight as in band_pass (8 rows per thread, one row of
+// loads at a time).  Lane = 8 * rq + c: rows 2 rq, 2 rq + 1 of the 8-row tile
+// band, chunk c of the warp's 32 pixels; a tile (8 x 8) is the 8 lanes
+// {c, c ^ 1} x rq, combined with three shuffles.  Same outputs as band_pass.
+constexpr int kBand2Warps = 4;
+constexpr int kBand2Rows = 4;          // 8-row tile bands per block (grid-stride in y)
+template <bool REFINE>
+__global__ void __launch_bounds__(32 * kBand2Warps)
+band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict__ z,
+           const int32_t *__restrict__ nsamp, const float *__restrict__ dexp,
+           float *__restrict__ refined, const uint32_t *__restrict__ minmax,
+           double2 *__restrict__ bands, float2 *__restrict__ records, int nv,
+           const int4 *__restrict__ roi = nullptr) {
+    static_assert(kBandTile == 8, "row-split band pass assumes 8x8 tiles");
+    const int v = nv - 1 - (int)blockIdx.z;          // reverse view order: L2 reuse of z / n
+    // the view's window and keys in one round trip (no dependent prologue loads)
+    const int4 w = roi ? __ldg(roi + v) : make_int4(0, 0, B.wm - 1, B.hm - 1);
+    const uint4 keys = minmax ? __ldg(reinterpret_cast<const uint4 *>(minmax) + v)
+                              : make_uint4(0xffffffffu, 0u, 0xffffffffu, 0u);
+    const int64_t plane = (int64_t)B.hm * B.wm;
+    const int64_t off = (int64_t)v * plane;
+    float2 *__restrict__ recA = records + 2 * off;
+    float2 *__restrict__ recB = recA + plane;
+    bool write_b = true;
+    float base = __int_as_float(0x7fc00000);
+    double base64 = __longlong_as_double(0x7ff8000000000000LL);
+    if (minmax) {
+        const uint32_t n0 = keys.z, n1 = keys.w;
+        double l0 = 0.0, h0 = 0.0, t1 = 0.0;
+        write_b = n0 <= n1 && band_px(1.0f, (int32_t)n0, 0.0f, B, l0, h0) !=
+                                  band_px(1.0f, (int32_t)n1, 0.0f, B, l0, h0);
+        if (n0 <= n1) base = band_px(1.0f, (int32_t)n0, 0.0f, B, l0, h0, t1);
+        if (n0 <= n1) base64 = t1;
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+            uint32_t *e = reinterpret_cast<uint32_t *>(bands + (int64_t)v * band_view_stride(B.nty, B.ntx) +
+                                                       (int64_t)B.nty * B.ntx);
+            e[4] = __float_as_uint(base);
+            e[7] = n0 <= n1 ? n0 : 0u;
+        }
+    }
+    const int rx0 = w.x, rx1 = min(w.z, B.wm - 1);
+    const int ty_first = w.y / kBandTile, ty_last = min(w.w, B.hm - 1) / kBandTile;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int rq = lane >> 3, c = lane & 7;
+    const int chunk = ((int)blockIdx.x * kBand2Warps + warp) * 8 + c;
+    const int x0 = rx0 + chunk * 4;
+    const bool active = x0 <= rx1 && x0 < B.wm;
+    bool any = false;
+    double lo_ref = 0.0, span = 0.0, rspan = 0.0;
+    if (REFINE) {
+        const uint32_t kmin = keys.x, kmax = keys.y;
+        any = kmin <= kmax;
+        lo_ref = any ? (double)key_f32(kmin) : 0.0;
+        const double hi_ref = any ? (double)key_f32(kmax) : 0.0;
+        span = hi_ref - lo_ref;
+        rspan = span > 0.0 ? 1.0 / span : 0.0;
+    }
+    uint32_t tmin = 0xffffffffu, tmax = 0u, nlo = 0xffffffffu, nhi = 0u, cnt = 0;
+    double2 *bv = bands + (int64_t)v * band_view_stride(B.nty, B.ntx);
+    // this block's tile bands: ty_first + blockIdx.y * kBand2Rows + i
+    float4 mm[2], dd[2], zz[2];
+    int4 nn[2];
+    bool ok0 = false, ok1 = false;
+    auto load = [&](int ty) {
+        const int row0 = ty * kBandTile + 2 * rq;
+        ok0 = active && ty <= ty_last && row0 < B.hm;
+        ok1 = active && ty <= ty_last && row0 + 1 < B.hm;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const bool okr = r ? ok1 : ok0;
+            const int64_t p = off + (int64_t)(row0 + r) * B.wm + x0;
+            mm[r] = okr ? __ldg(reinterpret_cast<const float4 *>(mask + p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            nn[r] = okr ? __ldg(reinterpret_cast<const int4 *>(nsamp + p)) : make_int4(0, 0, 0, 0);
+            dd[r] = okr ? __ldg(reinterpret_cast<const float4 *>(dexp + p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            zz[r] = (REFINE && okr) ? __ldg(reinterpret_cast<const float4 *>(z + p))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    const int tyb = ty_first + (int)blockIdx.y * kBand2Rows;
+    if (tyb > ty_last) return;
+    load(tyb);
+#pragma unroll 1
+    for (int i = 0; i < kBand2Rows; ++i) {
+        const int ty = tyb + i;
+        if (ty > ty_last) break;
+        const int row0 = ty * kBandTile + 2 * rq;
+        const bool c0 = ok0, c1 = ok1;
+        float4 cm[2] = {mm[0], mm[1]}, cd[2] = {dd[0], dd[1]}, cz[2] = {zz[0], zz[1]};
+        int4 cn[2] = {nn[0], nn[1]};
+        if (i + 1 < kBand2Rows) load(ty + 1);        // next band's loads in flight meanwhile
+        float lo = __int_as_float(0x7f800000);      // +inf
+        float hi = -lo;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            if (!(r ? c1 : c0)) continue;
+            const int64_t p = off + (int64_t)(row0 + r) * B.wm + x0;
+            float m[4] = {cm[r].x, cm[r].y, cm[r].z, cm[r].w};
+            const int32_t n[4] = {cn[r].x, cn[r].y, cn[r].z, cn[r].w};
+            const float d[4] = {cd[r].x, cd[r].y, cd[r].z, cd[r].w};
+            if (REFINE) {
+                const float zv[4] = {cz[r].x, cz[r].y, cz[r].z, cz[r].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    m[k] = refine_px_fast(m[k], zv[k], n[k], any, lo_ref, span, rspan);
+                if (refined)
+                    __stcs(reinterpret_cast<float4 *>(refined + p), make_float4(m[0], m[1], m[2], m[3]));
+            }
+            const int64_t q = p - off;
+            float2 a[4], b[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                double t64 = 0.0;
+                const float t32 = band_px32(m[k], n[k], d[k], B, lo, hi, t64);
+                const bool sup = t32 >= 0.0f;
+                const bool flag = sup && !(t64 == base64);
+                cnt += sup ? (flag ? 0x10001u : 1u) : 0u;
+                a[k] = make_float2(flag ? -m[k] : m[k], sup ? d[k] : __int_as_float(0x7fc00000));
+                b[k] = make_float2(t32, __int_as_float(n[k]));
+                if (sup) {
+                    tmin = min(tmin, tau_key(t32));
+                    tmax = max(tmax, tau_key(t32));
+                    nlo = min(nlo, (uint32_t)n[k]);
+                    nhi = max(nhi, (uint32_t)n[k]);
+                }
+            }
+            float4 *a4 = reinterpret_cast<float4 *>(recA + q);
+            a4[0] = make_float4(a[0].x, a[0].y, a[1].x, a[1].y);
+            a4[1] = make_float4(a[2].x, a[2].y, a[3].x, a[3].y);
+            if (write_b) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (a[k].y == a[k].y) recB[q + k] = b[k];
+            }
+        }
+        // the 8 lanes of a tile: chunk pair (xor 1) x row pairs (xor 8, 16)
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 8));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 8));
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 16));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 16));
+        if (active && rq == 0 && (c & 1) == 0)
+            bv[(int64_t)ty * B.ntx + x0 / kBandTile] = make_double2((double)lo, (double)hi);
+    }
+    if (__any_sync(0xffffffffu, cnt != 0)) {
+        for (int o = 16; o > 0; o >>= 1) {
+            tmin = min(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+            tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+            nlo = min(nlo, __shfl_xor_sync(0xffffffffu, nlo, o));
+            nhi = max(nhi, __shfl_xor_sync(0xffffffffu, nhi, o));
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+        if (lane == 0) {
             uint32_t *e = reinterpret_cast<uint32_t *>(bv + (int64_t)B.nty * B.ntx);
             atomicMin(e, tmin);
             atomicMax(e + 1, tmax);

@@ -48,6 +48,37 @@ __device__ __forceinline__ float refine_px(float m, float z, int32_t n, bool any
     return __double2float_rn(o);
 }
 
+// The same value without the f64 division on almost every pixel: zhat from
+// the view's reciprocal rspan = RN(1 / span), then the f32 rounding of the
+// clipped product is CERTIFIED.  For 0 <= z - lo <= span and |m| <= M the
+// approximate product is within 7.1 * 2^-53 * max(1, M) of the reference's
+// (three roundings of zhat, two of 1 - zhat, two of the product); when no f32
+// rounding boundary lies within E = 2^-48 * max(1, |m|) of it (4x slack) the
+// f32 result is the reference's.  Otherwise -- and for zero, subnormal or
+// out-of-range values -- refine_px's exact chain runs.
+__device__ __forceinline__ float refine_px_fast(float m, float z, int32_t n, bool any, double lo,
+                                                double span, double rspan) {
+    if (!(any && n > 0)) return 0.0f;                       // o = 0 -> clip -> +0
+    if (!(span > 0.0)) return refine_px(m, z, n, any, lo, span);
+    const double a = (double)z - lo;
+    if (!(a >= 0.0 && a < span)) return refine_px(m, z, n, any, lo, span);
+    // 0 <= zhat <= 1 here, so m * (1 - zhat) is m * (a non-negative number):
+    // a zero mask gives a zero of m's sign, which the clip keeps
+    if (m == 0.0f) return m;
+    double c = (double)m * (1.0 - a * rspan);
+    if (c < 0.0) c = 0.0;
+    if (c > 1.0) c = 1.0;
+    const float f = __double2float_rn(c);
+    if (f > 1.17549435e-38f && f < 3.0e38f) {
+        const double E = 3.552713678800501e-15 * fmax(1.0, fabs((double)m));   // 2^-48 max(1, |m|)
+        const double fd = (double)f;
+        const double up = (double)__int_as_float(__float_as_int(f) + 1);
+        const double dn = (double)__int_as_float(__float_as_int(f) - 1);
+        if (c + E < 0.5 * (fd + up) && c - E > 0.5 * (fd + dn)) return f;
+    }
+    return refine_px(m, z, n, any, lo, span);
+}
+
 void set_error(const char *fmt, ...);
 int check_launch(const char *what);
 

@@ -104,6 +104,7 @@ refine_apply(const float *__restrict__ mask, const float *__restrict__ z,
     const double lo = any ? (double)key_f32(kmin) : 0.0;
     const double hi = any ? (double)key_f32(kmax) : 0.0;
     const double span = hi - lo;
+    const double rspan = span > 0.0 ? 1.0 / span : 0.0;
     const int64_t off = (int64_t)v * plane;
     const int64_t nvec = plane / VEC;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
@@ -113,13 +114,13 @@ refine_apply(const float *__restrict__ mask, const float *__restrict__ z,
             const float4 zz = __ldg(reinterpret_cast<const float4 *>(z + off) + i);
             const int4 nn = __ldg(reinterpret_cast<const int4 *>(n + off) + i);
             float4 o;
-            o.x = refine_px(m.x, zz.x, nn.x, any, lo, span);
-            o.y = refine_px(m.y, zz.y, nn.y, any, lo, span);
-            o.z = refine_px(m.z, zz.z, nn.z, any, lo, span);
-            o.w = refine_px(m.w, zz.w, nn.w, any, lo, span);
+            o.x = refine_px_fast(m.x, zz.x, nn.x, any, lo, span, rspan);
+            o.y = refine_px_fast(m.y, zz.y, nn.y, any, lo, span, rspan);
+            o.z = refine_px_fast(m.z, zz.z, nn.z, any, lo, span, rspan);
+            o.w = refine_px_fast(m.w, zz.w, nn.w, any, lo, span, rspan);
             __stcs(reinterpret_cast<float4 *>(out + off) + i, o);
         } else {
-            out[off + i] = refine_px(mask[off + i], z[off + i], n[off + i], any, lo, span);
+            out[off + i] = refine_px_fast(mask[off + i], z[off + i], n[off + i], any, lo, span, rspan);
         }
     }
 }
@@ -215,10 +216,23 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
         // threads per block: enough 4-pixel chunks for the (window) width, in
         // warps, so narrow windows do not idle half of every block
         const int64_t chunks = gw / 4;
-        const int bt = (int)std::min<int64_t>(256, std::max<int64_t>(32, (chunks + 31) / 32 * 32));
-        dim3 bg((unsigned)((chunks + bt - 1) / bt), (unsigned)gty, (unsigned)nv);
-        band_pass<4, true><<<bg, bt, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, mm,
-                                             (double2 *)bands, (float2 *)records, nv, r4);
+#ifndef DIVAS_BAND_ROWSPLIT
+#define DIVAS_BAND_ROWSPLIT 1
+#endif
+        if (DIVAS_BAND_ROWSPLIT && kBandTile == 8) {
+            // row-split pass: 8 chunks per warp, kBand2Warps warps per block
+            const int64_t per = 8 * kBand2Warps;
+            dim3 bg((unsigned)((chunks + per - 1) / per),
+                    (unsigned)((gty + kBand2Rows - 1) / kBand2Rows), (unsigned)nv);
+            band_pass2<true><<<bg, 32 * kBand2Warps, 0, s>>>(B, mask, z_surface, n_samples, dexp,
+                                                              out, mm, (double2 *)bands,
+                                                              (float2 *)records, nv, r4);
+        } else {
+            const int bt = (int)std::min<int64_t>(256, std::max<int64_t>(32, (chunks + 31) / 32 * 32));
+            dim3 bg((unsigned)((chunks + bt - 1) / bt), (unsigned)gty, (unsigned)nv);
+            band_pass<4, true><<<bg, bt, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, mm,
+                                                 (double2 *)bands, (float2 *)records, nv, r4);
+        }
     } else {
         if (!keys) refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         dim3 bg((unsigned)((gw + 255) / 256), (unsigned)gty, (unsigned)nv);

@@ -11,7 +11,7 @@ timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline ${BENCH_ARGS
 python - <<'PY'
 import json
 d=json.loads(open("gpurun_out/q/bench.json").read().strip().splitlines()[-1])
-print("ms", round(d["ms_per_step"],4), "breakdown", {k: (round(v,4) if v is not None else None) for k,v in d["breakdown_ms"].items()}, "frac", round(d["roofline"]["frac"],3), "parity", d.get("parity"), "inc", {k: d["incremental"].get(k) for k in ("p50_ms","p99_ms","bit_exact_vs_full")} if d.get("incremental") else None, "e2e", d["e2e"]["ms_per_step"] if d.get("e2e") else None)
+print("ms", round(d["ms_per_step"],4), "breakdown", d["breakdown_ms"], "frac", round(d["roofline"]["frac"],3), "parity", d.get("parity"), "inc", {k: d["incremental"].get(k) for k in ("p50_ms","p99_ms","bit_exact_vs_full")} if d.get("incremental") else None, "e2e", d["e2e"]["ms_per_step"] if d.get("e2e") else None)
 PY
 if [ "${LAUNCHES:-1}" = "1" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k 'regex:fuse_|band_pass|refine_|gate_|tile_cull' --csv \
