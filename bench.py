@@ -786,6 +786,9 @@ def run_ours(args):
                    "overlap": ("density gate on a side stream, concurrent with refine + band pass "
                                "in the timed steps; breakdown_ms / roofline from K more steps "
                                "with the operators run back to back" if overlap else None),
+                   "refined_masks": ("the timed step refines into the scan records only (no "
+                                     "planar refined-mask plane is written; e2e's refine_and_fuse "
+                                     "writes and returns them)"),
                    "step": ("refine+aux(own views) + gate + bcast(gated list) + pairs(own views)"
                             " + all-gather(contributions) + reduce" if views_mode else
                             "refine+aux(all views; records in windows) + fuse(slab, threshold fused)"
@@ -835,48 +838,73 @@ def run_e2e(args, wl, params, dev):
         p.copy_(t)
         return p.numpy()
 
-    planes = {k: pinned(getattr(wl, k)) for k in
-              ("raw_masks", "z_surface", "dmins", "dmaxs", "dexps", "nsamps")}
-    grid = VoxelGrid(wl.g, workloads.GRID_HALF, wl.origin)
-    dens = DensityGrid(grid, pinned(wl.density).reshape(wl.g, wl.g, wl.g))
-    views = []
-    for v, c in enumerate(wl.cams):
-        cam = Camera(c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.world_from_camera)
-        vg = ViewGeometry(cam, None, planes["dmins"][v], planes["dmaxs"][v], planes["dexps"][v],
-                          planes["nsamps"][v], planes["z_surface"][v])
-        views.append((vg, ConfidenceMask(planes["raw_masks"][v])))
+    def pageable(t):
+        return t.cpu().numpy().copy()     # ordinary (pageable) numpy, as render_view returns
 
-    xfer = {}
+    def views_of(host):
+        planes = {k: host(getattr(wl, k)) for k in
+                  ("raw_masks", "z_surface", "dmins", "dmaxs", "dexps", "nsamps")}
+        grid = VoxelGrid(wl.g, workloads.GRID_HALF, wl.origin)
+        dens = DensityGrid(grid, host(wl.density).reshape(wl.g, wl.g, wl.g))
+        views = []
+        for v, c in enumerate(wl.cams):
+            cam = Camera(c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.world_from_camera)
+            vg = ViewGeometry(cam, None, planes["dmins"][v], planes["dmaxs"][v],
+                              planes["dexps"][v], planes["nsamps"][v], planes["z_surface"][v])
+            views.append((vg, ConfidenceMask(planes["raw_masks"][v])))
+        return grid, dens, views
 
-    def once():
-        return refine_and_fuse(grid, dens, views, params, transfer_stats=xfer)
+    def timed(host):
+        grid, dens, views = views_of(host)
+        xfer = {}
 
-    once()
-    torch.cuda.synchronize()
-    times = []
-    for _ in range(max(1, args.e2e_steps)):
-        og = refined = None               # the previous update's results are released
-        t0 = time.perf_counter()
-        og, refined = once()
-        times.append(time.perf_counter() - t0)
-    ms = 1e3 * float(np.median(times))
+        def once():
+            return refine_and_fuse(grid, dens, views, params, transfer_stats=xfer)
+
+        once()
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(max(1, args.e2e_steps)):
+            og = refined = None               # the previous update's results are released
+            t0 = time.perf_counter()
+            og, refined = once()
+            times.append(time.perf_counter() - t0)
+        return 1e3 * float(np.median(times)), xfer
+
+    ms, xfer = timed(pinned)
+    ms_pageable, _x = timed(pageable)
     h2d, d2h = xfer["h2d_bytes"], xfer["d2h_bytes"]   # counted by refine_and_fuse
     return {"value": wl.updates() / (ms / 1e3), "unit": "updates/s", "ms_per_step": ms,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "api": "refine_and_fuse(grid, density, [(ViewGeometry, raw ConfidenceMask)], params)"
                    " -> (OccupancyGrid, refined masks)",
-            "host_buffers": "pinned"}
+            "host_buffers": "pinned",
+            "pinned_ms": ms, "pageable_ms": ms_pageable,
+            "pageable_value": wl.updates() / (ms_pageable / 1e3)}
 
 
 def run_incremental(args, wl, params, dev, full_probs, updates=200):
-    """BASELINE C4: re-refine + re-fuse one view of the fused C3 state, cycling
-    over the views; per-update device latency (CUDA events) p50 / p99, and a
-    bit-exactness check of the final state against the full fusion."""
+    """BASELINE C4 on the fused C3 state, p50 / p99 device latency (CUDA events):
+
+    * replace: re-refine + re-fuse one view with a NEW raw mask (the view's
+      silhouette shifted by -1 / 0 / +1 px and scaled by 1 / 0.95 / 0.9 / 0.85,
+      cycling), 200 updates cycling over the views; the final state is checked
+      bit for bit against a full fusion of the final mask set;
+    * add: append one view from host numpy (upload of its six planes + refine +
+      pair evaluation + re-reduction), 50 times (the view is popped again
+      between repetitions, untimed); the state after the last add is checked
+      against the full fusion of the 32 views;
+    * overlay: project_grid_overlay of the fused grid onto a centroid-zoom view
+      (fusion.py:846-865), device-resident inputs, and the host API call."""
     import torch
 
     import workloads
-    from paper_2601_04860_b200 import DensityGrid, FusionSession, VoxelGrid
-    from paper_2601_04860_b200.fusion import pack_cameras
+    from paper_2601_04860_b200 import DensityGrid, FusionSession, VoxelGrid, ViewGeometry
+    from paper_2601_04860_b200.fusion import (DeviceViews, Fuser, pack_cameras,
+                                              project_grid_overlay,
+                                              project_grid_overlay_device)
+    from paper_2601_04860_b200.geometry import Camera
+    from paper_2601_04860_b200.segmenter import refine_bands_device
     nv, H, W = wl.shape
     grid = VoxelGrid(wl.g, workloads.GRID_HALF, wl.origin)
     dens = DensityGrid(grid, wl.density.cpu().numpy().reshape(wl.g, wl.g, wl.g))
@@ -890,24 +918,122 @@ def run_incremental(args, wl, params, dev, full_probs, updates=200):
     s._refine(0, nv)
     s._fuse(0, nv)
     torch.cuda.synchronize()
-    lat = []
+
+    def variant(i, k):
+        m = torch.roll(wl.raw_masks[i], shifts=(k % 3) - 1, dims=1)
+        return (m * (1.0 - 0.05 * (k % 4))).contiguous()
+
+    masks = {}                                # perturbed masks, made outside the timing
     warm = nv + 5          # every view's update once (its CUDA graph is captured) + 5
+    for k in range(updates + warm):
+        masks[k] = variant(k % nv, k)
+    final = wl.raw_masks.clone()
+    lat = []
     for k in range(updates + warm):
         i = k % nv
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        s.replace_mask_device(i, wl.raw_masks[i])
+        s.replace_mask_device(i, masks[k])
         e1.record()
         e1.synchronize()
+        final[i].copy_(masks[k])
         if k >= warm:
             lat.append(e0.elapsed_time(e1))
-    exact = bool(torch.equal(s.probs, full_probs))
+    # full fusion of the final mask set, from scratch
+    fp = params
+    dv = DeviceViews(torch.from_numpy(pack_cameras(wl.cams)).to(dev), torch.empty_like(final),
+                     wl.dmins, wl.dmaxs, wl.dexps, wl.nsamps, z_surface=wl.z_surface,
+                     raw_masks=final)
+    _m, aux = refine_bands_device(final, wl.z_surface, wl.nsamps, wl.dexps, fp, wl.dx,
+                                  out=dv.masks)
+    gr = type("G", (), {"resolution": wl.g, "origin": wl.origin, "voxel_size": lambda q=None: wl.dx})()
+    ref = Fuser(gr, fp).run(wl.density, dv, aux=aux)["probs"]
+    torch.cuda.synchronize()
+    exact_replace = bool(torch.equal(s.probs, ref))
+    changed = int((ref != full_probs).sum().item())
     lat = np.asarray(lat)
-    return {"config": "C4: re-refine + re-fuse 1 of 32 views of the fused C3 state, "
-                      f"{updates} updates cycling over the views",
-            "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
-            "mean_ms": float(lat.mean()), "bit_exact_vs_full": exact,
-            "full_recompute_ms_for_comparison": None}
+    rec = {"config": "C4: re-refine + re-fuse 1 of 32 views of the fused C3 state with a new "
+                     f"(shifted / scaled) raw mask, {updates} updates cycling over the views",
+           "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+           "mean_ms": float(lat.mean()), "bit_exact_vs_full": exact_replace,
+           "check": "final session state vs a from-scratch refine + fuse of the final mask set",
+           "voxels_changed_by_the_updates": changed,
+           "full_recompute_ms_for_comparison": None}
+    # -- add one view (host inputs) ------------------------------------------
+    for name, src in (("raw", wl.raw_masks),):
+        getattr(s, name)[:nv].copy_(src)
+    s.pop_view()
+    s._refine(0, nv - 1)
+    s.refuse()
+    torch.cuda.synchronize()
+    c = wl.cams[nv - 1]
+    host = {k: getattr(wl, k)[nv - 1].cpu().numpy().copy() for k in
+            ("raw_masks", "z_surface", "dmins", "dmaxs", "dexps", "nsamps")}
+    vg = ViewGeometry(Camera(c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.world_from_camera),
+                      None, host["dmins"], host["dmaxs"], host["dexps"], host["nsamps"],
+                      host["z_surface"])
+    from paper_2601_04860_b200 import ConfidenceMask
+    cm = ConfidenceMask(host["raw_masks"])
+    alat, hlat = [], []
+    reps = 50
+    for k in range(reps + 3):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        s.add_view(vg, cm)
+        e1.record()
+        e1.synchronize()
+        t1 = time.perf_counter()
+        if k >= 3:
+            alat.append(e0.elapsed_time(e1))
+            hlat.append(1e3 * (t1 - t0))
+        if k < reps + 2:
+            s.pop_view()
+    torch.cuda.synchronize()
+    exact_add = bool(torch.equal(s.probs, full_probs))
+    alat, hlat = np.asarray(alat), np.asarray(hlat)
+    rec["add_view"] = {"config": "C4: add 1 view (its six planes uploaded from pageable host "
+                                 "numpy, refined, its pairs evaluated, voxels re-reduced) to the "
+                                 f"fused 31-view state, {reps} repetitions",
+                       "p50_ms": float(np.percentile(alat, 50)),
+                       "p99_ms": float(np.percentile(alat, 99)),
+                       "host_p50_ms": float(np.percentile(hlat, 50)),
+                       "bit_exact_vs_full": exact_add}
+    # -- overlay onto the next centroid view -----------------------------------
+    i = nv - 1
+    cam = Camera(wl.cams[i].fx, wl.cams[i].fy, wl.cams[i].cx, wl.cams[i].cy, wl.cams[i].width,
+                 wl.cams[i].height, wl.cams[i].world_from_camera)
+    out = torch.empty((H, W), dtype=torch.uint8, device=dev)
+    olat = []
+    for k in range(23):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        project_grid_overlay_device(full_probs, grid, cam, wl.dmins[i], wl.dmaxs[i],
+                                    wl.nsamps[i], 0.5, out=out)
+        e1.record()
+        e1.synchronize()
+        if k >= 3:
+            olat.append(e0.elapsed_time(e1))
+    from paper_2601_04860_b200 import OccupancyGrid
+    og = OccupancyGrid(grid, full_probs.cpu().numpy().reshape(wl.g, wl.g, wl.g))
+    vgi = ViewGeometry(cam, None, wl.dmins[i].cpu().numpy(), wl.dmaxs[i].cpu().numpy(),
+                       wl.dexps[i].cpu().numpy(), wl.nsamps[i].cpu().numpy(),
+                       wl.z_surface[i].cpu().numpy())
+    project_grid_overlay(og, vgi)
+    t0 = time.perf_counter()
+    for _ in range(5):
+        mask = project_grid_overlay(og, vgi)
+    host_ms = 1e3 * (time.perf_counter() - t0) / 5
+    same = bool(np.array_equal(mask, out.cpu().numpy().astype(bool)))
+    rec["overlay"] = {"config": f"project_grid_overlay of the fused C3 grid onto view {i} "
+                                f"(centroid zoom, {W}x{H}), threshold 0.5",
+                      "device_p50_ms": float(np.percentile(olat, 50)),
+                      "api_ms": host_ms,
+                      "api": "project_grid_overlay(OccupancyGrid with host probs, ViewGeometry)"
+                             " -> bool (H, W): uploads the 134 MB grid every call",
+                      "device_equals_api": same, "pixels_on": int(mask.sum())}
+    return rec
 
 
 def main():

@@ -15,6 +15,7 @@ from .segmenter import (ConfidenceMask, ViewAux, ViewWindows, refine_bands_devic
                         refine_masks_device)
 from .fusion import (DeviceViews, FusionParams, FusionStats, Fuser, OccupancyGrid,
                      extract, extract_device, fuse, fuse_with_stats, project_grid_overlay,
+                     project_grid_overlay_device,
                      refine_and_fuse,
                      threshold, threshold_device)
 
@@ -32,6 +33,7 @@ __all__ = [
     "ConfidenceMask", "ViewAux", "ViewWindows", "refine_mask", "refine_masks", "refine_masks_device", "refine_bands_device",
     "DeviceViews", "FusionParams", "FusionStats", "Fuser", "OccupancyGrid",
     "fuse", "fuse_with_stats", "refine_and_fuse", "project_grid_overlay",
+    "project_grid_overlay_device",
     "threshold", "threshold_device", "extract", "extract_device", "FusionSession",
     "ThickPathDecision", "ThinPathDecision", "depth_gradient", "depth_weight", "thick_check",
     "thin_check",

@@ -861,28 +861,38 @@ def extract(probs, thr: float = 0.5):
 # overlay (fusion.py:846-865)
 # ---------------------------------------------------------------------------
 
+def project_grid_overlay_device(probs, grid, camera, d_min, d_max, n_samples,
+                                threshold: float = 0.5, bounds=None, out=None, stream=None):
+    """``project_grid_overlay`` on device-resident data: ``probs`` the fused
+    [G^3] f64 grid and the view's (H, W) d_min / d_max / n_samples as CUDA
+    tensors; returns the (H, W) uint8 overlay on the device (no host sync)."""
+    import ctypes
+    h, w = int(camera.height), int(camera.width)
+    if out is None:
+        out = empty((h, w), np.uint8, probs.device)
+    rec = pack_cameras([camera])[0]
+    bc, bh, unb = bounds_arrays(bounds)
+    D3 = ctypes.c_double * 3
+    origin = np.asarray(grid.origin, dtype=np.float64).reshape(3)
+    _native.check(_native.lib().divas_overlay(
+        rec.ctypes.data_as(ctypes.c_void_p), h, w, _native.ptr(d_min), _native.ptr(d_max),
+        _native.ptr(n_samples), _native.ptr(probs.contiguous()), int(grid.resolution),
+        D3(*origin), float(grid.voxel_size()), D3(*bc), D3(*bh), int(unb), float(threshold),
+        _native.ptr(out), _native.stream_handle(stream)), "divas_overlay")
+    return out
+
+
 def project_grid_overlay(ogrid: OccupancyGrid, view, threshold: float = 0.5,
                          bounds=None) -> np.ndarray:
-    """Binary (H, W) mask of pixels whose ray meets a voxel with p >= threshold."""
-    import ctypes
+    """Binary (H, W) mask of pixels whose ray meets a voxel with p >= threshold
+    (fusion.py:846-865)."""
     import torch
     dev = device()
-    cam = view.camera
-    h, w = int(cam.height), int(cam.width)
     probs = ogrid.probs
     p = probs if isinstance(probs, torch.Tensor) else as_device(probs, np.float64, dev)
     dmin = as_device(view.d_min, np.float32, dev)
     dmax = as_device(view.d_max, np.float32, dev)
     ns = as_device(view.n_samples, np.int32, dev)
-    out = empty((h, w), np.uint8, dev)
-    rec = pack_cameras([cam])[0]
-    bc, bh, unb = bounds_arrays(bounds)
-    D3 = ctypes.c_double * 3
-    grid = ogrid.grid
-    origin = np.asarray(grid.origin, dtype=np.float64).reshape(3)
-    _native.check(_native.lib().divas_overlay(
-        rec.ctypes.data_as(ctypes.c_void_p), h, w, _native.ptr(dmin), _native.ptr(dmax),
-        _native.ptr(ns), _native.ptr(p.contiguous()), int(grid.resolution), D3(*origin),
-        float(grid.voxel_size()), D3(*bc), D3(*bh), int(unb), float(threshold),
-        _native.ptr(out), _native.stream_handle()), "divas_overlay")
+    out = project_grid_overlay_device(p, ogrid.grid, view.camera, dmin, dmax, ns, threshold,
+                                      bounds)
     return out.cpu().numpy().astype(bool)

@@ -188,6 +188,24 @@ class FusionSession:
             self._graphs[key] = g
         g.replay()
 
+    def pop_view(self):
+        """Drop the last view: its contribution bits are cleared and the
+        value-sorted sums re-taken over the remaining views (bit-identical to
+        a fusion of the remaining view set)."""
+        if self.nv == 0:
+            raise IndexError("the session holds no view")
+        i = self.nv - 1
+        if self._fused:
+            out = self.fuser.run(self.density, self._views(), probs=self.probs, occ=self.occ,
+                                 workspace=self._ws, max_gated=self._cap, aux=self.aux,
+                                 nv_cap=self.max_views, view_range=(i, i + 1),
+                                 steps=_native.STEP_CLEAR_VIEWS | _native.STEP_REDUCE)
+            self._ws = out["workspace"]
+            self._out = out
+        self.nv -= 1
+        self.sizes.pop()
+        self._graphs.clear()
+
     def refuse(self):
         """Full recompute of the current view set (same result, for checking)."""
         self._fused = False
