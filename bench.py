@@ -73,6 +73,9 @@ def parse():
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="slab mode, N>1: occupancy all-gather fused into the fusion's stores "
                          "over NVLink (symmetric memory), or a separate NCCL all_gather")
+    ap.add_argument("--slab-config", default="C5", choices=["C5", "C3", "C2", "C1", "none"],
+                    help="N > 1 (or DIVAS_FORCE_DIST=1): also time the slab path at this config")
+    ap.add_argument("--slab-steps", type=int, default=5)
     ap.add_argument("--overlap", default="on", choices=["on", "off"],
                     help="run the density gate on a side stream concurrently with the refine")
     ap.add_argument("--inputs", default="marcher", choices=["marcher", "analytic"],
@@ -813,12 +816,128 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     line.update(extra)
+    if dist_on and not views_mode and args.slab_config != "none":
+        # the slab path at the north star's scaling configuration, beside the C3 headline
+        sub = run_slab_subrecord(args, args.slab_config, world, rank, dev,
+                                 steps=min(K, args.slab_steps), warmup=min(args.warmup, 3))
+        line["slab_scaling"] = sub
     if dist_on:
         dist.barrier()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist_on:
         dist.destroy_process_group()
+
+
+def run_slab_subrecord(args, config, world, rank, dev, steps, warmup):
+    """North star's slab-scaling evidence at one more configuration (C5:
+    512^3 x 128 views at 1920x1080 by default): rank 0 builds the view set, NCCL
+    broadcasts it once, every rank takes the z min/max pass of its block of
+    views (keys all-gathered), builds scan records in its slab's windows,
+    fuses its work-balanced axis-0 slab and the occupancy slabs are
+    all-gathered (NCCL).  Per-rank device times (CUDA events), the step as the
+    max over ranks, and the gated-work balance."""
+    import torch
+    import torch.distributed as dist
+
+    import workloads
+    from paper_2601_04860_b200 import sharding
+    from paper_2601_04860_b200.fusion import DeviceViews, FusionParams, Fuser, pack_cameras
+    from paper_2601_04860_b200.segmenter import refine_bands_device, refine_minmax_device
+    params = FusionParams()
+    pv = params.as_vector()
+    meta = [None]
+    wl = None
+    if rank == 0:
+        wl = workloads.make(config, device=dev, source=args.inputs)
+        meta = [dict(nv=wl.nv, h=wl.shape[1], w=wl.shape[2], g=wl.g, cams=wl.cams,
+                     origin=wl.origin, dx=wl.dx)]
+    dist.broadcast_object_list(meta, src=0)
+    m = meta[0]
+    nv, H, W, g = m["nv"], m["h"], m["w"], m["g"]
+    if rank != 0:
+        e = lambda dt: torch.empty((nv, H, W), dtype=dt, device=dev)  # noqa: E731
+        wl = workloads.Workload(config, g, m["origin"], m["dx"],
+                                torch.empty(g ** 3, dtype=torch.float32, device=dev), m["cams"],
+                                e(torch.float32), e(torch.float32), e(torch.float32),
+                                e(torch.float32), e(torch.float32), e(torch.int32))
+    cams_t = torch.from_numpy(pack_cameras(wl.cams)).to(dev)
+    dv = DeviceViews(cams_t, torch.empty_like(wl.raw_masks), wl.dmins, wl.dmaxs, wl.dexps,
+                     wl.nsamps, z_surface=wl.z_surface, raw_masks=wl.raw_masks)
+    torch.cuda.synchronize()
+    dist.barrier()
+    b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b0.record()
+    sharding.broadcast_views(dv, src=0)
+    dist.broadcast(wl.density, src=0)
+    b1.record()
+    torch.cuda.synchronize()
+    bcast_ms = b0.elapsed_time(b1)
+    slabs = sharding.balanced_slabs(sharding.slice_weights(wl.density.reshape(g, g, g), pv, nv),
+                                    world)
+    lo, hi = sharding.slab_voxel_range(slabs[rank], g)
+    grid = type("G", (), {"resolution": g, "origin": wl.origin, "voxel_size": lambda s=None: wl.dx})()
+    fuser = Fuser(grid, params)
+    cap = fuser.capacity(wl.density, lo, hi)
+    roi = sharding.slab_view_rois(wl.density, pv, g, wl.origin, wl.dx, cams_t.cpu().numpy(),
+                                  [(H, W)] * nv, vox_range=(lo, hi))
+    blocks, rows = sharding.view_blocks(nv, world)
+    k_mine = torch.zeros((rows, 4), dtype=torch.int32, device=dev)
+    k_all = torch.zeros((world * rows, 4), dtype=torch.int32, device=dev)
+    probs = torch.empty(g ** 3, dtype=torch.float64, device=dev)
+    occ = torch.empty(g ** 3, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    state = {"ws": None, "bands": None}
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record()
+        v0, v1 = blocks[rank]
+        if v1 > v0:
+            refine_minmax_device(dv.z_surface[v0:v1], dv.nsamps[v0:v1], keys=k_mine[:v1 - v0])
+        dist.all_gather_into_tensor(k_all, k_mine)
+        _m, state["bands"] = refine_bands_device(dv.raw_masks, dv.z_surface, dv.nsamps, dv.dexps,
+                                                 params, wl.dx, aux=state["bands"], planar=False,
+                                                 roi=roi, keys=k_all[:nv])
+        if ev is not None:
+            ev[1].record()
+        out = fuser.run(wl.density, dv, probs=probs, occ=occ, vox_range=(lo, hi),
+                        workspace=state["ws"], aux=state["bands"], max_gated=cap)
+        state["ws"] = out["workspace"]
+        if ev is not None:
+            ev[2].record()
+        full = sharding.gather_occupancy(occ[lo:hi], slabs, g, rank)
+        if ev is not None:
+            ev[3].record()
+        return full
+
+    for _ in range(max(warmup, 2)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    for k in range(steps):
+        flush.zero_()
+        step(evs[k])
+    torch.cuda.synchronize()
+    dist.barrier()
+    mine = {"rank": rank, "slab": list(slabs[rank]), "gated_voxels": int(cap),
+            "refine_ms": float(np.mean([a.elapsed_time(b) for a, b, _c, _d in evs])),
+            "fuse_ms": float(np.mean([b.elapsed_time(c) for _a, b, c, _d in evs])),
+            "gather_ms": float(np.mean([c.elapsed_time(d) for _a, _b, c, d in evs])),
+            "step_ms": float(np.mean([a.elapsed_time(d) for a, _b, _c, d in evs])),
+            "windows_fraction": float(roi.fraction(H, W))}
+    allr = [None] * world
+    dist.all_gather_object(allr, mine)
+    step_ms = max(r["step_ms"] for r in allr)
+    work = np.asarray([r["gated_voxels"] for r in allr], dtype=np.float64)
+    del flush
+    return {"config": CONFIG_DESC[config], "n_gpus": world, "steps": steps, "slabs": slabs,
+            "step_ms": step_ms, "value": g ** 3 * nv / (step_ms / 1e3), "unit": "updates/s",
+            "broadcast_once_ms": bcast_ms,
+            "gated_balance_max_over_mean": float(work.max() / work.mean()) if work.mean() else None,
+            "gather": "nccl all_gather of the slab occupancy bytes", "per_rank": allr}
 
 
 def run_e2e(args, wl, params, dev):
