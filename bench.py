@@ -563,6 +563,12 @@ def run_ours(args):
     # the density gate (rho stream, zero fill of p / occupancy, slot list) does
     # not depend on the refined masks: it runs on a side stream concurrently
     # with the refine + band pass, and the pair / reduce launches wait for it
+    # stream plan of the timed step (bit-identical to the one-call fusion):
+    #   main : refine + band pass -> [gate done] tile cull + pairs + reduce
+    #   side : density gate (rho stream, zero fill of p / occupancy, slot list),
+    #          beside the refine
+    # (measured alternative, slower: the zero fill split off (STEP_ZERO) onto a
+    # third stream beside the pair kernel -- it displaces pair CTAs)
     overlap = args.overlap == "on" and not views_mode
     side = torch.cuda.Stream(dev) if overlap else None
     gate_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -682,6 +688,7 @@ def run_ours(args):
     # + pairs / reduce after both streams joined; without overlap one span
     t_gate = [gate_evs[k][0].elapsed_time(gate_evs[k][1]) for k in range(K)] if overlap else None
     if overlap:
+        # gate (side stream) + pairs / reduce after the gate joined
         t_fuse = []
         for k, (a, b, c, _d) in enumerate(evs):
             join = max(a.elapsed_time(b), a.elapsed_time(gate_evs[k][1]))

@@ -131,6 +131,14 @@ int divas_refine_bands_roi(int32_t nv, int64_t hm, int64_t wm,
 #define DIVAS_STEP_CLEAR_VIEWS 4  /* zero the bits of views [view_lo, view_hi) */
 #define DIVAS_STEP_PAIRS       8  /* evaluate views [view_lo, view_hi)          */
 #define DIVAS_STEP_REDUCE     16  /* value-sorted sums over all nv views -> p  */
+#define DIVAS_STEP_ZERO       32  /* only the zero fill of the outputs on
+                                     [lo, hi) (p, votes, sums, occupancy, peer
+                                     buffers): with GATE_KEEP below, the dense
+                                     fill can run on another stream, e.g.
+                                     beside the compute-bound PAIRS step      */
+#define DIVAS_STEP_GATE_KEEP  64  /* with GATE: build the gated-voxel list but
+                                     leave the outputs untouched (a ZERO step
+                                     must precede REDUCE)                     */
 #define DIVAS_FUSE_FULL        0  /* = GATE | CLEAR_ALL | PAIRS(all) | REDUCE  */
 #define DIVAS_FUSE_INCREMENTAL (DIVAS_STEP_CLEAR_VIEWS | DIVAS_STEP_PAIRS | DIVAS_STEP_REDUCE)
 /* Steps without GATE reuse the gated list, and steps without PAIRS the

@@ -78,6 +78,7 @@ NFALLBACK = 8
 
 FUSE_FULL = 0
 STEP_GATE, STEP_CLEAR_ALL, STEP_CLEAR_VIEWS, STEP_PAIRS, STEP_REDUCE = 1, 2, 4, 8, 16
+STEP_ZERO, STEP_GATE_KEEP = 32, 64
 FUSE_INCREMENTAL = STEP_CLEAR_VIEWS | STEP_PAIRS | STEP_REDUCE
 
 

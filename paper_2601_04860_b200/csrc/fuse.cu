@@ -267,6 +267,7 @@ constexpr int kGateRounds = 4;                     // quads per thread per 16^3 
 constexpr int kGateTile = 4 * kGateRounds * kGateThreads;   // 4096 = 16^3
 constexpr int64_t kGateTileMax = (1LL << 32) / kGateTile;   // tiles of any u32 voxel range
 
+template <bool ZERO>
 __global__ void __launch_bounds__(kGateThreads)
 gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
            uint32_t *__restrict__ tiles) {
@@ -287,11 +288,11 @@ gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
 #pragma unroll
         for (int r = 0; r < kGateRounds; ++r, base += (kGateThreads / 64) * gg) {
             const float4 v = __ldg(reinterpret_cast<const float4 *>(dens + base));
-            if (O.probs) {
+            if (ZERO && O.probs) {
                 __stcs(reinterpret_cast<double2 *>(O.probs + base), z2);
                 __stcs(reinterpret_cast<double2 *>(O.probs + base) + 1, z2);
             }
-            if (O.n_thick || O.n_thin || O.sw || O.smw || O.st) {   // stats outputs (rare)
+            if (ZERO && (O.n_thick || O.n_thin || O.sw || O.smw || O.st)) {   // stats (rare)
                 if (O.n_thick) *reinterpret_cast<int4 *>(O.n_thick + base) = make_int4(0, 0, 0, 0);
                 if (O.n_thin) *reinterpret_cast<int4 *>(O.n_thin + base) = make_int4(0, 0, 0, 0);
                 double *sums[3] = {O.sw, O.smw, O.st};
@@ -302,9 +303,10 @@ gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
                     }
             }
             const uchar4 o4 = make_uchar4(occ0, occ0, occ0, occ0);
-            if (O.occ) *reinterpret_cast<uchar4 *>(O.occ + base) = o4;
-            for (int p = 0; p < O.n_peers; ++p)
-                *reinterpret_cast<uchar4 *>(O.occ_peers[p] + base) = o4;
+            if (ZERO && O.occ) *reinterpret_cast<uchar4 *>(O.occ + base) = o4;
+            if (ZERO)
+                for (int p = 0; p < O.n_peers; ++p)
+                    *reinterpret_cast<uchar4 *>(O.occ_peers[p] + base) = o4;
             cnt += (int)density_gate(v.x, C) + (int)density_gate(v.y, C) +
                    (int)density_gate(v.z, C) + (int)density_gate(v.w, C);
         }
@@ -312,7 +314,7 @@ gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
 #pragma unroll
         for (int r = 0; r < kGateRounds; ++r)
             cnt += __popc(gate_brick_quad(dens, C, O, Bo, r * kGateThreads + (int)threadIdx.x,
-                                          false, base));
+                                          !ZERO, base));
     }
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = cnt;
@@ -450,6 +452,59 @@ gate_emit(const float *__restrict__ dens, FuseConst C, BrickGrid G,
             if (pos < C.cap) work[pos] = (uint32_t)(base + k);
             ++pos;
         }
+    }
+}
+
+// Zero fill of the outputs on [lo, hi) alone (DIVAS_STEP_ZERO): p (f64) and
+// the optional votes / sums / occupancy / peer buffers, 16-byte streaming
+// stores over aligned 16-voxel groups, scalar stores at the range ends.  The
+// exact value every voxel outside the density gate keeps (p = 0, occupancy
+// 0 >= occ_thr).
+__global__ void __launch_bounds__(256)
+fuse_zero(FuseConst C, FuseOut O) {
+    const uint8_t occ0 = (0.0 >= C.occ_thr) ? 1 : 0;
+    const int64_t a = (C.lo + 15) & ~(int64_t)15, b = C.hi & ~(int64_t)15;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    auto scalar = [&](int64_t i) {
+        if (O.probs) O.probs[i] = 0.0;
+        if (O.n_thick) O.n_thick[i] = 0;
+        if (O.n_thin) O.n_thin[i] = 0;
+        if (O.sw) O.sw[i] = 0.0;
+        if (O.smw) O.smw[i] = 0.0;
+        if (O.st) O.st[i] = 0.0;
+        if (O.occ) O.occ[i] = occ0;
+        for (int p = 0; p < O.n_peers; ++p) O.occ_peers[p][i] = occ0;
+    };
+    if (b <= a) {                                   // tiny range: scalar only
+        for (int64_t i = C.lo + tid; i < C.hi; i += nth) scalar(i);
+        return;
+    }
+    for (int64_t i = C.lo + tid; i < a; i += nth) scalar(i);
+    for (int64_t i = b + tid; i < C.hi; i += nth) scalar(i);
+    const double2 z2 = make_double2(0.0, 0.0);
+    const int4 zi = make_int4(0, 0, 0, 0);
+    const uint32_t o1 = occ0 * 0x01010101u;
+    const uint4 o16 = make_uint4(o1, o1, o1, o1);
+    for (int64_t g = a / 16 + tid; g < b / 16; g += nth) {      // 16 voxels per thread
+        const int64_t i = g * 16;
+        if (O.probs) {
+            double2 *q = reinterpret_cast<double2 *>(O.probs + i);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) __stcs(q + k, z2);
+        }
+        if (O.n_thick || O.n_thin || O.sw || O.smw || O.st) {
+            int32_t *iv[2] = {O.n_thick, O.n_thin};
+            for (int s = 0; s < 2; ++s)
+                if (iv[s])
+                    for (int k = 0; k < 4; ++k) reinterpret_cast<int4 *>(iv[s] + i)[k] = zi;
+            double *dv[3] = {O.sw, O.smw, O.st};
+            for (int s = 0; s < 3; ++s)
+                if (dv[s])
+                    for (int k = 0; k < 8; ++k) reinterpret_cast<double2 *>(dv[s] + i)[k] = z2;
+        }
+        if (O.occ) *reinterpret_cast<uint4 *>(O.occ + i) = o16;
+        for (int p = 0; p < O.n_peers; ++p) *reinterpret_cast<uint4 *>(O.occ_peers[p] + i) = o16;
     }
 }
 
@@ -1950,7 +2005,7 @@ static void launch_gate_count(const FuseConst &C, const float *dens, WsHeader *h
 // 256 slots are spatially adjacent voxels (their footprints overlap: L1 reuse)
 // and the slot order is reproducible.
 static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O, uint32_t *work,
-                        WsHeader *hdr, uint32_t *tiles, cudaStream_t s) {
+                        WsHeader *hdr, uint32_t *tiles, bool zero, cudaStream_t s) {
     const int64_t g = C.g, gg = g * g;
     BrickGrid G;
     G.ix0 = C.lo / gg;
@@ -1958,7 +2013,8 @@ static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O,
     G.nbx = (int)((ix1 - G.ix0 + kBrick - 1) / kBrick);
     G.nby = G.nbz = (int)((g + kBrick - 1) / kBrick);
     const int64_t ntiles = (int64_t)G.nbx * G.nby * G.nbz;
-    gate_tiles<<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, O, G, tiles);
+    if (zero) gate_tiles<true><<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, O, G, tiles);
+    else gate_tiles<false><<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, O, G, tiles);
     gate_scan<<<1, 1024, 0, s>>>(tiles, ntiles, C.cap, hdr);
     gate_emit<<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, G, tiles, ntiles, hdr, work);
 }
@@ -2069,7 +2125,11 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     const int steps = a->mode == DIVAS_FUSE_FULL
                           ? (DIVAS_STEP_GATE | DIVAS_STEP_CLEAR_ALL | DIVAS_STEP_PAIRS | DIVAS_STEP_REDUCE)
                           : a->mode;
-    if (steps & ~31) { set_error("divas_fuse: bad mode %d", a->mode); return DIVAS_EINVAL; }
+    if (steps & ~127) { set_error("divas_fuse: bad mode %d", a->mode); return DIVAS_EINVAL; }
+    if ((steps & DIVAS_STEP_ZERO) && !a->probs) {
+        set_error("divas_fuse: the ZERO step needs the output grid");
+        return DIVAS_EINVAL;
+    }
     int v0 = 0, v1 = a->nv;
     if (a->mode != DIVAS_FUSE_FULL && (steps & (DIVAS_STEP_PAIRS | DIVAS_STEP_CLEAR_VIEWS))) {
         v0 = a->view_lo; v1 = a->view_hi;
@@ -2105,10 +2165,23 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         M.rec = rec;
         M.bands = bands;
     }
+    if (steps & DIVAS_STEP_ZERO) {
+        const int64_t groups = (a->vox_hi - a->vox_lo) / 16 + 1;
+        // (blocks per SM: an experiment knob for running the fill beside the
+        // pair kernel, which holds every register of an SM)
+#ifndef DIVAS_ZERO_BLOCKS_PER_SM
+#define DIVAS_ZERO_BLOCKS_PER_SM 8
+#endif
+        const int64_t blocks = std::min<int64_t>((groups + 255) / 256,
+                                                 (int64_t)sm_count() * DIVAS_ZERO_BLOCKS_PER_SM);
+        fuse_zero<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(C, O);
+        if ((rc = check_launch("divas_fuse(zero)"))) return rc;
+    }
     if (steps & DIVAS_STEP_GATE) {
         if (cudaMemsetAsync(hdr, 0, sizeof(WsHeader), s) != cudaSuccess)
             return check_launch("divas_fuse(memset)");
-        launch_gate(C, a->density, O, work, hdr, (uint32_t *)(ws + L.gtiles), s);
+        launch_gate(C, a->density, O, work, hdr, (uint32_t *)(ws + L.gtiles),
+                    !(steps & DIVAS_STEP_GATE_KEEP), s);
         if ((rc = check_launch("divas_fuse(gate)"))) return rc;
     }
     if (steps & DIVAS_STEP_CLEAR_ALL) {
