@@ -625,8 +625,20 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     host = (torch.empty((nv, hm, wm), dtype=torch.float32, pin_memory=True)
             if return_refined else None)
     cam_t = torch.from_numpy(pack_cameras(cams)).to(dev, non_blocking=True)
+    # pageable host arrays (what render_view returns) go through pinned
+    # staging slots filled by host threads (staging.Stager); pinned ones are
+    # DMA sources as they are
+    from .staging import is_pinned, stager
+    first = views[0][1].values if hasattr(views[0][1], "values") else views[0][1]
+    stg = None if is_pinned(first) else stager(dev)
     # 1. density first (the gate count needs it), then every view upload queued
-    dens = as_device(density.values, np.float32, dev, non_blocking=True)
+    dvals = density.values
+    if stg is not None and not isinstance(dvals, torch.Tensor) and not is_pinned(dvals):
+        dens = torch.empty(nvox, dtype=torch.float32, device=dev)
+        stg.copy(dens.data_ptr(), np.ascontiguousarray(dvals, np.float32), cur)
+        stg.flush()
+    else:
+        dens = as_device(dvals, np.float32, dev, non_blocking=True)
     cnt = torch.zeros(256, dtype=torch.uint8, device=dev)
     _native.check(_native.lib().divas_gate_count(ctypes.byref(fuser._args(dens, 0, nvox)),
                                                  _native.ptr(cnt), _native.stream_handle()),
@@ -643,6 +655,11 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     def upload_full(k, v0, v1):
         dt = np.int32 if k == "nsamps" else np.float32
         h2d[0] += sum(sizes[i][0] * sizes[i][1] for i in range(v0, v1)) * 4
+        if stg is not None:
+            for i in range(v0, v1):
+                stg.copy2d(planes[k][i].data_ptr(), 4 * wm,
+                           np.ascontiguousarray(srcs[i][k], dt), up)
+            return
         run = _adjacent_run([srcs[i][k] for i in range(v0, v1)], dt, (hm, wm))
         if run is not None:                   # the views' planes are one host block
             planes[k][v0:v1].copy_(torch.from_numpy(run), non_blocking=True)
@@ -661,12 +678,16 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     with torch.cuda.stream(up):
         for v0, v1 in bounds_k:
             upload_full("raw", v0, v1)
+        if stg is not None:
+            stg.flush()
         raw_done = torch.cuda.Event()
         raw_done.record(up)
         for v0, v1 in bounds_k:
             for k in full_names:
                 if k != "raw":
                     upload_full(k, v0, v1)
+        if stg is not None:
+            stg.flush()
     # the windows need the gated voxels' bounding box: one wait for the density
     # upload, while the full planes above keep the link busy
     rois = None
@@ -708,10 +729,16 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
                     a = np.ascontiguousarray(srcs[i][k], np.float32)
                     keep.append(a)
                     h2d[0] += 4 * (x1 - x0 + 1) * (y1 - y0 + 1)
+                    if stg is not None:
+                        stg.copy2d(planes[k][i].data_ptr() + 4 * (y0 * wm + x0), 4 * wm,
+                                   a[y0:y1 + 1, x0:x1 + 1], up)
+                        continue
                     _native.check(lib.divas_copy2d_h2d(
                         planes[k][i].data_ptr() + 4 * (y0 * wm + x0), 4 * wm,
                         a.ctypes.data + 4 * (y0 * w + x0), 4 * w, 4 * (x1 - x0 + 1), y1 - y0 + 1,
                         _native.stream_handle(up)), "divas_copy2d_h2d")
+            if stg is not None:
+                stg.flush()
             ev = torch.cuda.Event()
             ev.record(up)
             ready.append(ev)
