@@ -76,7 +76,10 @@ def parse():
     ap.add_argument("--slab-config", default="C5", choices=["C5", "C3", "C2", "C1", "none"],
                     help="N > 1 (or DIVAS_FORCE_DIST=1): also time the slab path at this config")
     ap.add_argument("--slab-steps", type=int, default=5)
-    ap.add_argument("--overlap", default="on", choices=["on", "off"],
+    ap.add_argument("--chunk-views", type=int, default=4)
+    ap.add_argument("--graph", default="on", choices=["on", "off"],
+                    help="N = 1: time CUDA-graph replays of the captured step")
+    ap.add_argument("--overlap", default="on", choices=["on", "off", "pipeline"],
                     help="run the density gate on a side stream concurrently with the refine")
     ap.add_argument("--inputs", default="marcher", choices=["marcher", "analytic"],
                     help="view planes + density: the reference's ray marcher and bake run on "
@@ -569,13 +572,23 @@ def run_ours(args):
     #          beside the refine
     # (measured alternative, slower: the zero fill split off (STEP_ZERO) onto a
     # third stream beside the pair kernel -- it displaces pair CTAs)
-    overlap = args.overlap == "on" and not views_mode
+    overlap = args.overlap in ("on", "pipeline") and not views_mode
+    # "pipeline" (N = 1 slab path): views in chunks -- the refine + band pass
+    # of chunk k+1 (HBM-bound) runs on the main stream while the pair kernel
+    # evaluates chunk k on a third stream (compute-bound); the reduction after
+    pipeline = args.overlap == "pipeline" and overlap and not dist_on
     side = torch.cuda.Stream(dev) if overlap else None
+    pstream = torch.cuda.Stream(dev) if pipeline else None
+    chunk = max(1, args.chunk_views)
+    chunks = [(c0, min(nv, c0 + chunk)) for c0 in range(0, nv, chunk)]
+    if pipeline:
+        bands = ViewAux.empty(nv, H, W, dev)
     gate_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)]
                 for _ in range(max(args.steps, 1))]
 
     def step(ev=None, check=False, k=0):
         nonlocal ws, bands
+        stream = torch.cuda.current_stream()          # (the capture stream under a graph)
         if ev is not None:
             ev[0].record(stream)
         fkw = dict(probs=probs, occ=occ_buf if (peer is None or check) else None,
@@ -591,6 +604,34 @@ def run_ours(args):
                                **fkw)["workspace"]
                 if ev is not None:
                     gate_evs[k][1].record(side)
+        if pipeline:
+            ready = []
+            for c0, c1 in chunks:                     # refine chunks back to back (HBM)
+                refine_bands_device(dv.raw_masks[c0:c1], dv.z_surface[c0:c1], dv.nsamps[c0:c1],
+                                    dv.dexps[c0:c1], params, wl.dx,
+                                    aux=bands.view_slices(c0, c1, nv, H, W), planar=False,
+                                    roi=roi.subset(c0, c1) if roi is not None else None)
+                e = torch.cuda.Event()
+                e.record(stream)
+                ready.append(e)
+            if ev is not None:
+                ev[1].record(stream)
+            pstream.wait_stream(side)                 # the gate list and cleared bits
+            with torch.cuda.stream(pstream):
+                for (c0, c1), e in zip(chunks, ready):
+                    pstream.wait_event(e)
+                    fuser.run(wl.density, dv, workspace=ws, steps=_native.STEP_PAIRS,
+                              view_range=(c0, c1), stream=pstream, **dict(fkw, aux=bands))
+            stream.wait_stream(pstream)
+            out = fuser.run(wl.density, dv, workspace=ws, steps=_native.STEP_REDUCE,
+                            **dict(fkw, aux=bands))
+            ws = out["workspace"]
+            if ev is not None:
+                ev[2].record(stream)
+            occ_full = None
+            if ev is not None:
+                ev[3].record(stream)
+            return out, occ_full
         if views_mode:
             if v1 > v0:
                 refine_bands_device(dv.raw_masks[v0:v1], dv.z_surface[v0:v1], dv.nsamps[v0:v1],
@@ -673,16 +714,38 @@ def run_ours(args):
 
     K = args.steps
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    # the whole step (every stream of it) captured once as a CUDA graph and
+    # replayed: no host launch overhead between its ~10-30 launches
+    graph = None
+    if args.graph == "on" and not dist_on:
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+        for _ in range(2):
+            flush.zero_()
+            graph.replay()
+        torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         if dist_on:
             dist.barrier()
         for k in range(K):
             flush.zero_()
-            step(evs[k], k=k)
+            if graph is not None:
+                evs[k][0].record()
+                graph.replay()
+                for e in evs[k][1:]:
+                    e.record()
+            else:
+                step(evs[k], k=k)
         torch.cuda.synchronize()
         if dist_on:
             dist.barrier()
+    if graph is not None:          # sub-spans are not visible inside a graph replay
+        for k in range(K):
+            gate_evs[k][0], gate_evs[k][1] = evs[k][0], evs[k][0]
     t_ref = [a.elapsed_time(b) for a, b, _c, _d in evs]
     # fuse = the gate's own duration (side stream, concurrent with the refine)
     # + pairs / reduce after both streams joined; without overlap one span
@@ -709,9 +772,10 @@ def run_ours(args):
     if overlap:
         # the operators' own durations, without the gate / refine contention:
         # K more steps with the overlap off (the roofline is quoted on these)
-        overlapped = {"refine_ms": float(np.mean(t_ref)), "fuse_ms": float(np.mean(t_fuse)),
-                      "gate_ms": float(np.mean(t_gate))}
-        overlap = False
+        overlapped = ({"refine_ms": float(np.mean(t_ref)), "fuse_ms": float(np.mean(t_fuse)),
+                       "gate_ms": float(np.mean(t_gate))} if graph is None else
+                      {"cuda_graph": True, "pipeline_chunks": len(chunks) if pipeline else None})
+        overlap, pipe_was, pipeline = False, pipeline, False
         torch.cuda.synchronize()
         for k in range(K):
             flush.zero_()
@@ -719,7 +783,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         t_ref = [a.elapsed_time(b) for a, b, _c, _d in evs]
         t_fuse = [b.elapsed_time(c) for _a, b, c, _d in evs]
-        overlap = True
+        overlap, pipeline = True, pipe_was
 
     # --- roofline of the dominant operator --------------------------------------
     peak, peak_kind = measured_peak()
@@ -782,8 +846,9 @@ def run_ours(args):
             extra["incremental"] = run_incremental(args, wl, params, dev, probs)
             extra["incremental"]["full_recompute_ms_for_comparison"] = ms
 
-    # refine: init, minmax, band_pass; fuse: gate_tiles, gate_scan, gate_emit, tile_cull, pairs, reduce
-    launches_per_step = 3 + 6
+    # refine: init, minmax, band_init, band_pass; fuse: gate_tiles, gate_scan, gate_emit,
+    # tile_cull, pairs, reduce (pipeline: refine + tile_cull + pairs per chunk of views)
+    launches_per_step = (3 + 6 * len(chunks) + 1) if pipeline else (4 + 6)
     line = {
         "metric": "voxel-view updates/s", "value": value, "unit": "updates/s",
         "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms,
