@@ -805,6 +805,18 @@ def run_ours(args):
                               "achieved_gbs": v[1] / (v[0] / 1e3) / 1e9,
                               "frac": v[1] / (v[0] / 1e3) / 1e9 / peak}
                           for k, v in ops.items() if k != dom}}
+    # the operator is bound by instruction issue, not HBM:
+    # its warp instructions per launch (committed ncu count of the same step)
+    # against 148 SMs x 4 schedulers x one issue per clock
+    inst = ncu_traffic(args.config, dom + "_inst")
+    if inst:
+        clk_hz = 1e6 * float(clk.summary().get("sm_mhz") or 1965.0)
+        peak_issue = 148 * 4 * clk_hz
+        roofline["issue"] = {"warp_inst_per_launch": inst,
+                             "achieved_inst_per_s": inst / (d_ms / 1e3),
+                             "peak_inst_per_s": peak_issue,
+                             "issue_frac": inst / (d_ms / 1e3) / peak_issue,
+                             "source": "profiles/ncu_traffic.json (smsp__inst_executed.sum)"}
 
     # --- stats / parity / cpu baseline (rank 0, N = 1) --------------------------
     torch.cuda.synchronize()
