@@ -13,6 +13,10 @@
 //      the z / n_samples tiles the reduction read last are still L2-resident.
 // HBM bytes per pixel: 8 (reduction) + 16 (apply) minus the L2 hits.
 #include "bands.cuh"
+#include "tma.cuh"
+
+#include <algorithm>
+#include <cstdlib>
 
 namespace divas {
 
@@ -93,6 +97,120 @@ refine_minmax(const float *__restrict__ z, const int32_t *__restrict__ n, int64_
     block_minmax_publish(nmin, nmax, ws + kKeys * v + 2);
 }
 
+// refine_minmax through the TMA engine: each block streams its run of the
+// view's z and n_samples planes through kTmaStages shared-memory stages of
+// kTmaTile elements (1-D cp.async.bulk, one elected thread issues, mbarrier
+// completion), so the loads need no registers and kTmaStages - 1 tiles stay
+// in flight while the block reduces the current one.  Same keys as
+// refine_minmax<4> (min / max are exact in any order).  Needs plane % 4 == 0
+// and 16-byte aligned planes.
+#ifndef DIVAS_TMA_TILE
+#define DIVAS_TMA_TILE 1024
+#endif
+#ifndef DIVAS_TMA_STAGES
+#define DIVAS_TMA_STAGES 4
+#endif
+#ifndef DIVAS_TMA_BPS
+#define DIVAS_TMA_BPS 12
+#endif
+constexpr int kTmaTile = DIVAS_TMA_TILE;   // elements per plane per stage
+constexpr int kTmaStages = DIVAS_TMA_STAGES;
+__global__ void __launch_bounds__(kRefineThreads)
+refine_minmax_tma(const float *__restrict__ z, const int32_t *__restrict__ n, int64_t plane,
+                  uint32_t *__restrict__ ws) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float *sz = reinterpret_cast<float *>(smem);
+    int32_t *sn = reinterpret_cast<int32_t *>(smem + (size_t)kTmaStages * kTmaTile * 4);
+    __shared__ __align__(8) uint64_t full[kTmaStages];
+    const int v = blockIdx.y;
+    const float *zv = z + (int64_t)v * plane;
+    const int32_t *nvp = n + (int64_t)v * plane;
+    // this block's contiguous run of whole tiles (the last may be partial)
+    const int64_t ntiles_v = (plane + kTmaTile - 1) / kTmaTile;
+    const int64_t per = (ntiles_v + gridDim.x - 1) / gridDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * per;
+    const int64_t t1 = min(ntiles_v, t0 + per);
+    uint32_t kmin = 0xffffffffu, kmax = 0u, nmin = 0xffffffffu, nmax = 0u;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int64_t t) {                     // thread 0 only
+        const int s = (int)(t % kTmaStages);
+        const int64_t e0 = t * kTmaTile;
+        const uint32_t cnt = (uint32_t)min((int64_t)kTmaTile, plane - e0);
+        mbar_arrive_expect_tx(&full[s], 8u * cnt);
+        tma_load_1d(sz + (size_t)s * kTmaTile, zv + e0, 4u * cnt, &full[s]);
+        tma_load_1d(sn + (size_t)s * kTmaTile, nvp + e0, 4u * cnt, &full[s]);
+    };
+    if (threadIdx.x == 0)
+        for (int64_t t = t0; t < min(t1, t0 + kTmaStages); ++t) issue(t);
+    for (int64_t t = t0; t < t1; ++t) {
+        const int s = (int)(t % kTmaStages);
+        mbar_wait(&full[s], (uint32_t)(((t - t0) / kTmaStages) & 1));
+        const int64_t e0 = t * kTmaTile;
+        const int cnt = (int)min((int64_t)kTmaTile, plane - e0);
+        const float4 *z4 = reinterpret_cast<const float4 *>(sz + (size_t)s * kTmaTile);
+        const int4 *n4 = reinterpret_cast<const int4 *>(sn + (size_t)s * kTmaTile);
+        for (int i = threadIdx.x; i < cnt / 4; i += blockDim.x) {
+            const float4 zz = z4[i];
+            const int4 nn = n4[i];
+            if (nn.x > 0) { uint32_t k = f32_key(zz.x); kmin = min(kmin, k); kmax = max(kmax, k); }
+            if (nn.y > 0) { uint32_t k = f32_key(zz.y); kmin = min(kmin, k); kmax = max(kmax, k); }
+            if (nn.z > 0) { uint32_t k = f32_key(zz.z); kmin = min(kmin, k); kmax = max(kmax, k); }
+            if (nn.w > 0) { uint32_t k = f32_key(zz.w); kmin = min(kmin, k); kmax = max(kmax, k); }
+            nmin = min(nmin, min(min(nn.x > 0 ? (uint32_t)nn.x : 0xffffffffu,
+                                     nn.y > 0 ? (uint32_t)nn.y : 0xffffffffu),
+                                 min(nn.z > 0 ? (uint32_t)nn.z : 0xffffffffu,
+                                     nn.w > 0 ? (uint32_t)nn.w : 0xffffffffu)));
+            nmax = max(nmax, (uint32_t)max(max(nn.x, nn.y), max(max(nn.z, nn.w), 0)));
+        }
+        __syncthreads();                              // stage s consumed by every thread
+        if (threadIdx.x == 0 && t + kTmaStages < t1) issue(t + kTmaStages);
+    }
+    block_minmax_publish(kmin, kmax, ws + kKeys * v);
+    __syncthreads();
+    block_minmax_publish(nmin, nmax, ws + kKeys * v + 2);
+}
+
+static int blocks_per_view(int64_t plane, int nv);
+
+static void launch_minmax(const float *z, const int32_t *n, int64_t plane, int nv, uint32_t *ws,
+                          cudaStream_t s) {
+    // The TMA pipeline is selected at run time with DIVAS_TMA=1 (measured on
+    // C3: 40.1 us against 39.2 us for refine_minmax<4>'s 128-bit loads, which
+    // already stream at ~5 TB/s; tests/test_gpu_tma.py keeps it exact).
+    static int use_tma = -1;
+    if (use_tma < 0) {
+        const char *e = getenv("DIVAS_TMA");
+        use_tma = (e && e[0] == '1') ? 1 : 0;
+    }
+    const size_t smem = (size_t)kTmaStages * kTmaTile * 8;
+    static unsigned long long attr_set = 0;        // bit per device ordinal < 64
+    if (use_tma && plane % 4 == 0 && ((((uintptr_t)z) | ((uintptr_t)n)) & 15) == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const unsigned long long bit = 1ull << (dev & 63);
+        if (!(__atomic_load_n(&attr_set, __ATOMIC_RELAXED) & bit)) {
+            cudaFuncSetAttribute(refine_minmax_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+            __atomic_fetch_or(&attr_set, bit, __ATOMIC_RELAXED);
+        }
+        // blocks per view: enough for ~3 resident blocks per SM over all views
+        const int64_t ntiles = (plane + kTmaTile - 1) / kTmaTile;
+        int64_t b = std::max<int64_t>(1, std::min<int64_t>(ntiles, (148 * DIVAS_TMA_BPS + nv - 1) / nv));
+        dim3 grid((unsigned)b, (unsigned)nv);
+        refine_minmax_tma<<<grid, kRefineThreads, smem, s>>>(z, n, plane, ws);
+    } else {
+        dim3 grid(blocks_per_view(plane, nv), nv);
+        if (plane % 4 == 0 && ((((uintptr_t)z) | ((uintptr_t)n)) & 15) == 0)
+            refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z, n, plane, ws);
+        else
+            refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z, n, plane, ws);
+    }
+}
+
 template <int VEC>
 __global__ void __launch_bounds__(kRefineThreads)
 refine_apply(const float *__restrict__ mask, const float *__restrict__ z,
@@ -163,11 +281,10 @@ extern "C" int divas_refine(int32_t nv, int64_t hm, int64_t wm, const float *mas
                        ((uintptr_t)out)) & 15) == 0;
     refine_init<<<(nv + 255) / 256, 256, 0, s>>>(ws, nv);
     dim3 grid(blocks_per_view(plane, nv), nv);
+    launch_minmax(z_surface, n_samples, plane, nv, ws, s);
     if (vec) {
-        refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         refine_apply<4><<<grid, kRefineThreads, 0, s>>>(mask, z_surface, n_samples, out, plane, ws);
     } else {
-        refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
         refine_apply<1><<<grid, kRefineThreads, 0, s>>>(mask, z_surface, n_samples, out, plane, ws);
     }
     return check_launch("divas_refine");
@@ -212,7 +329,7 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
     const int4 *r4 = reinterpret_cast<const int4 *>(roi);
     launch_band_init((double2 *)bands, B, nv, s);
     if (vec) {
-        if (!keys) refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
+        if (!keys) launch_minmax(z_surface, n_samples, plane, nv, ws, s);
         // threads per block: enough 4-pixel chunks for the (window) width, in
         // warps, so narrow windows do not idle half of every block
         const int64_t chunks = gw / 4;
@@ -234,7 +351,7 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
                                                  (double2 *)bands, (float2 *)records, nv, r4);
         }
     } else {
-        if (!keys) refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, ws);
+        if (!keys) launch_minmax(z_surface, n_samples, plane, nv, ws, s);
         dim3 bg((unsigned)((gw + 255) / 256), (unsigned)gty, (unsigned)nv);
         band_pass<1, true><<<bg, 256, 0, s>>>(B, mask, z_surface, n_samples, dexp, out, mm,
                                               (double2 *)bands, (float2 *)records, nv, r4);
@@ -261,10 +378,7 @@ extern "C" int divas_refine_minmax(int32_t nv, int64_t hm, int64_t wm, const flo
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t plane = hm * wm;
     refine_init<<<(nv + 255) / 256, 256, 0, s>>>(keys, nv);
-    dim3 grid(blocks_per_view(plane, nv), nv);
-    const bool vec = (wm % 4 == 0) && ((((uintptr_t)z_surface) | ((uintptr_t)n_samples)) & 15) == 0;
-    if (vec) refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, keys);
-    else refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z_surface, n_samples, plane, keys);
+    launch_minmax(z_surface, n_samples, plane, nv, keys, s);
     return check_launch("divas_refine_minmax");
 }
 
