@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DIVAS_ABI_VERSION 9
+#define DIVAS_ABI_VERSION 10
 
 /* error codes */
 #define DIVAS_OK          0

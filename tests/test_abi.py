@@ -39,7 +39,7 @@ def test_library_exports_every_symbol(lib):
 
 
 def test_version_and_error(lib):
-    assert lib.divas_abi_version() == 9
+    assert lib.divas_abi_version() == 10
     assert isinstance(lib.divas_last_error(), bytes)
 
 
