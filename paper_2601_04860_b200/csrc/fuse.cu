@@ -1382,6 +1382,8 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     const double t = (p_cov >= C.thin_pct) ? m_max : p_cov;
     if (m_max < C.thin_accept) { PSTAT(16, 1); PSTAT(17, npix); }   // no vote possible
     if (sup == 0) { PSTAT(18, 1); PSTAT(19, npix); }
+    if (sup == npix) { PSTAT(20, 1); PSTAT(21, npix); }
+    if (npix >= 64) { PSTAT(22, 1); PSTAT(23, npix); }
     if (npix > 0 && t >= C.thin_accept) {
         K.t[(int64_t)view * C.cap + q.slot] = t;
         PSTAT(11, 1);

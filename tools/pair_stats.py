@@ -15,7 +15,8 @@ NAMES = ["pairs", "in_frustum", "valid_px", "thick_try", "thick_depth_ok", "thic
          "thin_gated", "band_tiles", "scan_items", "scan_pixels", "unsure_recounts",
          "thin_votes", "thick_exact_fallback", "corner_exact_fallback", "centre_uncertain",
          "band_too_wide", "items_mmax_below_accept", "pixels_mmax_below_accept",
-         "items_zero_support", "pixels_zero_support"]
+         "items_zero_support", "pixels_zero_support", "items_full_support", "pixels_full_support",
+         "items_64px_or_more", "pixels_64px_or_more"]
 
 
 def main():
