@@ -6,7 +6,12 @@ from paper_2601_04860_b200.geometry import Camera
 import paper_2601_04860_b200.staging as stg_mod
 dev = torch.device("cuda", 0)
 wl = workloads.make("C3", device=dev, source="marcher")
-def host(t): return t.cpu().numpy().copy()
+import os
+PIN = os.environ.get("PIN") == "1"
+def host(t):
+    if PIN:
+        p = torch.empty(t.shape, dtype=t.dtype, pin_memory=True); p.copy_(t); return p.numpy()
+    return t.cpu().numpy().copy()
 planes = {k: host(getattr(wl, k)) for k in ("raw_masks", "z_surface", "dmins", "dmaxs", "dexps", "nsamps")}
 grid = VoxelGrid(wl.g, workloads.GRID_HALF, wl.origin)
 dens = DensityGrid(grid, host(wl.density).reshape(wl.g, wl.g, wl.g))
