@@ -66,6 +66,7 @@ class FusionSession:
         self._fused = False
         self._out = None
         self._graphs = {}          # (view, nv) -> CUDA graph of its re-refine + re-fuse
+        self._rois = None          # per-view record windows (sharding.slab_view_rois)
 
     # -- state ---------------------------------------------------------------
     def _views(self):
@@ -93,16 +94,31 @@ class FusionSession:
                 plane.zero_()
             plane[:h, :w].copy_(torch.from_numpy(np.ascontiguousarray(arr, dt)))
         self.cams[i].copy_(torch.from_numpy(pack_cameras([cam])[0]))
+        self._rois = None          # new camera: new windows (and captured graphs use the old)
+        self._graphs.clear()
         if i == len(self.sizes):
             self.sizes.append((h, w))
         else:
             self.sizes[i] = (h, w)
 
+    def _windows(self):
+        """The views' record windows: the fusion reads no record or band
+        outside the projection of the gated voxels' bounding box (DESIGN.md
+        section 3), so a view's refine + band pass runs only there.  Fixed by
+        the density and the cameras; recomputed when the view set changes."""
+        if self._rois is None or self._rois.nv != self.nv:
+            from .sharding import slab_view_rois
+            self._rois = slab_view_rois(self.density, self.fuser.pv, self.g,
+                                        self.fuser.origin, self.fuser.dx,
+                                        self.cams[:self.nv].cpu().numpy(), self.sizes)
+        return self._rois
+
     def _refine(self, v0, v1):
         recs, bands = self.aux.view_slices(v0, v1, self.max_views, self.hm, self.wm)
         refine_bands_device(self.raw[v0:v1], self.z[v0:v1], self.nsamps[v0:v1],
                             self.dexps[v0:v1], self.fuser.pv, self.fuser.dx,
-                            aux=(recs, bands), planar=False)
+                            aux=(recs, bands), planar=False,
+                            roi=self._windows().subset(v0, v1))
 
     def _fuse(self, v0, v1):
         incr = (v0, v1) if self._fused else None
@@ -205,6 +221,7 @@ class FusionSession:
         self.nv -= 1
         self.sizes.pop()
         self._graphs.clear()
+        self._rois = None
 
     def refuse(self):
         """Full recompute of the current view set (same result, for checking)."""
