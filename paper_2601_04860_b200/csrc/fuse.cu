@@ -1606,9 +1606,12 @@ __device__ __forceinline__ uint32_t view_word_mask(int wd, int view_lo, int view
 
 constexpr int kReduceThreads = 128;
 
-__device__ __forceinline__ void reduce_store(const FuseConst &C, const FuseOut &O, uint32_t vi,
-                                             int n_thick, int n_thin, double sw, double smw,
-                                             double st) {
+// Stores p, the optional votes / sums and the local occupancy of voxel vi;
+// returns the occupancy byte (the peer copies are stored by fuse_reduce,
+// coalesced per warp: peer_store_occ).
+__device__ __forceinline__ uint8_t reduce_store(const FuseConst &C, const FuseOut &O, uint32_t vi,
+                                                int n_thick, int n_thin, double sw, double smw,
+                                                double st) {
     const double denom = sw + (double)n_thin;
     const double p = (denom > C.eps) ? (smw + st) / denom : 0.0;
     O.probs[vi] = p;
@@ -1619,7 +1622,30 @@ __device__ __forceinline__ void reduce_store(const FuseConst &C, const FuseOut &
     if (O.st) O.st[vi] = st;
     const uint8_t oc = (p >= C.occ_thr) ? 1 : 0;
     if (O.occ) O.occ[vi] = oc;
-    for (int r = 0; r < O.n_peers; ++r) O.occ_peers[r][vi] = oc;
+    return oc;
+}
+
+// The reduced voxels' occupancy bytes into every peer buffer (the slab
+// all-gather fused into the reduction).  Called by all 32 lanes; `has` lanes
+// hold voxel vi's byte oc.  Slots run in brick-blocked order, so the four
+// voxels of an iz quad are usually four neighbouring lanes: those publish one
+// 4-byte store per peer (gathered with a match + OR reduction) instead of
+// four 1-byte NVLink stores; any other voxel stores its own byte.
+__device__ __forceinline__ void peer_store_occ(const FuseOut &O, bool has, uint32_t vi,
+                                               uint8_t oc) {
+    const int lane = threadIdx.x & 31;
+    const unsigned key = has ? (vi >> 2) : (0xffffffffu - (unsigned)lane);
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    if (!has) return;
+    if (__popc(grp) == 4) {                               // the whole quad is here
+        const uint32_t word = (uint32_t)oc << (8 * (vi & 3u));
+        const uint32_t all = __reduce_or_sync(grp, word);
+        if (lane == __ffs(grp) - 1)
+            for (int r = 0; r < O.n_peers; ++r)
+                *reinterpret_cast<uint32_t *>(O.occ_peers[r] + (vi & ~3u)) = all;
+    } else {
+        for (int r = 0; r < O.n_peers; ++r) O.occ_peers[r][vi] = oc;
+    }
 }
 
 // One voxel, lists in local memory (any count up to MAXV views).
@@ -1628,10 +1654,11 @@ __device__ __forceinline__ void reduce_store(const FuseConst &C, const FuseOut &
 #endif
 constexpr int kRGroup = DIVAS_RGROUP;          // contribution loads in flight per thread
 template <int MAXV>
-__device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &K,
-                                             const FuseOut &O, const uint32_t *work,
-                                             long long slot) {
+__device__ __forceinline__ uint8_t reduce_local(const FuseConst &C, const Contrib &K,
+                                                const FuseOut &O, const uint32_t *work,
+                                                long long slot, uint32_t &vi_out) {
     const uint32_t vi = work[slot];                          // issued early
+    vi_out = vi;
     double tw[MAXV], tmw[MAXV], tt[MAXV];
     int n_thick = 0, n_thin = 0;
     // contributions are fetched in groups of 4 (all loads in flight before
@@ -1693,7 +1720,7 @@ __device__ __forceinline__ void reduce_local(const FuseConst &C, const Contrib &
     double sw = 0.0, smw = 0.0, st = 0.0;
     for (int i = 0; i < n_thick; ++i) { sw += tw[i]; smw += tmw[i]; }
     for (int i = 0; i < n_thin; ++i) st += tt[i];
-    reduce_store(C, O, vi, n_thick, n_thin, sw, smw, st);
+    return reduce_store(C, O, vi, n_thick, n_thin, sw, smw, st);
 }
 
 // dirty != NULL (incremental update of views [view_lo, view_hi)): only slots
@@ -1706,15 +1733,34 @@ fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work
             int view_hi) {
     const long long n = min((long long)hdr->count, (long long)C.cap);
     const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (slot >= n) return;
-    if (dirty && !dirty[slot]) {
+    if (O.n_peers == 0) {                      // (the common case: no peer buffers)
+        if (slot >= n) return;
+        if (dirty && !dirty[slot]) {
+            uint32_t now = 0;
+            for (int wd = view_lo >> 5; wd <= (view_hi - 1) >> 5; ++wd)
+                now |= (K.bits_thick[(int64_t)wd * C.cap + slot] |
+                        K.bits_thin[(int64_t)wd * C.cap + slot]) &
+                       view_word_mask(wd, view_lo, view_hi);
+            if (!now) return;
+        }
+        uint32_t vi;
+        reduce_local<MAXV>(C, K, O, work, slot, vi);
+        return;
+    }
+    if (slot - (threadIdx.x & 31) >= n) return;           // whole warp past the end
+    bool valid = slot < n;
+    if (valid && dirty && !dirty[slot]) {
         uint32_t now = 0;
         for (int wd = view_lo >> 5; wd <= (view_hi - 1) >> 5; ++wd)
             now |= (K.bits_thick[(int64_t)wd * C.cap + slot] | K.bits_thin[(int64_t)wd * C.cap + slot]) &
                    view_word_mask(wd, view_lo, view_hi);
-        if (!now) return;
+        valid = now != 0;
     }
-    reduce_local<MAXV>(C, K, O, work, slot);
+    uint32_t vi = 0;
+    uint8_t oc = 0;
+    if (valid) oc = reduce_local<MAXV>(C, K, O, work, slot, vi);
+    __syncwarp();
+    peer_store_occ(O, valid, vi, oc);
 }
 
 // ---------------------------------------------------------------------------
