@@ -26,6 +26,18 @@ constexpr int kBandMaxTiles = kBandTile == 8 ? 16 : 36;
 // over the valid pixels (n > 0)
 constexpr int kKeys = 4;
 
+// L2 cache-policy helpers (sm_80+): a fractional evict-last policy and
+// 16-byte stores carrying it
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void st_evict_last(float4 *p, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+                 ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+
 struct BandParams {
     double gamma, beta, bmax, dx;
     int hm, wm, ntx, nty;
@@ -306,6 +318,7 @@ band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict
            const int4 *__restrict__ roi = nullptr) {
     static_assert(kBandTile == 8, "row-split band pass assumes 8x8 tiles");
     const int v = nv - 1 - (int)blockIdx.z;          // reverse view order: L2 reuse of z / n
+    const uint64_t pol = l2_policy_evict_last();
     // the view's window and keys in one round trip (no dependent prologue loads)
     const int4 w = roi ? __ldg(roi + v) : make_int4(0, 0, B.wm - 1, B.hm - 1);
     const uint4 keys = minmax ? __ldg(reinterpret_cast<const uint4 *>(minmax) + v)
@@ -417,8 +430,18 @@ band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict
                 }
             }
             float4 *a4 = reinterpret_cast<float4 *>(recA + q);
-            a4[0] = make_float4(a[0].x, a[0].y, a[1].x, a[1].y);
-            a4[1] = make_float4(a[2].x, a[2].y, a[3].x, a[3].y);
+#ifndef DIVAS_REC_EVICT_LAST
+#define DIVAS_REC_EVICT_LAST 1
+#endif
+            if (DIVAS_REC_EVICT_LAST) {
+                // the pair kernel reads these next: keep them in L2 (evict-last
+                // policy) against the streams running beside this pass
+                st_evict_last(a4, make_float4(a[0].x, a[0].y, a[1].x, a[1].y), pol);
+                st_evict_last(a4 + 1, make_float4(a[2].x, a[2].y, a[3].x, a[3].y), pol);
+            } else {
+                a4[0] = make_float4(a[0].x, a[0].y, a[1].x, a[1].y);
+                a4[1] = make_float4(a[2].x, a[2].y, a[3].x, a[3].y);
+            }
             if (write_b) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
