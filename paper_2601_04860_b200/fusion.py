@@ -567,8 +567,22 @@ def _side_stream(dev, name):
     return _STREAMS[key]
 
 
+_RF_LOCKS = {}
+_RF_LOCKS_GUARD = __import__("threading").Lock()
+
+
 def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
                     return_refined=True, chunk_views=4, windows=True, transfer_stats=None):
+    key = str(device())
+    with _RF_LOCKS_GUARD:
+        lock = _RF_LOCKS.setdefault(key, __import__("threading").Lock())
+    with lock:
+        return _refine_and_fuse(grid, density, views, params, bounds, workers, return_refined,
+                                chunk_views, windows, transfer_stats)
+
+
+def _refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
+                     return_refined=True, chunk_views=4, windows=True, transfer_stats=None):
     """``refine_mask`` on every (ViewGeometry, raw ConfidenceMask) pair, then
     ``fuse`` of the refined set -- the session's update (session.py:204-215)
     as one device pass: each host map is uploaded once, refinement writes the
@@ -800,6 +814,14 @@ def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
         hn = host.numpy()
         masks = [_trusted_mask(hn[i, :h, :w]) for i, (h, w) in enumerate(sizes)]
     return OccupancyGrid(grid, hpn.reshape(g, g, g)), masks
+
+
+refine_and_fuse.__doc__ = (_refine_and_fuse.__doc__ or "") + """
+    Calls on one device are serialised (they share its upload / download
+    streams and pinned staging ring), so callers on several threads -- the
+    reference's service fuses concurrently across sessions (service.py:88-94)
+    -- stay correct.
+    """
 
 
 def gradient_maps_device(views: DeviceViews, eps: float, kappa: float, stream=None):

@@ -42,7 +42,8 @@ class Stager:
     """Ring of ``nslots`` pinned slots of ``slot_bytes`` and ``threads`` host
     copy workers.  ``copy2d`` / ``copy`` enqueue jobs; ``flush`` issues every
     remaining DMA (all on ``stream``).  Not thread-safe: one user at a time
-    (``stager()`` hands out a per-device instance under a lock)."""
+    (``stager()`` hands out one instance per device; ``refine_and_fuse``, its
+    user, serialises calls per device)."""
 
     def __init__(self, slot_bytes=8 << 20, nslots=12, threads=8):
         import torch
