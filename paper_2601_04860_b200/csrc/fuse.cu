@@ -696,8 +696,13 @@ constexpr double kCertRel = 1e-11;
 
 // floor(U) certified for |U - exact| <= E; returns false when undecidable.
 __device__ __forceinline__ bool cert_floor(double U, double E, long long &out) {
+    // (|f| < 2^30: a 32-bit conversion; larger coordinates -- far outside any
+    // image -- take the exact chain)
     const double f = floor(U);
-    if (U - f > E && (f + 1.0) - U > E && fabs(f) < 9.0e18) { out = (long long)f; return true; }
+    if (U - f > E && (f + 1.0) - U > E && fabs(f) < 1073741824.0) {
+        out = (long long)__double2int_rz(f);
+        return true;
+    }
     return false;
 }
 
