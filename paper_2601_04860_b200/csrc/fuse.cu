@@ -1274,8 +1274,36 @@ __device__ __forceinline__ bool scan_exact(const float2 *__restrict__ rp, int wm
     };
     const int rem = bw & 3;
     const int full = bw - rem;
+#ifndef DIVAS_SCAN_2ROWS
+#define DIVAS_SCAN_2ROWS 1
+#endif
+    int y = 0;
+    if (DIVAS_SCAN_2ROWS) {
+        // two rows per pass: eight loads in flight per group, the loop
+        // bookkeeping shared by both rows
 #pragma unroll 1
-    for (int y = 0; y < bh; ++y, rp += wm) {
+        for (; y + 1 < bh; y += 2, rp += 2 * wm) {
+            const float2 *rq = rp + wm;
+            int c = 0;
+#pragma unroll 1
+            for (; c < full; c += 4) {
+                float2 r[8];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) { r[j] = __ldg(rp + c + j); r[4 + j] = __ldg(rq + c + j); }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) pix(r[j]);
+            }
+            if (rem & 2) {
+                const float2 a0 = __ldg(rp + c), a1 = __ldg(rp + c + 1);
+                const float2 b0 = __ldg(rq + c), b1 = __ldg(rq + c + 1);
+                pix(a0); pix(a1); pix(b0); pix(b1);
+                c += 2;
+            }
+            if (rem & 1) { const float2 a0 = __ldg(rp + c), b0 = __ldg(rq + c); pix(a0); pix(b0); }
+        }
+    }
+#pragma unroll 1
+    for (; y < bh; ++y, rp += wm) {
         int c = 0;
 #pragma unroll 1
         for (; c < full; c += 4) {
