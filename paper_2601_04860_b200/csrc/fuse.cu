@@ -755,6 +755,16 @@ __device__ __forceinline__ double rcp_fast1(double d) {
     return fma(r, fma(-d, r, 1.0), r);
 }
 
+// 1/sqrt(x) to ~1 ulp: the MUFU seed + two Newton steps in f64 (certified
+// approximations only; 1e-300 < x < 1e300)
+__device__ __forceinline__ double rsqrt_fast(double x) {
+    double y = (double)rsqrtf((float)x);
+    const double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    y = y * fma(-h * y, y, 1.5);
+    return y;
+}
+
 // branch-free min / max of finite doubles (fmin / fmax carry NaN handling)
 __device__ __forceinline__ double dmin2(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double dmax2(double a, double b) { return b > a ? b : a; }
@@ -925,7 +935,9 @@ __device__ __forceinline__ int thick_certified(const FuseConst &C, const Cam &k,
                                                double relz, float dmin, float dmax, double g,
                                                double &tc, bool &need_exact_t) {
     const double L2 = relx * relx + rely * rely + relz * relz;
-    const double L = sqrt(L2);
+    if (!(L2 > 1e-300 && L2 < 1e300)) return 2;
+    const double rL = rsqrt_fast(L2);                 // ~1 ulp: certified below
+    const double L = L2 * rL;
     const double scale = fabs(xc0) + fabs(xc1) + fabs(xc2) + fabs(k.p0) + fabs(k.p1) +
                          fabs(k.p2) + L + fabs((double)dmin) + fabs((double)dmax) + 1.0;
     double E = 1e-10 * scale;
@@ -943,7 +955,7 @@ __device__ __forceinline__ int thick_certified(const FuseConst &C, const Cam &k,
     if (clamp == 0) {
         pcx = xc0; pcy = xc1; pcz = xc2;          // the ray point at t_proj is X
     } else {
-        const double s = t_c / L;
+        const double s = t_c * rL;
         pcx = k.p0 + relx * s;
         pcy = k.p1 + rely * s;
         pcz = k.p2 + relz * s;
@@ -962,11 +974,12 @@ __device__ __forceinline__ int thick_certified(const FuseConst &C, const Cam &k,
         }
     }
     const double ex = xc0 - pcx, ey = xc1 - pcy, ez = xc2 - pcz;
-    const double delta = sqrt(ex * ex + ey * ey + ez * ez);
+    const double d2 = ex * ex + ey * ey + ez * ez;    // delta^2: no sqrt needed
     const float span = dmax - dmin;                                   // f32 site
     const double tau_sp = C.dx * g + C.lam * (double)span;
-    if (delta > tau_sp + E) return 0;
-    if (delta < tau_sp - E) {
+    const double thi = tau_sp + E, tlo = tau_sp - E;
+    if (d2 > thi * thi) return 0;
+    if (tlo > 0.0 && d2 < tlo * tlo) {
         tc = t_c;
         need_exact_t = clamp == 0;
         return 1;
