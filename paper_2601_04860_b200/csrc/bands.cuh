@@ -307,8 +307,19 @@ band_pass(BandParams B, const float *__restrict__ mask, const float *__restrict_
 // loads at a time).  Lane = 8 * rq + c: rows 2 rq, 2 rq + 1 of the 8-row tile
 // band, chunk c of the warp's 32 pixels; a tile (8 x 8) is the 8 lanes
 // {c, c ^ 1} x rq, combined with three shuffles.  Same outputs as band_pass.
-constexpr int kBand2Warps = 4;
-constexpr int kBand2Rows = 4;          // 8-row tile bands per block (grid-stride in y)
+#ifndef DIVAS_BAND_WARPS
+#define DIVAS_BAND_WARPS 4
+#endif
+constexpr int kBand2Warps = DIVAS_BAND_WARPS;
+#ifndef DIVAS_BAND_ROWS
+#define DIVAS_BAND_ROWS 4
+#endif
+constexpr int kBand2Rows = DIVAS_BAND_ROWS;   // 8-row tile bands per block (grid-stride in y)
+#ifndef DIVAS_BAND_RPT
+#define DIVAS_BAND_RPT 1
+#endif
+constexpr int kBandRpt = DIVAS_BAND_RPT;   // rows of the 8-row band per thread (1 or 2)
+constexpr int kBandCpw = 4 * kBandRpt;     // 4-pixel chunks per warp row
 template <bool REFINE>
 __global__ void __launch_bounds__(32 * kBand2Warps)
 band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict__ z,
@@ -347,8 +358,8 @@ band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict
     const int rx0 = w.x, rx1 = min(w.z, B.wm - 1);
     const int ty_first = w.y / kBandTile, ty_last = min(w.w, B.hm - 1) / kBandTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int rq = lane >> 3, c = lane & 7;
-    const int chunk = ((int)blockIdx.x * kBand2Warps + warp) * 8 + c;
+    const int rq = lane / kBandCpw, c = lane % kBandCpw;
+    const int chunk = ((int)blockIdx.x * kBand2Warps + warp) * kBandCpw + c;
     const int x0 = rx0 + chunk * 4;
     const bool active = x0 <= rx1 && x0 < B.wm;
     bool any = false;
@@ -368,11 +379,11 @@ band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict
     int4 nn[2];
     bool ok0 = false, ok1 = false;
     auto load = [&](int ty) {
-        const int row0 = ty * kBandTile + 2 * rq;
+        const int row0 = ty * kBandTile + kBandRpt * rq;
         ok0 = active && ty <= ty_last && row0 < B.hm;
-        ok1 = active && ty <= ty_last && row0 + 1 < B.hm;
+        ok1 = kBandRpt > 1 && active && ty <= ty_last && row0 + 1 < B.hm;
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
+        for (int r = 0; r < kBandRpt; ++r) {
             const bool okr = r ? ok1 : ok0;
             const int64_t p = off + (int64_t)(row0 + r) * B.wm + x0;
             mm[r] = okr ? __ldg(reinterpret_cast<const float4 *>(mask + p)) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -389,7 +400,7 @@ band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict
     for (int i = 0; i < kBand2Rows; ++i) {
         const int ty = tyb + i;
         if (ty > ty_last) break;
-        const int row0 = ty * kBandTile + 2 * rq;
+        const int row0 = ty * kBandTile + kBandRpt * rq;
         const bool c0 = ok0, c1 = ok1;
         float4 cm[2] = {mm[0], mm[1]}, cd[2] = {dd[0], dd[1]}, cz[2] = {zz[0], zz[1]};
         int4 cn[2] = {nn[0], nn[1]};
@@ -397,7 +408,7 @@ band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict
         float lo = __int_as_float(0x7f800000);      // +inf
         float hi = -lo;
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
+        for (int r = 0; r < kBandRpt; ++r) {
             if (!(r ? c1 : c0)) continue;
             const int64_t p = off + (int64_t)(row0 + r) * B.wm + x0;
             float m[4] = {cm[r].x, cm[r].y, cm[r].z, cm[r].w};
@@ -451,10 +462,11 @@ band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict
         // the 8 lanes of a tile: chunk pair (xor 1) x row pairs (xor 8, 16)
         lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
         hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 1));
-        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 8));
-        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 8));
-        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, 16));
-        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, 16));
+#pragma unroll
+        for (int o = kBandCpw; o < 32; o <<= 1) {          // the tile's other row groups
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
         if (active && rq == 0 && (c & 1) == 0)
             bv[(int64_t)ty * B.ntx + x0 / kBandTile] = make_double2((double)lo, (double)hi);
     }

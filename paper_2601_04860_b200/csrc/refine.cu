@@ -338,7 +338,7 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
 #endif
         if (DIVAS_BAND_ROWSPLIT && kBandTile == 8) {
             // row-split pass: 8 chunks per warp, kBand2Warps warps per block
-            const int64_t per = 8 * kBand2Warps;
+            const int64_t per = kBandCpw * kBand2Warps;
             dim3 bg((unsigned)((chunks + per - 1) / per),
                     (unsigned)((gty + kBand2Rows - 1) / kBand2Rows), (unsigned)nv);
             band_pass2<true><<<bg, 32 * kBand2Warps, 0, s>>>(B, mask, z_surface, n_samples, dexp,
