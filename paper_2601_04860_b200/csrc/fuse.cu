@@ -1455,7 +1455,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
 // scan into a shared-memory queue; phase B runs them on densely packed warps.
 __device__ __forceinline__ void pair_tile(const FuseConst &C, const Cam &k,
                                           const float *__restrict__ dens, const FuseMaps &M,
-                                          const Contrib &K, const uint32_t *__restrict__ work,
+                                          const Contrib &K, uint32_t vi,
                                           long long n, long long block0, int view, QItem *s_q,
                                           int *s_nq) {
     const long long slot = block0 + threadIdx.x;
@@ -1463,7 +1463,7 @@ __device__ __forceinline__ void pair_tile(const FuseConst &C, const Cam &k,
     QItem q;
     if (slot < n) {
         q.slot = (uint32_t)slot;
-        q.vi = __ldg(work + slot);
+        q.vi = vi;
         has = pair_route(C, k, dens, M, K, q.vi, view, (int64_t)view * C.cap + slot,
                          (int64_t)(view >> 5) * C.cap + slot, 1u << (view & 31), q.x_d, q.xcam,
                          q.ycam);
@@ -1591,20 +1591,21 @@ tile_cull(FuseConst C, const double *__restrict__ cams, FuseMaps M,
           const uint32_t *__restrict__ work, const WsHeader *__restrict__ hdr, int nviews,
           uint8_t *__restrict__ skip) {
     __shared__ unsigned s_bb[6];
-    const long long n = min((long long)hdr->count, (long long)C.cap);
     const long long block0 = (long long)blockIdx.x * blockDim.x;
     const long long ntiles = gridDim.x;
+    const long long slot = block0 + threadIdx.x;
+    const uint32_t vi = slot < C.cap ? __ldg(work + slot) : 0u;   // beside the count load
+    const long long n = min((long long)hdr->count, (long long)C.cap);
     if (block0 >= n) return;                         // fuse_pairs exits on its own
     if (threadIdx.x == 0) {
         s_bb[0] = s_bb[1] = s_bb[2] = 0xffffffffu;
         s_bb[3] = s_bb[4] = s_bb[5] = 0u;
     }
     __syncthreads();
-    const long long slot = block0 + threadIdx.x;
     unsigned ix = 0xffffffffu, iy = 0xffffffffu, iz = 0xffffffffu;
     unsigned jx = 0u, jy = 0u, jz = 0u;
     if (slot < n) {
-        voxel_coords(C, __ldg(work + slot), ix, iy, iz);
+        voxel_coords(C, vi, ix, iy, iz);
         jx = ix; jy = iy; jz = iz;
     }
     ix = __reduce_min_sync(0xffffffffu, ix); iy = __reduce_min_sync(0xffffffffu, iy);
@@ -1639,16 +1640,21 @@ fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict
            const WsHeader *__restrict__ hdr, int nviews, const uint8_t *__restrict__ skip) {
     __shared__ QItem s_q[kQueue];
     __shared__ int s_nq;
-    const long long n = min((long long)hdr->count, (long long)C.cap);
     const int view = C.view0 + (int)blockIdx.y;
     const long long block0 = (long long)blockIdx.x * blockDim.x;
+    // the count, the skip byte and the slot's voxel are independent loads:
+    // all in flight at once (work holds cap entries)
+    const long long slot = block0 + threadIdx.x;
+    const uint32_t vi = slot < C.cap ? __ldg(work + slot) : 0u;
+    const uint8_t sk = skip ? __ldg(skip + (int64_t)blockIdx.y * gridDim.x + blockIdx.x) : 0;
+    const long long n = min((long long)hdr->count, (long long)C.cap);
     if (block0 >= n) return;                                   // whole CTA idle
-    if (skip && __ldg(skip + (int64_t)blockIdx.y * gridDim.x + blockIdx.x)) return;
+    if (sk) return;
     if (threadIdx.x == 0) s_nq = 0;
     __syncthreads();
     Cam k;
     load_cam(cams + (int64_t)view * kCamStride, k);
-    pair_tile(C, k, dens, M, K, work, n, block0, view, s_q, &s_nq);
+    pair_tile(C, k, dens, M, K, vi, n, block0, view, s_q, &s_nq);
 }
 
 // ---------------------------------------------------------------------------
@@ -1711,17 +1717,15 @@ __device__ __forceinline__ void peer_store_occ(const FuseOut &O, bool has, uint3
 constexpr int kRGroup = DIVAS_RGROUP;          // contribution loads in flight per thread
 template <int MAXV>
 __device__ __forceinline__ uint8_t reduce_local(const FuseConst &C, const Contrib &K,
-                                                const FuseOut &O, const uint32_t *work,
-                                                long long slot, uint32_t &vi_out) {
-    const uint32_t vi = work[slot];                          // issued early
-    vi_out = vi;
+                                                const FuseOut &O, uint32_t vi,
+                                                uint32_t bt0, uint32_t bn0, long long slot) {
     double tw[MAXV], tmw[MAXV], tt[MAXV];
     int n_thick = 0, n_thin = 0;
-    // contributions are fetched in groups of 4 (all loads in flight before
-    // the first insertion), then inserted in view order as before
+    // contributions are fetched in groups of kRGroup (all loads in flight
+    // before the first insertion), then inserted in view order as before
     for (int wd = 0; wd < C.w32; ++wd) {
-        uint32_t bt = K.bits_thick[(int64_t)wd * C.cap + slot];
-        uint32_t bn = K.bits_thin[(int64_t)wd * C.cap + slot];     // both words in flight
+        uint32_t bt = wd ? K.bits_thick[(int64_t)wd * C.cap + slot] : bt0;
+        uint32_t bn = wd ? K.bits_thin[(int64_t)wd * C.cap + slot] : bn0;
         while (bt) {
             double kw[kRGroup], km[kRGroup];
             int c = 0;
@@ -1787,8 +1791,14 @@ __global__ void __launch_bounds__(kReduceThreads)
 fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work,
             const WsHeader *__restrict__ hdr, const uint8_t *__restrict__ dirty, int view_lo,
             int view_hi) {
-    const long long n = min((long long)hdr->count, (long long)C.cap);
     const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // the slot's voxel and first bit words load beside the count (the
+    // arrays hold cap entries per word)
+    const bool in_cap = slot < C.cap;
+    const uint32_t vi = in_cap ? work[slot] : 0u;
+    const uint32_t bt0 = in_cap ? K.bits_thick[slot] : 0u;
+    const uint32_t bn0 = in_cap ? K.bits_thin[slot] : 0u;
+    const long long n = min((long long)hdr->count, (long long)C.cap);
     if (O.n_peers == 0) {                      // (the common case: no peer buffers)
         if (slot >= n) return;
         if (dirty && !dirty[slot]) {
@@ -1799,8 +1809,7 @@ fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work
                        view_word_mask(wd, view_lo, view_hi);
             if (!now) return;
         }
-        uint32_t vi;
-        reduce_local<MAXV>(C, K, O, work, slot, vi);
+        reduce_local<MAXV>(C, K, O, vi, bt0, bn0, slot);
         return;
     }
     if (slot - (threadIdx.x & 31) >= n) return;           // whole warp past the end
@@ -1812,9 +1821,8 @@ fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work
                    view_word_mask(wd, view_lo, view_hi);
         valid = now != 0;
     }
-    uint32_t vi = 0;
     uint8_t oc = 0;
-    if (valid) oc = reduce_local<MAXV>(C, K, O, work, slot, vi);
+    if (valid) oc = reduce_local<MAXV>(C, K, O, vi, bt0, bn0, slot);
     __syncwarp();
     peer_store_occ(O, valid, vi, oc);
 }
