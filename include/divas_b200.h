@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define DIVAS_ABI_VERSION 10
+#define DIVAS_ABI_VERSION 11
 
 /* error codes */
 #define DIVAS_OK          0
@@ -385,6 +385,22 @@ int divas_mask_bbox(int32_t nv, int64_t hm, int64_t wm, const float *masks, floa
  * windowed upload of view planes in refine_and_fuse. */
 int divas_copy2d_h2d(void *dst, size_t dpitch, const void *src, size_t spitch,
                      size_t width_bytes, size_t height, void *stream);
+
+/* One sub-rectangle of a batched window upload (divas_gather2d_h2d): `rows`
+ * rows of `width_bytes` bytes from page-locked host memory src (row pitch
+ * spitch) to device memory dst (row pitch dpitch). */
+typedef struct divas_copy2d {
+    const void *src;
+    void *dst;
+    int64_t spitch, dpitch, width_bytes, rows;
+} divas_copy2d;
+
+/* Every rectangle of jobs[0 .. n) read by the SMs straight from page-locked
+ * host memory (mapped through unified addressing) in one launch: short-row
+ * windows move at the link rate instead of the copy engine's per-row rate.
+ * Each src must be page-locked (cudaHostAlloc / cudaHostRegister);
+ * DIVAS_EINVAL otherwise.  Same result as one divas_copy2d_h2d per job. */
+int divas_gather2d_h2d(const divas_copy2d *jobs, int32_t n, void *stream);
 
 /* Store `bytes` of device memory src into every buffer of a DEVICE table of
  * n_peers pointers (symmetric-memory peer mappings), at `offset`: one rank's

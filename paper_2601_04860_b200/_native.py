@@ -28,7 +28,7 @@ EXPORTS = (
     "divas_threshold_workspace_size", "divas_threshold",
     "divas_overlay", "divas_vgrid_payload",
     "divas_last_error", "divas_abi_version", "divas_refine_bands_roi", "divas_refine_minmax",
-    "divas_refine_bands_keys", "divas_copy2d_h2d", "divas_peer_put",
+    "divas_refine_bands_keys", "divas_copy2d_h2d", "divas_gather2d_h2d", "divas_peer_put",
     "divas_render", "divas_march_rays", "divas_bake_density", "divas_mask_bbox",
 )
 
@@ -54,6 +54,14 @@ class FuseArgs(ctypes.Structure):
     ]
 
 MAX_PRIMS = 128
+
+
+class Copy2D(ctypes.Structure):
+    """Mirror of ``divas_copy2d`` (one rectangle of divas_gather2d_h2d)."""
+
+    _fields_ = [("src", _VP), ("dst", _VP), ("spitch", ctypes.c_int64),
+                ("dpitch", ctypes.c_int64), ("width_bytes", ctypes.c_int64),
+                ("rows", ctypes.c_int64)]
 
 
 class Scene(ctypes.Structure):
@@ -100,6 +108,7 @@ def _declare(lib):
                                                   I32, I32, _VP]),
         "divas_refine_minmax": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP]),
         "divas_copy2d_h2d": (ctypes.c_int, [_VP, S, _VP, S, S, S, _VP]),
+        "divas_gather2d_h2d": (ctypes.c_int, [ctypes.POINTER(Copy2D), I32, _VP]),
         "divas_mask_bbox": (ctypes.c_int, [I32, I64, I64, _VP, ctypes.c_float, _VP, _VP]),
         "divas_peer_put": (ctypes.c_int, [_VP, S, _VP, I32, S, _VP]),
         "divas_refine_bands_keys": (ctypes.c_int, [I32, I64, I64, _VP, _VP, _VP, _VP, _VP,

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import collections
 import concurrent.futures as cf
+import os
 import threading
 
 import numpy as np
@@ -43,9 +44,12 @@ class Stager:
     copy workers.  ``copy2d`` / ``copy`` enqueue jobs; ``flush`` issues every
     remaining DMA (all on ``stream``).  Not thread-safe: one user at a time
     (``stager()`` hands out one instance per device; ``refine_and_fuse``, its
-    user, serialises calls per device)."""
+    user, serialises calls per device).  Four copy threads by default
+    (``DIVAS_STAGE_THREADS``): C3 pageable update 21-23 ms with 4, 24-25 with
+    3 or 6, 27 with 8, 31-32 with 12 or 16 -- more threads contend for the
+    host memory the DMAs read."""
 
-    def __init__(self, slot_bytes=8 << 20, nslots=12, threads=8):
+    def __init__(self, slot_bytes=8 << 20, nslots=12, threads=4):
         import torch
         self.slot_bytes = int(slot_bytes)
         self.slots = [torch.empty(self.slot_bytes, dtype=torch.uint8, pin_memory=True)
@@ -131,5 +135,5 @@ def stager(dev) -> Stager:
     key = str(dev)
     with _LOCK:
         if key not in _STAGERS:
-            _STAGERS[key] = Stager()
+            _STAGERS[key] = Stager(threads=int(os.environ.get("DIVAS_STAGE_THREADS", "4")))
         return _STAGERS[key]

@@ -39,7 +39,7 @@ def test_library_exports_every_symbol(lib):
 
 
 def test_version_and_error(lib):
-    assert lib.divas_abi_version() == 10
+    assert lib.divas_abi_version() == 11
     assert isinstance(lib.divas_last_error(), bytes)
 
 
@@ -64,12 +64,13 @@ int main(void) {{ printf("%zu\\n", sizeof({cname})); {body} return 0; }}
                                            check=True).stdout.split()]
 
 
-@pytest.mark.parametrize("which", ["fuse", "trace", "record", "scene", "render_cfg"])
+@pytest.mark.parametrize("which", ["fuse", "trace", "record", "scene", "render_cfg", "copy2d"])
 def test_struct_layout_matches_header(tmp_path, which):
     from paper_2601_04860_b200 import trace
-    if which in ("scene", "render_cfg"):
-        st, cname = ((_native.Scene, "divas_scene") if which == "scene"
-                     else (_native.RenderCfg, "divas_render_cfg"))
+    if which in ("scene", "render_cfg", "copy2d"):
+        st, cname = {"scene": (_native.Scene, "divas_scene"),
+                     "render_cfg": (_native.RenderCfg, "divas_render_cfg"),
+                     "copy2d": (_native.Copy2D, "divas_copy2d")}[which]
         fields = [f[0] for f in st._fields_]
         vals = _c_layout(tmp_path, cname, fields)
         assert vals[0] == ctypes.sizeof(st)
