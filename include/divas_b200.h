@@ -208,7 +208,10 @@ typedef struct divas_fuse_args {
 #define DIVAS_FB_BAND_WIDE   6   /* band test skipped: box wider than its tiles  */
 #define DIVAS_FB_TILE_SKIP   7   /* (not a fallback) pair tiles rejected whole by
                                     the tile-level band test                    */
-#define DIVAS_NFALLBACK      8
+#define DIVAS_FB_THIN_SORT   8   /* reduction: a voxel's thin sum needed the
+                                    value sort (its view-order sum was not
+                                    certified exact in every order)             */
+#define DIVAS_NFALLBACK      9
 
 /* Workspace bytes for divas_fuse with slot capacity `max_gated`, `nv_cap`
  * views of padded size hm x wm (~ max_gated * (4 + nv_cap * 24.25) bytes for

@@ -81,8 +81,8 @@ class RenderCfg(ctypes.Structure):
 
 # fallback counters (divas_fuse_args.fallbacks), DIVAS_FB_* in the header
 FALLBACKS = ("centre", "thick", "thick_t", "corners", "recount", "thin_gate", "band_wide",
-             "tile_skip")
-NFALLBACK = 8
+             "tile_skip", "thin_sort")
+NFALLBACK = 9
 
 FUSE_FULL = 0
 STEP_GATE, STEP_CLEAR_ALL, STEP_CLEAR_VIEWS, STEP_PAIRS, STEP_REDUCE = 1, 2, 4, 8, 16

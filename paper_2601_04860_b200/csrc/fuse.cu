@@ -1715,12 +1715,37 @@ __device__ __forceinline__ void peer_store_occ(const FuseOut &O, bool has, uint3
 #define DIVAS_RGROUP 8
 #endif
 constexpr int kRGroup = DIVAS_RGROUP;          // contribution loads in flight per thread
+#ifndef DIVAS_THIN_EXACT
+#define DIVAS_THIN_EXACT 1
+#endif
+
+// log2 of the granularity of a finite nonzero f64 (the weight of its lowest
+// set significand bit): every multiple of 2^g up to 2^(g + 53) is exact.
+__device__ __forceinline__ int f64_grain(double t) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(t);
+    const int e = (int)((b >> 52) & 0x7ffu);
+    const unsigned long long sig = (b & 0xfffffffffffffULL) | (e ? (1ULL << 52) : 0ULL);
+    return (e ? e : 1) - 1075 + (__ffsll((long long)sig) - 1);
+}
+
 template <int MAXV>
 __device__ __forceinline__ uint8_t reduce_local(const FuseConst &C, const Contrib &K,
                                                 const FuseOut &O, uint32_t vi,
                                                 uint32_t bt0, uint32_t bn0, long long slot) {
-    double tw[MAXV], tmw[MAXV], tt[MAXV];
+    double tw[MAXV], tmw[MAXV];
     int n_thick = 0, n_thin = 0;
+    // The thin sum (fusion.py:373-386: ascending order, sequential f64 adds)
+    // is first taken in view order, beside a certificate that EVERY order's
+    // partial sums are exact: all t are multiples of 2^g (g = the smallest
+    // granularity among them) and sum |t| < 2^(g + 53) bounds every partial
+    // sum, so each add is exact and the sorted sum equals this one.  Thin
+    // votes carry t = m_max, an f32 mask value >= thin_accept, whenever
+    // thin_accept >= thin_percent_cover (the defaults): the certificate then
+    // always holds and the sort disappears.  Otherwise the values are
+    // sorted as the reference does (second pass below).
+    double st = 0.0, sabs = 0.0;
+    int gmin = 4096;
+    bool thin_ok = true;
     // contributions are fetched in groups of kRGroup (all loads in flight
     // before the first insertion), then inserted in view order as before
     for (int wd = 0; wd < C.w32; ++wd) {
@@ -1769,17 +1794,43 @@ __device__ __forceinline__ uint8_t reduce_local(const FuseConst &C, const Contri
 #pragma unroll
             for (int u = 0; u < kRGroup; ++u) {
                 if (u < c) {
-                    int j = n_thin - 1;    // fusion.py:373-386
-                    while (j >= 0 && tt[j] > kt[u]) { tt[j + 1] = tt[j]; --j; }
-                    tt[j + 1] = kt[u];
+                    const double t = kt[u];
+                    st += t;
+                    sabs += fabs(t);
+                    if (t != 0.0) {
+                        if (!(fabs(t) < 1.0e300)) thin_ok = false;     // inf / NaN
+                        else gmin = min(gmin, f64_grain(t));
+                    }
                     ++n_thin;
                 }
             }
         }
     }
-    double sw = 0.0, smw = 0.0, st = 0.0;
+    // sum |t| rounded up (the adds above round to nearest: relative 2^-46
+    // covers up to 2^6 of them; larger counts take the sorted path)
+    if (!DIVAS_THIN_EXACT || !thin_ok || n_thin > 64 ||
+        (n_thin > 0 && gmin < 4096 &&
+         !(sabs * (1.0 + 1.0 / 70368744177664.0) < ldexp(1.0, min(gmin + 53, 1000))))) {
+        fallback(C, DIVAS_FB_THIN_SORT);
+        double tt[MAXV];
+        n_thin = 0;
+        for (int wd = 0; wd < C.w32; ++wd) {
+            uint32_t bn = K.bits_thin[(int64_t)wd * C.cap + slot];
+            while (bn) {
+                const int view = wd * 32 + __ffs(bn) - 1;
+                bn &= bn - 1;
+                const double t = K.t[(int64_t)view * C.cap + slot];
+                int j = n_thin - 1;        // fusion.py:373-386
+                while (j >= 0 && tt[j] > t) { tt[j + 1] = tt[j]; --j; }
+                tt[j + 1] = t;
+                ++n_thin;
+            }
+        }
+        st = 0.0;
+        for (int i = 0; i < n_thin; ++i) st += tt[i];
+    }
+    double sw = 0.0, smw = 0.0;
     for (int i = 0; i < n_thick; ++i) { sw += tw[i]; smw += tmw[i]; }
-    for (int i = 0; i < n_thin; ++i) st += tt[i];
     return reduce_store(C, O, vi, n_thick, n_thin, sw, smw, st);
 }
 

@@ -81,6 +81,33 @@ def test_lattice_fires_every_exact_fallback():
         assert counts[site] > 0, counts
 
 
+def test_thin_sum_paths_both_run_and_agree():
+    """fuse_reduce's thin sum: the view-order sum, certified exact in every
+    order, for the default parameters (every thin vote's t is an f32 mask
+    value); the reference's value sort where the certificate fails (random
+    thin_percent_cover > thin_accept: t = support / npix votes).  Both
+    bit-identical to the oracle."""
+    import torch
+    from paper_2601_04860_b200 import _native
+    sop = golden_io.scene_cases()["sop"]
+    # defaults: no sort at all
+    got, fb = _gpu(sop)
+    assert np.array_equal(got["probs"], sop.p)
+    counts = dict(zip(_native.FALLBACKS, fb.cpu().tolist()))
+    assert counts["thin_sort"] == 0, counts
+    # random parameters with thin_percent_cover > thin_accept: sorted sums
+    sorted_hits = 0
+    for seed in range(6):
+        c = stress_cases.dense_case(sop, 48, seed=900 + seed)
+        c["pv"][6], c["pv"][8] = 0.9, 0.3           # thin_pct, thin_accept
+        case = _case_obj(f"dense_sort{seed}", c)
+        fb = torch.zeros(_native.NFALLBACK, dtype=torch.int64, device="cuda")
+        got, fb = _gpu(case, fb)
+        _assert_same(got, _oracle(case), case)
+        sorted_hits += int(fb[_native.FALLBACKS.index("thin_sort")].item())
+    assert sorted_hits > 0
+
+
 @pytest.mark.parametrize("seed", [0, 1])
 def test_lattice_larger_vs_oracle(seed):
     """Bigger lattices (G = 64, 128 x 128 px) than the committed goldens."""
