@@ -779,8 +779,14 @@ def _refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
                       "divas_mask_bbox")
         mbox = bbox.cpu().numpy()
     keep = []
+    # the last chunk's windows go after the remaining full planes, so that the
+    # final upload is small and the refined masks of the last chunk download
+    # while it streams (C3: 9.66 ms against 9.72-9.9 with none, 2 or 3)
+    n_tail = 1 if windows and len(bounds_k) > n_pre else 0
     with torch.cuda.stream(up):
-        for v0, v1 in bounds_k:
+        for ci, (v0, v1) in enumerate(bounds_k):
+            if ci == len(bounds_k) - n_tail:
+                upload_fulls(range(n_pre, len(bounds_k)))
             jobs = []                         # pinned sources: one gather launch per chunk
             for k in win_names:
                 if rois is None:
@@ -814,7 +820,8 @@ def _refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
             ev = torch.cuda.Event()
             ev.record(up)
             ready.append(ev)
-        upload_fulls(range(n_pre, len(bounds_k)))
+        if n_tail == 0:
+            upload_fulls(range(n_pre, len(bounds_k)))
     # 2. exact workspace size (the count finished long before the uploads)
     cap = max(int(cnt[:8].view(torch.int64).item()), 1)
     dv = DeviceViews(cam_t, refined if refined is not None else planes["raw"], planes["dmins"],
