@@ -1570,9 +1570,13 @@ __device__ __forceinline__ void tile_culled4(const FuseConst &C, const double *_
         const double lo_ = __shfl_sync(0xffffffffu, dlo, 8 * s);
         const double hi_ = __shfl_sync(0xffffffffu, dhi, 8 * s);
         const double2 *bv = M.bands + (int64_t)(C.view0 + v0 + s) * band_view_stride(C.nty, C.ntx);
+        // i / ntx as a multiply-high by ceil(2^32 / ntx): exact for i * ntx < 2^32
+        // (i < 256, ntx <= 256 here); the divide was a quarter of the kernel
+        const unsigned magic = ntx > 1 ? 0xffffffffu / (unsigned)ntx + 1u : 0u;
         bool hit = false;
         for (int i = lane; i < ntt; i += 32) {
-            const int ty = by + i / ntx, tx = bx + i % ntx;
+            const int q = ntx > 1 ? (int)__umulhi((unsigned)i, magic) : i;
+            const int ty = by + q, tx = bx + (i - q * ntx);
             const double2 b = __ldg(bv + (int64_t)ty * C.ntx + tx);
             hit |= hi_ >= b.x && lo_ <= b.y;
         }
