@@ -1721,7 +1721,7 @@ __device__ __forceinline__ void peer_store_occ(const FuseOut &O, bool has, uint3
 
 // One voxel, lists in local memory (any count up to MAXV views).
 #ifndef DIVAS_RGROUP
-#define DIVAS_RGROUP 8
+#define DIVAS_RGROUP 4
 #endif
 constexpr int kRGroup = DIVAS_RGROUP;          // contribution loads in flight per thread
 #ifndef DIVAS_THIN_EXACT
@@ -1847,7 +1847,12 @@ __device__ __forceinline__ uint8_t reduce_local(const FuseConst &C, const Contri
 // that held or now hold a contribution of those views are re-reduced; the
 // others' outputs are already those of the unchanged contribution set.
 template <int MAXV>
-__global__ void __launch_bounds__(kReduceThreads)
+// eight blocks per SM (62 registers with four contribution loads in flight;
+// eight loads needed 76 registers and six blocks): C5 270 -> 201 us cold
+#ifndef DIVAS_REDUCE_MINB
+#define DIVAS_REDUCE_MINB 8
+#endif
+__global__ void __launch_bounds__(kReduceThreads, DIVAS_REDUCE_MINB)
 fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work,
             const WsHeader *__restrict__ hdr, const uint8_t *__restrict__ dirty, int view_lo,
             int view_hi) {
