@@ -1234,7 +1234,8 @@ def run_incremental(args, wl, params, dev, full_probs, updates=200):
                       "device_p50_ms": float(np.percentile(olat, 50)),
                       "api_ms": host_ms,
                       "api": "project_grid_overlay(OccupancyGrid with host probs, ViewGeometry)"
-                             " -> bool (H, W): uploads the 134 MB grid every call",
+                             " -> bool (H, W): uploads the 134 MB grid every call (pageable numpy:"
+                             " through the pinned staging ring)",
                       "device_equals_api": same, "pixels_on": int(mask.sum())}
     return rec
 

@@ -610,12 +610,17 @@ _RF_LOCKS = {}
 _RF_LOCKS_GUARD = __import__("threading").Lock()
 
 
+def _device_lock(dev):
+    """The per-device lock of the shared upload / download streams and the
+    pinned staging ring (``refine_and_fuse``, ``project_grid_overlay``)."""
+    key = str(dev)
+    with _RF_LOCKS_GUARD:
+        return _RF_LOCKS.setdefault(key, __import__("threading").Lock())
+
+
 def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
                     return_refined=True, chunk_views=4, windows=True, transfer_stats=None):
-    key = str(device())
-    with _RF_LOCKS_GUARD:
-        lock = _RF_LOCKS.setdefault(key, __import__("threading").Lock())
-    with lock:
+    with _device_lock(device()):
         return _refine_and_fuse(grid, density, views, params, bounds, workers, return_refined,
                                 chunk_views, windows, transfer_stats)
 
@@ -1005,14 +1010,34 @@ def project_grid_overlay_device(probs, grid, camera, d_min, d_max, n_samples,
     return out
 
 
+def _grid_to_device(probs, dev):
+    """The dense f64 grid on the device.  A pageable numpy grid (134 MB at
+    256^3) goes through the pinned staging ring (``staging.Stager``, host
+    threads + DMA) instead of torch's synchronous pageable copy (~10 GB/s);
+    page-locked grids (what ``fuse`` / ``refine_and_fuse`` return) and torch
+    tensors are copied directly."""
+    import torch
+
+    from .staging import is_pinned, stager
+    if isinstance(probs, torch.Tensor):
+        return as_device(probs, np.float64, dev)
+    a = np.ascontiguousarray(probs, dtype=np.float64)
+    if a.nbytes < (16 << 20) or is_pinned(a):
+        return as_device(a, np.float64, dev, non_blocking=is_pinned(a))
+    t = torch.empty(a.shape, dtype=torch.float64, device=dev)
+    with _device_lock(dev):                   # one user of the staging ring at a time
+        stg = stager(dev)
+        stg.copy(t.data_ptr(), a, torch.cuda.current_stream(dev))
+        stg.flush()                           # host copies done: `a` may go
+    return t
+
+
 def project_grid_overlay(ogrid: OccupancyGrid, view, threshold: float = 0.5,
                          bounds=None) -> np.ndarray:
     """Binary (H, W) mask of pixels whose ray meets a voxel with p >= threshold
     (fusion.py:846-865)."""
-    import torch
     dev = device()
-    probs = ogrid.probs
-    p = probs if isinstance(probs, torch.Tensor) else as_device(probs, np.float64, dev)
+    p = _grid_to_device(ogrid.probs, dev)
     dmin = as_device(view.d_min, np.float32, dev)
     dmax = as_device(view.d_max, np.float32, dev)
     ns = as_device(view.n_samples, np.int32, dev)
