@@ -246,15 +246,33 @@ class DeviceViews:
         names = ["masks", "dmins", "dmaxs", "dexps", "nsamps"] + (["z_surface"] if with_z else [])
         planes = {k: alloc((nv, hm, wm), dtype=torch.int32 if k == "nsamps" else torch.float32,
                            device=dev) for k in names}
-        for i, ((vg, m), (h, w)) in enumerate(zip(views, sizes)):
+        from .staging import is_pinned, stager
+        srcs = []
+        for (vg, m), (h, w) in zip(views, sizes):
             src = {"masks": m.values if hasattr(m, "values") else m, "dmins": vg.d_min,
                    "dmaxs": vg.d_max, "dexps": vg.d_exp, "nsamps": vg.n_samples}
             if with_z:
                 src["z_surface"] = vg.z_surface
+            srcs.append({k: np.ascontiguousarray(src[k], np.int32 if k == "nsamps" else np.float32)
+                         for k in names})
+        # page-locked maps are DMA sources as they are; pageable ones (what
+        # render_view returns) go through the pinned staging ring (host
+        # threads + DMA) instead of torch's synchronous pageable copies
+        pageable = [(i, k) for i in range(nv) for k in names if not is_pinned(srcs[i][k])]
+        if pageable:
+            cur = torch.cuda.current_stream(dev)
+            with _device_lock(dev):
+                stg = stager(dev)
+                for i, k in pageable:
+                    stg.copy2d(planes[k][i].data_ptr(), 4 * wm, srcs[i][k], cur)
+                stg.flush()
+        staged = set(pageable)
+        for i, (h, w) in enumerate(sizes):
             for k in names:
-                dt = np.int32 if k == "nsamps" else np.float32
-                planes[k][i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(src[k], dt)))
+                if (i, k) not in staged:
+                    planes[k][i, :h, :w].copy_(torch.from_numpy(srcs[i][k]), non_blocking=True)
         cam_t = torch.from_numpy(pack_cameras(cams)).to(dev)
+        torch.cuda.current_stream(dev).synchronize()   # the host maps may go after return
         return cls(cam_t, planes["masks"], planes["dmins"], planes["dmaxs"], planes["dexps"],
                    planes["nsamps"], z_surface=planes.get("z_surface"), sizes=sizes)
 
@@ -500,7 +518,7 @@ def _device_inputs(grid, density, views, params, bounds):
     _check_layout(grid, density)
     dev = device()
     dv = DeviceViews.from_views(views, dev)
-    dens = as_device(density.values, np.float32, dev)
+    dens = _staged_to_device(density.values, np.float32, dev)
     return Fuser(grid, params, bounds), dens, dv
 
 
@@ -542,27 +560,6 @@ def fuse_with_stats(grid, density, views, params, bounds=None):
     stats = FusionStats(host["n_thick"], host["n_thin"], host["sw"], host["smw"], host["st"],
                         gated)
     return OccupancyGrid(grid, host["probs"]), stats
-
-
-def _upload_planes(views, masks, dev, names):
-    """Copy host maps straight into padded [nv, hm, wm] device planes."""
-    import torch
-    cams = [vg.camera for vg in views]
-    hm = max(int(c.height) for c in cams)
-    wm = max(int(c.width) for c in cams)
-    sizes = [(int(c.height), int(c.width)) for c in cams]
-    same = all(sz == (hm, wm) for sz in sizes)
-    alloc = torch.empty if same else torch.zeros
-    planes = {k: alloc((len(views), hm, wm), dtype=torch.int32 if k == "nsamps" else torch.float32,
-                       device=dev) for k in names}
-    for i, (vg, m, (h, w)) in enumerate(zip(views, masks, sizes)):
-        src = {"raw": m.values if hasattr(m, "values") else m, "z": vg.z_surface,
-               "dmins": vg.d_min, "dmaxs": vg.d_max, "dexps": vg.d_exp, "nsamps": vg.n_samples}
-        for k in names:
-            dt = np.int32 if k == "nsamps" else np.float32
-            planes[k][i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(src[k], dt)),
-                                       non_blocking=True)
-    return planes, sizes, cams
 
 
 def _trusted_mask(values):
@@ -1010,21 +1007,25 @@ def project_grid_overlay_device(probs, grid, camera, d_min, d_max, n_samples,
     return out
 
 
-def _grid_to_device(probs, dev):
-    """The dense f64 grid on the device.  A pageable numpy grid (134 MB at
-    256^3) goes through the pinned staging ring (``staging.Stager``, host
-    threads + DMA) instead of torch's synchronous pageable copy (~10 GB/s);
-    page-locked grids (what ``fuse`` / ``refine_and_fuse`` return) and torch
-    tensors are copied directly."""
+def _staged_to_device(arr, np_dtype, dev):
+    """A large host array (the dense grid, the density) on the device.  A
+    pageable numpy array goes through the pinned staging ring
+    (``staging.Stager``, host threads + DMA) instead of torch's synchronous
+    pageable copy (~10 GB/s); page-locked arrays (what ``fuse`` /
+    ``refine_and_fuse`` return) and torch tensors are copied directly."""
     import torch
 
     from .staging import is_pinned, stager
-    if isinstance(probs, torch.Tensor):
-        return as_device(probs, np.float64, dev)
-    a = np.ascontiguousarray(probs, dtype=np.float64)
-    if a.nbytes < (16 << 20) or is_pinned(a):
-        return as_device(a, np.float64, dev, non_blocking=is_pinned(a))
-    t = torch.empty(a.shape, dtype=torch.float64, device=dev)
+    if isinstance(arr, torch.Tensor):
+        return as_device(arr, np_dtype, dev)
+    a = np.ascontiguousarray(arr, dtype=np_dtype)
+    pinned = is_pinned(a)
+    if a.nbytes < (16 << 20) or pinned:
+        t = as_device(a, np_dtype, dev, non_blocking=pinned)
+        if pinned:
+            torch.cuda.current_stream(dev).synchronize()   # `a` may go after return
+        return t
+    t = empty(a.shape, np_dtype, dev)
     with _device_lock(dev):                   # one user of the staging ring at a time
         stg = stager(dev)
         stg.copy(t.data_ptr(), a, torch.cuda.current_stream(dev))
@@ -1037,7 +1038,7 @@ def project_grid_overlay(ogrid: OccupancyGrid, view, threshold: float = 0.5,
     """Binary (H, W) mask of pixels whose ray meets a voxel with p >= threshold
     (fusion.py:846-865)."""
     dev = device()
-    p = _grid_to_device(ogrid.probs, dev)
+    p = _staged_to_device(ogrid.probs, np.float64, dev)
     dmin = as_device(view.d_min, np.float32, dev)
     dmax = as_device(view.d_max, np.float32, dev)
     ns = as_device(view.n_samples, np.int32, dev)
