@@ -1015,14 +1015,19 @@ __device__ __forceinline__ double exact_tproj(const Cam &k, double xc0, double x
     return ((xc0 - k.p0) * ddx + (xc1 - k.p1) * ddy + (xc2 - k.p2) * ddz);
 }
 
+#ifndef DIVAS_QSMALL
+#define DIVAS_QSMALL 1
+#endif
 struct QItem {                  // a thin candidate that survived the band test
     uint32_t slot, vi;
+#if !DIVAS_QSMALL
     double x_d, xcam, ycam;
+#endif
 };
 
 constexpr int kQueue = kPairThreads;
 #ifndef DIVAS_CARVEOUT
-#define DIVAS_CARVEOUT 25
+#define DIVAS_CARVEOUT (DIVAS_QSMALL ? 7 : 25)
 #endif
 constexpr int kPairCarveout = DIVAS_CARVEOUT;      // % of the unified L1 / shared memory
 
@@ -1348,8 +1353,19 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     const double xc0 = C.origin0 + ((double)ix + 0.5) * C.dx;
     const double xc1 = C.origin1 + ((double)iy + 0.5) * C.dx;
     const double xc2 = C.origin2 + ((double)iz + 0.5) * C.dx;
+#if DIVAS_QSMALL
+    // the camera-frame centre again, the very operations of pair_route (so
+    // bit-identical): a queue item is 8 bytes, which leaves the pair kernel
+    // a 16 KB shared-memory carve-out and 240 KB of L1 for the scans
+    const double relx = xc0 - k.p0, rely = xc1 - k.p1, relz = xc2 - k.p2;
+    const double q_x_d = -(k.r[2] * relx + k.r[5] * rely + k.r[8] * relz);
+    const double q_xcam = k.r[0] * relx + k.r[3] * rely + k.r[6] * relz;
+    const double q_ycam = k.r[1] * relx + k.r[4] * rely + k.r[7] * relz;
+#else
+    const double q_x_d = q.x_d, q_xcam = q.xcam, q_ycam = q.ycam;
+#endif
     long long xs, xe, ys, ye;
-    if (!thin_bounds(C, k, xc0, xc1, xc2, q.x_d, q.xcam, q.ycam, xs, xe, ys, ye)) return;
+    if (!thin_bounds(C, k, xc0, xc1, xc2, q_x_d, q_xcam, q_ycam, xs, xe, ys, ye)) return;
     const long long wi = (long long)k.w, hi = (long long)k.h;
     if (xe < 0 || xs > wi - 1 || ye < 0 || ys > hi - 1) return;
     if (xs < 0) xs = 0;
@@ -1357,7 +1373,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
     if (xe > wi - 1) xe = wi - 1;
     if (ye > hi - 1) ye = hi - 1;
 #if defined(DIVAS_ABL) && DIVAS_ABL >= 1
-    K.t[(int64_t)view * C.cap + q.slot] = q.x_d + (double)(xe - xs);
+    K.t[(int64_t)view * C.cap + q.slot] = q_x_d + (double)(xe - xs);
     return;
 #endif
     // Footprint scan over record plane A {m, D (NaN: cannot support)} and,
@@ -1375,7 +1391,7 @@ __device__ __forceinline__ void thin_item(const FuseConst &C, const Cam &k, cons
         M.bands + (int64_t)view * band_view_stride(C.nty, C.ntx) + (int64_t)C.nty * C.ntx);
     const uint32_t tk0 = __ldg(te), tk1 = __ldg(te + 1);
     const uint32_t nflag = __ldg(te + 2), nsup = __ldg(te + 3);
-    const double xd = q.x_d;
+    const double xd = q_x_d;
     const float xd32 = (float)xd;
     const float Mg = (float)(9.5367431640625e-07 * (fabs(xd) + C.tau_max));   // 2^-20
     const int bw = (int)(xe - xs) + 1;
@@ -1461,12 +1477,17 @@ __device__ __forceinline__ void pair_tile(const FuseConst &C, const Cam &k,
     const long long slot = block0 + threadIdx.x;
     bool has = false;
     QItem q;
+#if DIVAS_QSMALL
+    double xd_, xcam_, ycam_;                   // (recomputed by thin_item)
+#else
+    double &xd_ = q.x_d, &xcam_ = q.xcam, &ycam_ = q.ycam;
+#endif
     if (slot < n) {
         q.slot = (uint32_t)slot;
         q.vi = vi;
         has = pair_route(C, k, dens, M, K, q.vi, view, (int64_t)view * C.cap + slot,
-                         (int64_t)(view >> 5) * C.cap + slot, 1u << (view & 31), q.x_d, q.xcam,
-                         q.ycam);
+                         (int64_t)(view >> 5) * C.cap + slot, 1u << (view & 31), xd_, xcam_,
+                         ycam_);
     }
     const unsigned ball = __ballot_sync(0xffffffffu, has);
     const int lane = threadIdx.x & 31;
