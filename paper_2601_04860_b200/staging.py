@@ -43,8 +43,9 @@ class Stager:
     """Ring of ``nslots`` pinned slots of ``slot_bytes`` and ``threads`` host
     copy workers.  ``copy2d`` / ``copy`` enqueue jobs; ``flush`` issues every
     remaining DMA (all on ``stream``).  Not thread-safe: one user at a time
-    (``stager()`` hands out one instance per device; ``refine_and_fuse``, its
-    user, serialises calls per device).  Four copy threads by default
+    (``stager()`` hands out one instance per device; its users --
+    ``refine_and_fuse``, ``fuse``'s view upload, ``project_grid_overlay`` --
+    hold the device's lock, ``fusion._device_lock``, while they use it).  Four copy threads by default
     (``DIVAS_STAGE_THREADS``): C3 pageable update 21-23 ms with 4, 24-25 with
     3 or 6, 27 with 8, 31-32 with 12 or 16 -- more threads contend for the
     host memory the DMAs read."""
