@@ -684,212 +684,216 @@ def _refine_and_fuse(grid, density, views, params, bounds=None, workers=None,
     cam_t = torch.from_numpy(pack_cameras(cams)).to(dev, non_blocking=True)
     # the result grid: page-locked, zero-filled by host threads from now on
     hp, hp_fill = _zeroed_host_async(nvox)
-    # pageable host arrays (what render_view returns) go through pinned
-    # staging slots filled by host threads (staging.Stager); pinned ones are
-    # DMA sources as they are
-    from .staging import is_pinned, stager
-    first = views[0][1].values if hasattr(views[0][1], "values") else views[0][1]
-    stg = None if is_pinned(first) else stager(dev)
-    # 1. density first (the gate count needs it), then every view upload queued
-    dvals = density.values
-    if stg is not None and not isinstance(dvals, torch.Tensor) and not is_pinned(dvals):
-        dens = torch.empty(nvox, dtype=torch.float32, device=dev)
-        stg.copy(dens.data_ptr(), np.ascontiguousarray(dvals, np.float32), cur)
-        stg.flush()
-    else:
-        dens = as_device(dvals, np.float32, dev, non_blocking=True)
-    cnt = torch.zeros(256, dtype=torch.uint8, device=dev)
-    _native.check(_native.lib().divas_gate_count(ctypes.byref(fuser._args(dens, 0, nvox)),
-                                                 _native.ptr(cnt), _native.stream_handle()),
-                  "divas_gate_count")
-    up.wait_stream(cur)                       # planes allocated on the current stream
-    chunk = max(1, int(chunk_views))
-    bounds_k = [(v0, min(nv, v0 + chunk)) for v0 in range(0, nv, chunk)]
-    ready = []
-    srcs = [{"raw": m.values if hasattr(m, "values") else m, "z": vg.z_surface, "dmins": vg.d_min,
-             "dmaxs": vg.d_max, "dexps": vg.d_exp, "nsamps": vg.n_samples} for vg, m in views]
-
-    h2d = [int(np.asarray(density.values).size) * 4]
-
-    def upload_full(k, v0, v1):
-        dt = np.int32 if k == "nsamps" else np.float32
-        h2d[0] += sum(sizes[i][0] * sizes[i][1] for i in range(v0, v1)) * 4
-        if stg is not None:
-            for i in range(v0, v1):
-                stg.copy2d(planes[k][i].data_ptr(), 4 * wm,
-                           np.ascontiguousarray(srcs[i][k], dt), up)
-            return
-        run = _adjacent_run([srcs[i][k] for i in range(v0, v1)], dt, (hm, wm))
-        if run is not None:                   # the views' planes are one host block
-            planes[k][v0:v1].copy_(torch.from_numpy(run), non_blocking=True)
-            return
-        for i in range(v0, v1):
-            h, w = sizes[i]
-            planes[k][i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(srcs[i][k], dt)),
-                                       non_blocking=True)
-
-    # with windows, d_exp too is read only inside them (the band pass builds
-    # records there; the planar refinement does not need it)
-    full_names = ("raw", "z", "nsamps") if windows else ("raw", "z", "dexps", "nsamps")
-    win_names = ("dmins", "dmaxs", "dexps") if windows else ("dmins", "dmaxs")
-    full_ready = [None] * len(bounds_k)       # chunk c's full planes are on the device
-
-    def upload_fulls(chunks):
-        for c in chunks:
-            v0, v1 = bounds_k[c]
-            for k in full_names:
-                if k != "raw":
-                    upload_full(k, v0, v1)
-            if stg is not None:
-                stg.flush()
-            full_ready[c] = torch.cuda.Event()
-            full_ready[c].record(up)
-
-    # Upload order: raw masks first (their per-view bounding box narrows the
-    # depth maps' windows); the full z / n_samples planes of the first
-    # chunks keep the link busy while the host waits for that box; then
-    # every window, then the remaining full planes, so that each later
-    # chunk's work can run as soon as its full planes land and the update
-    # ends one chunk after the last upload.
-    n_pre = min(2, len(bounds_k)) if windows else len(bounds_k)
-    with torch.cuda.stream(up):
-        for v0, v1 in bounds_k:
-            upload_full("raw", v0, v1)
-        if stg is not None:
+    try:
+        # pageable host arrays (what render_view returns) go through pinned
+        # staging slots filled by host threads (staging.Stager); pinned ones are
+        # DMA sources as they are
+        from .staging import is_pinned, stager
+        first = views[0][1].values if hasattr(views[0][1], "values") else views[0][1]
+        stg = None if is_pinned(first) else stager(dev)
+        # 1. density first (the gate count needs it), then every view upload queued
+        dvals = density.values
+        if stg is not None and not isinstance(dvals, torch.Tensor) and not is_pinned(dvals):
+            dens = torch.empty(nvox, dtype=torch.float32, device=dev)
+            stg.copy(dens.data_ptr(), np.ascontiguousarray(dvals, np.float32), cur)
             stg.flush()
-        raw_done = torch.cuda.Event()
-        raw_done.record(up)
-        upload_fulls(range(n_pre))
-    # the windows need the gated voxels' bounding box: one wait for the density
-    # upload, while the full planes above keep the link busy
-    rois = None
-    lib = _native.lib()
-    if windows:
-        from .sharding import slab_view_rois
-        rois = slab_view_rois(dens, fuser.pv, g, np.asarray(grid.origin, dtype=np.float64),
-                              fuser.dx, pack_cameras(cams), sizes)
-        # d_min / d_max / d_exp are read only where the refined mask reaches
-        # mask_thr or exceeds 0.5 (refined <= raw) and at those pixels'
-        # 4-neighbours: intersect each window with the mask's box + 1 px
-        thr = np.float32(min(float(fuser.pv[10]), 0.5))
-        if float(thr) > min(float(fuser.pv[10]), 0.5):
-            thr = np.nextafter(thr, np.float32(-np.inf))
-        bbox = torch.empty((nv, 4), dtype=torch.int32, device=dev)
-        cur.wait_event(raw_done)
-        _native.check(lib.divas_mask_bbox(nv, hm, wm, planes["raw"].data_ptr(), float(thr),
-                                          bbox.data_ptr(), _native.stream_handle()),
-                      "divas_mask_bbox")
-        mbox = bbox.cpu().numpy()
-    keep = []
-    # the last chunk's windows go after the remaining full planes, so that the
-    # final upload is small and the refined masks of the last chunk download
-    # while it streams (C3: 9.66 ms against 9.72-9.9 with none, 2 or 3)
-    n_tail = 1 if windows and len(bounds_k) > n_pre else 0
-    with torch.cuda.stream(up):
-        for ci, (v0, v1) in enumerate(bounds_k):
-            if ci == len(bounds_k) - n_tail:
-                upload_fulls(range(n_pre, len(bounds_k)))
-            jobs = []                         # pinned sources: one gather launch per chunk
-            for k in win_names:
-                if rois is None:
-                    upload_full(k, v0, v1)
-                    continue
+        else:
+            dens = as_device(dvals, np.float32, dev, non_blocking=True)
+        cnt = torch.zeros(256, dtype=torch.uint8, device=dev)
+        _native.check(_native.lib().divas_gate_count(ctypes.byref(fuser._args(dens, 0, nvox)),
+                                                     _native.ptr(cnt), _native.stream_handle()),
+                      "divas_gate_count")
+        up.wait_stream(cur)                       # planes allocated on the current stream
+        chunk = max(1, int(chunk_views))
+        bounds_k = [(v0, min(nv, v0 + chunk)) for v0 in range(0, nv, chunk)]
+        ready = []
+        srcs = [{"raw": m.values if hasattr(m, "values") else m, "z": vg.z_surface, "dmins": vg.d_min,
+                 "dmaxs": vg.d_max, "dexps": vg.d_exp, "nsamps": vg.n_samples} for vg, m in views]
+
+        h2d = [int(np.asarray(density.values).size) * 4]
+
+        def upload_full(k, v0, v1):
+            dt = np.int32 if k == "nsamps" else np.float32
+            h2d[0] += sum(sizes[i][0] * sizes[i][1] for i in range(v0, v1)) * 4
+            if stg is not None:
                 for i in range(v0, v1):
-                    h, w = sizes[i]
-                    x0, y0, x1, y1 = (int(c) for c in rois.host[i])
-                    x1, y1 = min(x1, w - 1), min(y1, h - 1)
-                    bx0, by0, bx1, by1 = (int(c) for c in mbox[i])
-                    if bx1 < 0:
-                        continue                  # no pixel can need a depth value
-                    x0, y0 = max(x0, bx0 - 1), max(y0, by0 - 1)
-                    x1, y1 = min(x1, bx1 + 1), min(y1, by1 + 1)
-                    if x1 < x0 or y1 < y0:
-                        continue
-                    a = np.ascontiguousarray(srcs[i][k], np.float32)
-                    keep.append(a)
-                    h2d[0] += 4 * (x1 - x0 + 1) * (y1 - y0 + 1)
-                    if stg is not None:
-                        stg.copy2d(planes[k][i].data_ptr() + 4 * (y0 * wm + x0), 4 * wm,
-                                   a[y0:y1 + 1, x0:x1 + 1], up)
-                        continue
-                    jobs.append((a.ctypes.data + 4 * (y0 * w + x0),
-                                 planes[k][i].data_ptr() + 4 * (y0 * wm + x0), 4 * w, 4 * wm,
-                                 4 * (x1 - x0 + 1), y1 - y0 + 1))
-            if jobs:
-                _upload_windows(lib, jobs, up)
+                    stg.copy2d(planes[k][i].data_ptr(), 4 * wm,
+                               np.ascontiguousarray(srcs[i][k], dt), up)
+                return
+            run = _adjacent_run([srcs[i][k] for i in range(v0, v1)], dt, (hm, wm))
+            if run is not None:                   # the views' planes are one host block
+                planes[k][v0:v1].copy_(torch.from_numpy(run), non_blocking=True)
+                return
+            for i in range(v0, v1):
+                h, w = sizes[i]
+                planes[k][i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(srcs[i][k], dt)),
+                                           non_blocking=True)
+
+        # with windows, d_exp too is read only inside them (the band pass builds
+        # records there; the planar refinement does not need it)
+        full_names = ("raw", "z", "nsamps") if windows else ("raw", "z", "dexps", "nsamps")
+        win_names = ("dmins", "dmaxs", "dexps") if windows else ("dmins", "dmaxs")
+        full_ready = [None] * len(bounds_k)       # chunk c's full planes are on the device
+
+        def upload_fulls(chunks):
+            for c in chunks:
+                v0, v1 = bounds_k[c]
+                for k in full_names:
+                    if k != "raw":
+                        upload_full(k, v0, v1)
+                if stg is not None:
+                    stg.flush()
+                full_ready[c] = torch.cuda.Event()
+                full_ready[c].record(up)
+
+        # Upload order: raw masks first (their per-view bounding box narrows the
+        # depth maps' windows); the full z / n_samples planes of the first
+        # chunks keep the link busy while the host waits for that box; then
+        # every window, then the remaining full planes, so that each later
+        # chunk's work can run as soon as its full planes land and the update
+        # ends one chunk after the last upload.
+        n_pre = min(2, len(bounds_k)) if windows else len(bounds_k)
+        with torch.cuda.stream(up):
+            for v0, v1 in bounds_k:
+                upload_full("raw", v0, v1)
             if stg is not None:
                 stg.flush()
-            ev = torch.cuda.Event()
-            ev.record(up)
-            ready.append(ev)
-        if n_tail == 0:
-            upload_fulls(range(n_pre, len(bounds_k)))
-    # 2. exact workspace size (the count finished long before the uploads)
-    cap = max(int(cnt[:8].view(torch.int64).item()), 1)
-    dv = DeviceViews(cam_t, refined if refined is not None else planes["raw"], planes["dmins"],
-                     planes["dmaxs"], planes["dexps"], planes["nsamps"], sizes=sizes)
-    # The result grid lives in page-locked host memory: zero-filled by the
-    # host while the views upload, and the reduction writes the gated voxels'
-    # p into it directly (unified addressing) -- no gather, copy or scatter.
-    # The gate pass gets no output (probs=None) so it leaves the grid alone.
-    kw = dict(max_gated=cap, aux=aux)
-    out = fuser.run(dens, dv, steps=_native.STEP_GATE | _native.STEP_CLEAR_ALL, probs=False, **kw)
-    kw["workspace"] = out["workspace"]
-    # 3. per chunk: refine -> pairs of those views; refined masks download.
-    # With windows the planar refinement needs only the full planes, so each
-    # chunk's is queued behind them and its download overlaps the rest of
-    # the uploads (the link is full duplex); the scan records / bands and the
-    # pairs then wait for the chunk's windows.
-    for c, ((v0, v1), ev) in enumerate(zip(bounds_k, ready)):
-        if rois is not None:
-            cur.wait_event(full_ready[c])
-            keys = keys_all[v0:v1]
-            if return_refined:
-                refine_masks_device(planes["raw"][v0:v1], planes["z"][v0:v1],
-                                    planes["nsamps"][v0:v1], out=refined[v0:v1], keys=keys)
+            raw_done = torch.cuda.Event()
+            raw_done.record(up)
+            upload_fulls(range(n_pre))
+        # the windows need the gated voxels' bounding box: one wait for the density
+        # upload, while the full planes above keep the link busy
+        rois = None
+        lib = _native.lib()
+        if windows:
+            from .sharding import slab_view_rois
+            rois = slab_view_rois(dens, fuser.pv, g, np.asarray(grid.origin, dtype=np.float64),
+                                  fuser.dx, pack_cameras(cams), sizes)
+            # d_min / d_max / d_exp are read only where the refined mask reaches
+            # mask_thr or exceeds 0.5 (refined <= raw) and at those pixels'
+            # 4-neighbours: intersect each window with the mask's box + 1 px
+            thr = np.float32(min(float(fuser.pv[10]), 0.5))
+            if float(thr) > min(float(fuser.pv[10]), 0.5):
+                thr = np.nextafter(thr, np.float32(-np.inf))
+            bbox = torch.empty((nv, 4), dtype=torch.int32, device=dev)
+            cur.wait_event(raw_done)
+            _native.check(lib.divas_mask_bbox(nv, hm, wm, planes["raw"].data_ptr(), float(thr),
+                                              bbox.data_ptr(), _native.stream_handle()),
+                          "divas_mask_bbox")
+            mbox = bbox.cpu().numpy()
+        keep = []
+        # the last chunk's windows go after the remaining full planes, so that the
+        # final upload is small and the refined masks of the last chunk download
+        # while it streams (C3: 9.66 ms against 9.72-9.9 with none, 2 or 3)
+        n_tail = 1 if windows and len(bounds_k) > n_pre else 0
+        with torch.cuda.stream(up):
+            for ci, (v0, v1) in enumerate(bounds_k):
+                if ci == len(bounds_k) - n_tail:
+                    upload_fulls(range(n_pre, len(bounds_k)))
+                jobs = []                         # pinned sources: one gather launch per chunk
+                for k in win_names:
+                    if rois is None:
+                        upload_full(k, v0, v1)
+                        continue
+                    for i in range(v0, v1):
+                        h, w = sizes[i]
+                        x0, y0, x1, y1 = (int(c) for c in rois.host[i])
+                        x1, y1 = min(x1, w - 1), min(y1, h - 1)
+                        bx0, by0, bx1, by1 = (int(c) for c in mbox[i])
+                        if bx1 < 0:
+                            continue                  # no pixel can need a depth value
+                        x0, y0 = max(x0, bx0 - 1), max(y0, by0 - 1)
+                        x1, y1 = min(x1, bx1 + 1), min(y1, by1 + 1)
+                        if x1 < x0 or y1 < y0:
+                            continue
+                        a = np.ascontiguousarray(srcs[i][k], np.float32)
+                        keep.append(a)
+                        h2d[0] += 4 * (x1 - x0 + 1) * (y1 - y0 + 1)
+                        if stg is not None:
+                            stg.copy2d(planes[k][i].data_ptr() + 4 * (y0 * wm + x0), 4 * wm,
+                                       a[y0:y1 + 1, x0:x1 + 1], up)
+                            continue
+                        jobs.append((a.ctypes.data + 4 * (y0 * w + x0),
+                                     planes[k][i].data_ptr() + 4 * (y0 * wm + x0), 4 * w, 4 * wm,
+                                     4 * (x1 - x0 + 1), y1 - y0 + 1))
+                if jobs:
+                    _upload_windows(lib, jobs, up)
+                if stg is not None:
+                    stg.flush()
+                ev = torch.cuda.Event()
+                ev.record(up)
+                ready.append(ev)
+            if n_tail == 0:
+                upload_fulls(range(n_pre, len(bounds_k)))
+        # 2. exact workspace size (the count finished long before the uploads)
+        cap = max(int(cnt[:8].view(torch.int64).item()), 1)
+        dv = DeviceViews(cam_t, refined if refined is not None else planes["raw"], planes["dmins"],
+                         planes["dmaxs"], planes["dexps"], planes["nsamps"], sizes=sizes)
+        # The result grid lives in page-locked host memory: zero-filled by the
+        # host while the views upload, and the reduction writes the gated voxels'
+        # p into it directly (unified addressing) -- no gather, copy or scatter.
+        # The gate pass gets no output (probs=None) so it leaves the grid alone.
+        kw = dict(max_gated=cap, aux=aux)
+        out = fuser.run(dens, dv, steps=_native.STEP_GATE | _native.STEP_CLEAR_ALL, probs=False, **kw)
+        kw["workspace"] = out["workspace"]
+        # 3. per chunk: refine -> pairs of those views; refined masks download.
+        # With windows the planar refinement needs only the full planes, so each
+        # chunk's is queued behind them and its download overlaps the rest of
+        # the uploads (the link is full duplex); the scan records / bands and the
+        # pairs then wait for the chunk's windows.
+        for c, ((v0, v1), ev) in enumerate(zip(bounds_k, ready)):
+            if rois is not None:
+                cur.wait_event(full_ready[c])
+                keys = keys_all[v0:v1]
+                if return_refined:
+                    refine_masks_device(planes["raw"][v0:v1], planes["z"][v0:v1],
+                                        planes["nsamps"][v0:v1], out=refined[v0:v1], keys=keys)
+                    down.wait_stream(cur)
+                    with torch.cuda.stream(down):
+                        host[v0:v1].copy_(refined[v0:v1], non_blocking=True)
+                else:
+                    refine_minmax_device(planes["z"][v0:v1], planes["nsamps"][v0:v1], keys=keys)
+            cur.wait_event(ev)
+            if rois is not None:
+                refine_bands_device(planes["raw"][v0:v1], planes["z"][v0:v1],
+                                    planes["nsamps"][v0:v1], planes["dexps"][v0:v1], fuser.pv,
+                                    fuser.dx, aux=aux.view_slices(v0, v1, nv, hm, wm), planar=False,
+                                    roi=rois.subset(v0, v1), keys=keys)
+            else:
+                refine_bands_device(planes["raw"][v0:v1], planes["z"][v0:v1],
+                                    planes["nsamps"][v0:v1], planes["dexps"][v0:v1], fuser.pv,
+                                    fuser.dx, out=refined[v0:v1] if return_refined else None,
+                                    aux=aux.view_slices(v0, v1, nv, hm, wm), planar=return_refined)
+            fuser.run(dens, dv, steps=_native.STEP_PAIRS, view_range=(v0, v1), probs=False, **kw)
+            if return_refined and rois is None:
                 down.wait_stream(cur)
                 with torch.cuda.stream(down):
                     host[v0:v1].copy_(refined[v0:v1], non_blocking=True)
-            else:
-                refine_minmax_device(planes["z"][v0:v1], planes["nsamps"][v0:v1], keys=keys)
-        cur.wait_event(ev)
-        if rois is not None:
-            refine_bands_device(planes["raw"][v0:v1], planes["z"][v0:v1],
-                                planes["nsamps"][v0:v1], planes["dexps"][v0:v1], fuser.pv,
-                                fuser.dx, aux=aux.view_slices(v0, v1, nv, hm, wm), planar=False,
-                                roi=rois.subset(v0, v1), keys=keys)
-        else:
-            refine_bands_device(planes["raw"][v0:v1], planes["z"][v0:v1],
-                                planes["nsamps"][v0:v1], planes["dexps"][v0:v1], fuser.pv,
-                                fuser.dx, out=refined[v0:v1] if return_refined else None,
-                                aux=aux.view_slices(v0, v1, nv, hm, wm), planar=return_refined)
-        fuser.run(dens, dv, steps=_native.STEP_PAIRS, view_range=(v0, v1), probs=False, **kw)
-        if return_refined and rois is None:
-            down.wait_stream(cur)
-            with torch.cuda.stream(down):
-                host[v0:v1].copy_(refined[v0:v1], non_blocking=True)
-    # 4. reduction (p lands in hp), then the overflow flag
-    for f in hp_fill:                         # the zero fill ran beside the uploads
-        f.result()
-    fuser.run(dens, dv, steps=_native.STEP_REDUCE, probs=hp, **kw)
-    hdr_h = torch.empty(16, dtype=torch.uint8, pin_memory=True)
-    hdr_h.copy_(kw["workspace"][:16], non_blocking=True)
-    cur.synchronize()
-    if int(hdr_h[8:12].view(torch.int32).item()) != 0:
-        raise RuntimeError("divas_fuse: gated voxels exceeded the workspace capacity")
-    hpn = hp.numpy()
-    if transfer_stats is not None:
-        transfer_stats["h2d_bytes"] = h2d[0] + cam_t.numel() * 8
-        # the header, each gated voxel's p (stored into the host grid by the
-        # reduction) and the refined masks
-        transfer_stats["d2h_bytes"] = 16 + 8 * cap + (sum(h * w for h, w in sizes) * 4
-                                                      if return_refined else 0)
-    masks = None
-    if return_refined:
-        down.synchronize()
-        hn = host.numpy()
-        masks = [_trusted_mask(hn[i, :h, :w]) for i, (h, w) in enumerate(sizes)]
-    return OccupancyGrid(grid, hpn.reshape(g, g, g)), masks
+        # 4. reduction (p lands in hp), then the overflow flag
+        for f in hp_fill:                         # the zero fill ran beside the uploads
+            f.result()
+        fuser.run(dens, dv, steps=_native.STEP_REDUCE, probs=hp, **kw)
+        hdr_h = torch.empty(16, dtype=torch.uint8, pin_memory=True)
+        hdr_h.copy_(kw["workspace"][:16], non_blocking=True)
+        cur.synchronize()
+        if int(hdr_h[8:12].view(torch.int32).item()) != 0:
+            raise RuntimeError("divas_fuse: gated voxels exceeded the workspace capacity")
+        hpn = hp.numpy()
+        if transfer_stats is not None:
+            transfer_stats["h2d_bytes"] = h2d[0] + cam_t.numel() * 8
+            # the header, each gated voxel's p (stored into the host grid by the
+            # reduction) and the refined masks
+            transfer_stats["d2h_bytes"] = 16 + 8 * cap + (sum(h * w for h, w in sizes) * 4
+                                                          if return_refined else 0)
+        masks = None
+        if return_refined:
+            down.synchronize()
+            hn = host.numpy()
+            masks = [_trusted_mask(hn[i, :h, :w]) for i, (h, w) in enumerate(sizes)]
+        return OccupancyGrid(grid, hpn.reshape(g, g, g)), masks
+    finally:
+        for f in hp_fill:                     # never leave a fill writing into a freed block
+            f.result()
 
 
 refine_and_fuse.__doc__ = (_refine_and_fuse.__doc__ or "") + """
