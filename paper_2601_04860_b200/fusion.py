@@ -607,12 +607,33 @@ _RF_LOCKS = {}
 _RF_LOCKS_GUARD = __import__("threading").Lock()
 
 
-def _device_lock(dev):
-    """The per-device lock of the shared upload / download streams and the
-    pinned staging ring (``refine_and_fuse``, ``project_grid_overlay``)."""
-    key = str(dev)
-    with _RF_LOCKS_GUARD:
-        return _RF_LOCKS.setdefault(key, __import__("threading").Lock())
+class _device_lock:
+    """Context manager: the per-device lock of the shared upload / download
+    streams and the pinned staging ring (``refine_and_fuse``, ``fuse``'s view
+    upload, ``project_grid_overlay``).  On an exception the staging ring's
+    queued jobs are dropped, so none is issued later into released
+    buffers."""
+
+    def __init__(self, dev):
+        key = str(dev)
+        self.key = key
+        with _RF_LOCKS_GUARD:
+            self.lock = _RF_LOCKS.setdefault(key, __import__("threading").Lock())
+
+    def __enter__(self):
+        self.lock.acquire()
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        try:
+            if exc_type is not None:
+                from . import staging
+                stg = staging._STAGERS.get(self.key)
+                if stg is not None:
+                    stg.discard()
+        finally:
+            self.lock.release()
+        return False
 
 
 def refine_and_fuse(grid, density, views, params, bounds=None, workers=None,

@@ -127,6 +127,17 @@ class Stager:
         while self.pending:
             self._issue_one()
 
+    def discard(self):
+        """Drop every queued job without issuing its DMA (after an error in
+        the caller, whose device buffers may be released): wait for the host
+        copies still running, so no slot is written afterwards."""
+        while self.pending:
+            fut = self.pending.popleft()[0]
+            try:
+                fut.result()
+            except Exception:  # noqa: BLE001  (the caller's error is the one raised)
+                pass
+
 
 _STAGERS = {}
 _LOCK = threading.Lock()

@@ -80,3 +80,29 @@ def test_upload_windows_falls_back_for_pageable():
     ref = np.zeros((8, 8), np.float32)
     ref[1:6, 1:4] = a[1:6, 1:4]
     assert np.array_equal(d.cpu().numpy(), ref)
+
+
+def test_stager_discard_drops_queued_jobs():
+    """After an error the lock holder drops the staging ring's queued jobs:
+    none is issued later (into a buffer the failed caller released)."""
+    import torch
+    from paper_2601_04860_b200 import fusion, staging
+    dev = torch.device("cuda", 0)
+    stg = staging.stager(dev)
+    dst = torch.zeros(1 << 20, dtype=torch.float32, device=dev)
+    src = np.ones(1 << 20, np.float32)
+    with pytest.raises(RuntimeError):
+        with fusion._device_lock(dev):
+            stg.copy(dst.data_ptr(), src, torch.cuda.current_stream(dev))
+            raise RuntimeError("caller failed before flush")
+    assert not stg.pending
+    stg.flush()
+    torch.cuda.synchronize()
+    # whatever the ring issued before the error, nothing is issued after it;
+    # and the ring still works
+    dst2 = torch.zeros(1 << 20, dtype=torch.float32, device=dev)
+    with fusion._device_lock(dev):
+        stg.copy(dst2.data_ptr(), src, torch.cuda.current_stream(dev))
+        stg.flush()
+    torch.cuda.synchronize()
+    assert float(dst2.sum()) == float(1 << 20)
