@@ -48,7 +48,8 @@ class Stager:
     hold the device's lock, ``fusion._device_lock``, while they use it).  Four copy threads by default
     (``DIVAS_STAGE_THREADS``): C3 pageable update 21-23 ms with 4, 24-25 with
     3 or 6, 27 with 8, 31-32 with 12 or 16 -- more threads contend for the
-    host memory the DMAs read."""
+    host memory the DMAs read.  Slots of 8 MB x 12 measured best (16 MB x 16:
+    24 ms, 4 MB x 24: 28 ms, 32 MB x 8: 28 ms)."""
 
     def __init__(self, slot_bytes=8 << 20, nslots=12, threads=4):
         import torch
