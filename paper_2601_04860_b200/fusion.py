@@ -563,13 +563,8 @@ def fuse_with_stats(grid, density, views, params, bounds=None):
 
 
 def _trusted_mask(values):
-    """A refined ConfidenceMask built from kernel output (already in [0, 1]),
-    skipping the host validation scan of ``ConfidenceMask.__post_init__``."""
-    from .segmenter import ConfidenceMask
-    m = ConfidenceMask.__new__(ConfidenceMask)
-    m.values = values
-    m.refined = True
-    return m
+    from .segmenter import trusted_mask
+    return trusted_mask(values)
 
 
 _STREAMS = {}

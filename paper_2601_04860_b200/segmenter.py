@@ -38,6 +38,17 @@ class ConfidenceMask:
         return self.values.shape
 
 
+def trusted_mask(values) -> ConfidenceMask:
+    """A refined ConfidenceMask built from kernel output, skipping the host
+    range scan of ``__post_init__``: the refinement clips to [0, 1] (NaN
+    passes the reference's scan too), so the scan cannot fail (a 762 K-pixel
+    view: ~0.4 ms of host time per mask)."""
+    m = ConfidenceMask.__new__(ConfidenceMask)
+    m.values = values
+    m.refined = True
+    return m
+
+
 def refine_masks_device(masks, z_surface, n_samples, out=None, stream=None, keys=None):
     """Batched refinement of device-resident planes ``[nv, hm, wm]``.
 
@@ -233,7 +244,7 @@ def refine_mask(mask: ConfidenceMask, view) -> ConfidenceMask:
     n = as_device(view.n_samples, np.int32, dev)
     out = empty(m.shape, np.float32, dev)
     refine_masks_device(m, z, n, out=out)
-    return ConfidenceMask(out.cpu().numpy(), refined=True)
+    return trusted_mask(out.cpu().numpy())
 
 
 def refine_masks(masks, views):
@@ -269,5 +280,5 @@ def refine_masks(masks, views):
         N[i, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(v.n_samples, np.int32)))
     out = refine_masks_device(M, Z, N)
     host = out.cpu().numpy()
-    return [ConfidenceMask(host[i, :m.shape[0], :m.shape[1]], refined=True)
+    return [trusted_mask(host[i, :m.shape[0], :m.shape[1]])
             for i, m in enumerate(masks)]
