@@ -69,6 +69,22 @@ __device__ __forceinline__ float refine_px_fast(float m, float z, int32_t n, boo
     if (c < 0.0) c = 0.0;
     if (c > 1.0) c = 1.0;
     const float f = __double2float_rn(c);
+#ifndef DIVAS_REFINE_ICERT
+#define DIVAS_REFINE_ICERT 1
+#endif
+    if (DIVAS_REFINE_ICERT && fabsf(m) <= 1.0f) {
+        // the same certificate in integer arithmetic (E = 2^-48 for |m| <= 1):
+        // for c in [2^e, 2^(e+1)), e >= -22, the only f32 rounding midpoint of
+        // c's f32 interval sits where the low 29 significand bits L equal
+        // 2^28, and one f64 ulp is 2^(e-52), so c +- E stays on one side of
+        // every midpoint iff |L - 2^28| > 2^(4-e) (the binade edges are f32
+        // values, >= 2^(e-25) from any midpoint)
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(c);
+        const int e = (int)((bits >> 52) & 0x7ffu) - 1023;
+        const int L = (int)((uint32_t)bits & 0x1fffffffu) - (1 << 28);
+        if (e >= -22 && e <= 0 && abs(L) > (1 << (4 - e))) return f;
+        return refine_px(m, z, n, any, lo, span);
+    }
     if (f > 1.17549435e-38f && f < 3.0e38f) {
         const double E = 3.552713678800501e-15 * fmax(1.0, fabs((double)m));   // 2^-48 max(1, |m|)
         const double fd = (double)f;
