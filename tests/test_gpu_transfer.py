@@ -106,3 +106,41 @@ def test_stager_discard_drops_queued_jobs():
         stg.flush()
     torch.cuda.synchronize()
     assert float(dst2.sum()) == float(1 << 20)
+
+
+def test_staged_api_uploads_match_device_inputs():
+    """The drop-in APIs' large pageable inputs go through the staging ring
+    (fusion._staged_to_device: >= 16 MiB): fuse() with a 168^3 pageable
+    density and project_grid_overlay() with a 128^3 pageable grid give the
+    same bits as the same data handed over as CUDA tensors."""
+    import torch
+    from paper_2601_04860_b200 import (DensityGrid, FusionParams, OccupancyGrid, VoxelGrid,
+                                       fuse, project_grid_overlay, project_grid_overlay_device)
+    from paper_2601_04860_b200.fusion import DeviceViews, Fuser
+    from tests import golden_io
+    from tests.gpu_cases import reference_objects
+    case = golden_io.scene_cases()["sop"]
+    grid0, _d, views, bounds = reference_objects(case)
+    rng = np.random.default_rng(5)
+    g = 168                                            # 18.9 MB of f32 density
+    grid = VoxelGrid(g, grid0.half_extent, grid0.origin)
+    dens = rng.random((g, g, g), dtype=np.float32) * 6.0
+    dens[dens < 4.5] = 0.0                             # ~25 % gated
+    og = fuse(grid, DensityGrid(grid, dens), views, FusionParams(), bounds=bounds)
+    dev = torch.device("cuda", 0)
+    dv = DeviceViews.from_views(views, dev)
+    out = Fuser(grid, FusionParams(), bounds).run(torch.from_numpy(dens.reshape(-1)).to(dev), dv)
+    ref = out["probs"].cpu().numpy().reshape(g, g, g)
+    assert np.array_equal(og.probs, ref)
+    assert int((ref > 0).sum()) > 0
+    # overlay of a 128^3 grid (16 MiB of f64): pageable numpy vs CUDA tensor
+    g2 = 128
+    grid2 = VoxelGrid(g2, grid0.half_extent, grid0.origin)
+    p = rng.random((g2, g2, g2))
+    vg = views[0][0]
+    got = project_grid_overlay(OccupancyGrid(grid2, p), vg, threshold=0.97)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)   # noqa: E731
+    want = project_grid_overlay_device(t(p.reshape(-1)), grid2, vg.camera, t(vg.d_min),
+                                       t(vg.d_max), t(vg.n_samples), 0.97)
+    want = want.cpu().numpy().astype(bool)
+    assert np.array_equal(got, want) and got.any() and not got.all()
