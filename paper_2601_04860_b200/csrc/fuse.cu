@@ -1090,8 +1090,11 @@ __device__ __forceinline__ bool pair_route(const FuseConst &C, const Cam &k, con
     DIVAS_BOUND(recA + q, recA, plane);
     const float2 ra = __ldg(recA + q);                         // {m, d_exp or NaN}
     const int32_t ns = __ldg(M.nsamps + pix);
-    if (ns <= 0) return false;                                 // valids[view, py, px] == 0
     const float m = fabsf(ra.x);                              // sign: the tau flag
+    // neither path can take a centre mask below both gates, whatever the
+    // pixel's validity: return without waiting for n_samples
+    if (!((double)m >= C.mask_thr) && !((double)m > C.thin_floor)) return false;
+    if (ns <= 0) return false;                                 // valids[view, py, px] == 0
     PSTAT(2, 1);
 #if defined(DIVAS_ABL) && DIVAS_ABL >= 3
     K.t[kidx] = (double)m;
