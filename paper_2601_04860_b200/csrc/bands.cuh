@@ -74,6 +74,7 @@ __device__ __forceinline__ uint32_t tau_key(float t) {   // t >= 0: order-preser
 
 // tau-range entries of views [0, nv) of a band buffer: {UINT_MAX, 0} (empty)
 static __global__ void band_init(double2 *__restrict__ bands, int nv, int nty, int ntx) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v < nv) {
         uint32_t *e = reinterpret_cast<uint32_t *>(bands + v * band_view_stride(nty, ntx) +
@@ -327,6 +328,7 @@ band_pass2(BandParams B, const float *__restrict__ mask, const float *__restrict
            float *__restrict__ refined, const uint32_t *__restrict__ minmax,
            double2 *__restrict__ bands, float2 *__restrict__ records, int nv,
            const int4 *__restrict__ roi = nullptr) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     static_assert(kBandTile == 8, "row-split band pass assumes 8x8 tiles");
     const int v = nv - 1 - (int)blockIdx.z;          // reverse view order: L2 reuse of z / n
     const uint64_t pol = l2_policy_evict_last();
@@ -509,7 +511,7 @@ inline size_t record_bytes(int nv, int hm, int wm) {
 }
 
 static inline void launch_band_init(double2 *bands, const BandParams &B, int nv, cudaStream_t s) {
-    band_init<<<(nv + 255) / 256, 256, 0, s>>>(bands, nv, B.nty, B.ntx);
+    launch_pdl(band_init, dim3((nv + 255) / 256), dim3(256), 0, s, bands, nv, B.nty, B.ntx);
 }
 
 }  // namespace divas

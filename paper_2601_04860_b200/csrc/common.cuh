@@ -10,9 +10,49 @@
 
 #include "../../include/divas_b200.h"
 
+#include <cstdlib>
+#include <utility>
+
 namespace divas {
 
 constexpr int kCamStride = DIVAS_CAM_STRIDE;
+
+// Programmatic dependent launch (sm_90+): a kernel of the step's chains is
+// launched with programmatic stream serialization (launch_pdl), so its blocks
+// are scheduled while the previous kernel's last blocks drain; every such
+// kernel starts with griddep_wait(), which returns once the previous grid has
+// completed and its writes are visible -- nothing is read or written before.
+// Without the launch attribute griddepcontrol.wait is a no-op.
+__device__ __forceinline__ void griddep_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("DIVAS_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on != 0;
+}
+
+// kernel<<<grid, block, smem, s>>>(args...) with the programmatic-serialization
+// attribute (kernel must begin with griddep_wait())
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // numba's int(math.floor(x)) on x86-64 lowers to cvttsd2si: values outside
 // int64 (and NaN) become INT64_MIN.  CUDA's cvt saturates instead, so restate.

@@ -271,6 +271,7 @@ template <bool ZERO>
 __global__ void __launch_bounds__(kGateThreads)
 gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
            uint32_t *__restrict__ tiles) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     __shared__ int s_w[kGateThreads / 32];
     int cnt = 0;
     int64_t base;
@@ -341,6 +342,7 @@ gate_tiles(const float *__restrict__ dens, FuseConst C, FuseOut O, BrickGrid G,
 // consecutive counts per round (a 16^3-brick grid of 256^3 is one round).
 __global__ void __launch_bounds__(1024)
 gate_scan(uint32_t *__restrict__ tiles, int64_t ntiles, int64_t cap, WsHeader *__restrict__ hdr) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     __shared__ unsigned long long s_w[32];
     __shared__ unsigned long long s_carry;
     if (threadIdx.x == 0) s_carry = 0;
@@ -394,6 +396,7 @@ __global__ void __launch_bounds__(kGateThreads)
 gate_emit(const float *__restrict__ dens, FuseConst C, BrickGrid G,
           const uint32_t *__restrict__ tiles, int64_t ntiles, const WsHeader *__restrict__ hdr,
           uint32_t *__restrict__ work) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     constexpr int NW = kGateThreads / 32;
     constexpr int NC = kGateRounds * NW;               // (round, warp) chunks, C order
     static_assert(NC % 32 == 0, "chunk scan");
@@ -1623,6 +1626,7 @@ __global__ void __launch_bounds__(kPairThreads, DIVAS_CULL_MINB)
 tile_cull(FuseConst C, const double *__restrict__ cams, FuseMaps M,
           const uint32_t *__restrict__ work, const WsHeader *__restrict__ hdr, int nviews,
           uint8_t *__restrict__ skip) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     __shared__ unsigned s_bb[6];
     const long long block0 = (long long)blockIdx.x * blockDim.x;
     const long long ntiles = gridDim.x;
@@ -1671,6 +1675,7 @@ __global__ void __launch_bounds__(kPairThreads, DIVAS_PAIR_MINB)
 fuse_pairs(FuseConst C, const double *__restrict__ cams, const float *__restrict__ dens,
            FuseMaps M, Contrib K, const uint32_t *__restrict__ work,
            const WsHeader *__restrict__ hdr, int nviews, const uint8_t *__restrict__ skip) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     __shared__ QItem s_q[kQueue];
     __shared__ int s_nq;
     const int view = C.view0 + (int)blockIdx.y;
@@ -1880,6 +1885,7 @@ __global__ void __launch_bounds__(kReduceThreads, DIVAS_REDUCE_MINB)
 fuse_reduce(FuseConst C, Contrib K, FuseOut O, const uint32_t *__restrict__ work,
             const WsHeader *__restrict__ hdr, const uint8_t *__restrict__ dirty, int view_lo,
             int view_hi) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     const long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     // the slot's voxel and first bit words load beside the count (the
     // arrays hold cap entries per word)
@@ -2216,8 +2222,9 @@ static void launch_gate(const FuseConst &C, const float *dens, const FuseOut &O,
     const int64_t ntiles = (int64_t)G.nbx * G.nby * G.nbz;
     if (zero) gate_tiles<true><<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, O, G, tiles);
     else gate_tiles<false><<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, O, G, tiles);
-    gate_scan<<<1, 1024, 0, s>>>(tiles, ntiles, C.cap, hdr);
-    gate_emit<<<(unsigned)ntiles, kGateThreads, 0, s>>>(dens, C, G, tiles, ntiles, hdr, work);
+    launch_pdl(gate_scan, dim3(1), dim3(1024), 0, s, tiles, ntiles, C.cap, hdr);
+    launch_pdl(gate_emit, dim3((unsigned)ntiles), dim3(kGateThreads), 0, s, dens, C, G, tiles,
+               ntiles, hdr, work);
 }
 
 // records + bands of views [v0, v0 + cnt) from planar refined masks
@@ -2416,11 +2423,12 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         uint8_t *skip = nullptr;
         if (C.cull) {       // tile-level band rejection first (exact, see tile_culled)
             skip = (uint8_t *)(ws + L.skip);
-            tile_cull<<<pg.x, kPairThreads, 0, s>>>(C, a->cams, M, work, hdr, v1 - v0, skip);
+            launch_pdl(tile_cull, dim3(pg.x), dim3(kPairThreads), 0, s, C, a->cams, M, work, hdr,
+                       v1 - v0, skip);
             if ((rc = check_launch("divas_fuse(tile_cull)"))) return rc;
         }
-        fuse_pairs<<<pg, kPairThreads, 0, s>>>(C, a->cams, a->density, M, K, work, hdr, v1 - v0,
-                                               skip);
+        launch_pdl(fuse_pairs, pg, dim3(kPairThreads), 0, s, C, a->cams, a->density, M, K, work,
+                   hdr, v1 - v0, (const uint8_t *)skip);
         if ((rc = check_launch("divas_fuse(pairs)"))) return rc;
     }
     if (steps & DIVAS_STEP_REDUCE) {
@@ -2430,7 +2438,8 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
         const uint8_t *dirty = ((steps & DIVAS_STEP_CLEAR_VIEWS) && (steps & DIVAS_STEP_PAIRS))
                                    ? (const uint8_t *)(ws + L.dirty) : nullptr;
 #define DIVAS_REDUCE(MV) \
-        fuse_reduce<MV><<<rblocks, kReduceThreads, 0, s>>>(C, K, O, work, hdr, dirty, v0, v1)
+        launch_pdl(fuse_reduce<MV>, dim3(rblocks), dim3(kReduceThreads), 0, s, C, K, O, \
+                   (const uint32_t *)work, (const WsHeader *)hdr, dirty, v0, v1)
         if (a->nv <= 32) DIVAS_REDUCE(32);
         else if (a->nv <= 64) DIVAS_REDUCE(64);
         else if (a->nv <= 128) DIVAS_REDUCE(128);

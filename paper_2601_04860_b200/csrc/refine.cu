@@ -23,6 +23,7 @@ namespace divas {
 constexpr int kRefineThreads = 256;
 
 __global__ void refine_init(uint32_t *ws, int nv) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nv) {
         ws[kKeys * i] = 0xffffffffu;      // z min key
@@ -60,6 +61,7 @@ template <int VEC>
 __global__ void __launch_bounds__(kRefineThreads)
 refine_minmax(const float *__restrict__ z, const int32_t *__restrict__ n, int64_t plane,
               uint32_t *__restrict__ ws) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     const int v = blockIdx.y;
     const float *zv = z + (int64_t)v * plane;
     const int32_t *nvp = n + (int64_t)v * plane;
@@ -412,7 +414,7 @@ static void launch_minmax(const float *z, const int32_t *n, int64_t plane, int n
     } else {
         dim3 grid(blocks_per_view(plane, nv), nv);
         if (plane % 4 == 0 && ((((uintptr_t)z) | ((uintptr_t)n)) & 15) == 0)
-            refine_minmax<4><<<grid, kRefineThreads, 0, s>>>(z, n, plane, ws);
+            launch_pdl(refine_minmax<4>, grid, dim3(kRefineThreads), 0, s, z, n, plane, ws);
         else
             refine_minmax<1><<<grid, kRefineThreads, 0, s>>>(z, n, plane, ws);
     }
@@ -573,9 +575,9 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
                     B, mask, z_surface, n_samples, dexp, out, mm, (double2 *)bands,
                     (float2 *)records, nv, r4);
             } else {
-                band_pass2<true><<<bg, 32 * kBand2Warps, 0, s>>>(B, mask, z_surface, n_samples,
-                                                                  dexp, out, mm, (double2 *)bands,
-                                                                  (float2 *)records, nv, r4);
+                launch_pdl(band_pass2<true>, bg, dim3(32 * kBand2Warps), 0, s, B, mask,
+                           z_surface, n_samples, dexp, out, mm, (double2 *)bands,
+                           (float2 *)records, nv, r4);
             }
         } else {
             const int bt = (int)std::min<int64_t>(256, std::max<int64_t>(32, (chunks + 31) / 32 * 32));
