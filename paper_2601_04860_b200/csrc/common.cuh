@@ -23,8 +23,15 @@ constexpr int kCamStride = DIVAS_CAM_STRIDE;
 // kernel starts with griddep_wait(), which returns once the previous grid has
 // completed and its writes are visible -- nothing is read or written before.
 // Without the launch attribute griddepcontrol.wait is a no-op.
+#ifndef DIVAS_PDL_EARLY
+#define DIVAS_PDL_EARLY 1
+#endif
 __device__ __forceinline__ void griddep_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // this block is running: once every block of the grid is, the next kernel
+    // of the stream may start placing its blocks in the slots our tail frees
+    // (they then wait in griddep_wait for this grid to complete)
+    if (DIVAS_PDL_EARLY) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 inline bool pdl_enabled() {
