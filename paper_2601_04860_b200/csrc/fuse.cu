@@ -2109,6 +2109,7 @@ __global__ void pair_trace_kernel(divas_trace_args A, FuseConst C) {
 // (its sums change even if the re-evaluated views add nothing back).
 __global__ void clear_view_bits(Contrib K, int64_t cap, int view_lo, int view_hi,
                                 const WsHeader *__restrict__ hdr, uint8_t *__restrict__ dirty) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     const long long n = min((long long)hdr->count, (long long)cap);
     for (long long slot = (long long)blockIdx.x * blockDim.x + threadIdx.x; slot < n;
          slot += (long long)gridDim.x * blockDim.x) {
@@ -2398,8 +2399,8 @@ extern "C" int divas_fuse(const divas_fuse_args *a, void *workspace, size_t work
     }
     if (steps & DIVAS_STEP_CLEAR_VIEWS) {
         const int64_t blocks = std::min<int64_t>((cap + 255) / 256, (int64_t)sm_count() * 8);
-        clear_view_bits<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
-            K, cap, v0, v1, hdr, (uint8_t *)(ws + L.dirty));
+        launch_pdl(clear_view_bits, dim3((unsigned)std::max<int64_t>(blocks, 1)), dim3(256), 0, s,
+                   K, (int64_t)cap, v0, v1, (const WsHeader *)hdr, (uint8_t *)(ws + L.dirty));
         if ((rc = check_launch("divas_fuse(clear)"))) return rc;
     }
     if (steps & DIVAS_STEP_PAIRS) {

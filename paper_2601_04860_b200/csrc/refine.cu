@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(kRefineThreads)
 refine_apply(const float *__restrict__ mask, const float *__restrict__ z,
              const int32_t *__restrict__ n, float *__restrict__ out, int64_t plane,
              const uint32_t *__restrict__ ws) {
+    griddep_wait();                     // PDL: after the previous kernel completes
     const int v = gridDim.y - 1 - blockIdx.y;   // reverse view order: L2 reuse
     const uint32_t kmin = ws[kKeys * v], kmax = ws[kKeys * v + 1];
     const bool any = kmin <= kmax;
@@ -492,7 +493,8 @@ extern "C" int divas_refine(int32_t nv, int64_t hm, int64_t wm, const float *mas
     dim3 grid(blocks_per_view(plane, nv), nv);
     launch_minmax(z_surface, n_samples, plane, nv, ws, s);
     if (vec) {
-        refine_apply<4><<<grid, kRefineThreads, 0, s>>>(mask, z_surface, n_samples, out, plane, ws);
+        launch_pdl(refine_apply<4>, grid, dim3(kRefineThreads), 0, s, mask, z_surface, n_samples,
+                   out, plane, (const uint32_t *)ws);
     } else {
         refine_apply<1><<<grid, kRefineThreads, 0, s>>>(mask, z_surface, n_samples, out, plane, ws);
     }
