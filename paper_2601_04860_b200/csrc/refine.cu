@@ -22,6 +22,31 @@ namespace divas {
 
 constexpr int kRefineThreads = 256;
 
+// refine_init and band_init in one launch (one kernel boundary less on the
+// refine chain): ws may be null (keys supplied by the caller)
+__global__ void refine_band_init(uint32_t *ws, double2 *__restrict__ bands, int nv, int nty,
+                                 int ntx) {
+    griddep_wait();                     // PDL: after the previous kernel completes
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nv) return;
+    if (ws) {
+        ws[kKeys * v] = 0xffffffffu;
+        ws[kKeys * v + 1] = 0u;
+        ws[kKeys * v + 2] = 0xffffffffu;
+        ws[kKeys * v + 3] = 0u;
+    }
+    uint32_t *e = reinterpret_cast<uint32_t *>(bands + v * band_view_stride(nty, ntx) +
+                                               (int64_t)nty * ntx);
+    e[0] = 0xffffffffu;
+    e[1] = 0u;
+    e[2] = 0u;
+    e[3] = 0u;
+    e[4] = 0x7fc00000u;
+    e[5] = 0xffffffffu;
+    e[6] = 0u;
+    e[7] = 0u;
+}
+
 __global__ void refine_init(uint32_t *ws, int nv) {
     griddep_wait();                     // PDL: after the previous kernel completes
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -528,17 +553,17 @@ static int refine_bands_impl(int32_t nv, int64_t hm, int64_t wm, const float *ma
                        ((uintptr_t)out) | ((uintptr_t)dexp) | ((uintptr_t)records)) & 15) == 0;
     // keys: the views' z min / max computed elsewhere (divas_refine_minmax,
     // e.g. by another rank); else computed here
-    if (!keys) refine_init<<<(nv + 255) / 256, 256, 0, s>>>(ws, nv);
     const uint32_t *mm = keys ? keys : ws;
     dim3 grid(blocks_per_view(plane, nv), nv);
     const BandParams B = band_params(pv, dx_vox, (int)hm, (int)wm);
+    launch_pdl(refine_band_init, dim3((nv + 255) / 256), dim3(256), 0, s, keys ? nullptr : ws,
+               (double2 *)bands, nv, B.nty, B.ntx);
     // grid extent: the whole plane, or the largest window (+ one tile of slack
     // for a window start that is not tile aligned in the caller's numbers)
     const int64_t gw = roi ? std::min<int64_t>(wm, (int64_t)roi_w + kBandTile) : wm;
     const int64_t gty = roi ? std::min<int64_t>(B.nty, (roi_h + kBandTile - 1) / kBandTile + 1)
                             : B.nty;
     const int4 *r4 = reinterpret_cast<const int4 *>(roi);
-    launch_band_init((double2 *)bands, B, nv, s);
     if (vec) {
         if (!keys) launch_minmax(z_surface, n_samples, plane, nv, ws, s);
         // threads per block: enough 4-pixel chunks for the (window) width, in
