@@ -858,9 +858,9 @@ def run_ours(args):
             extra["incremental"] = run_incremental(args, wl, params, dev, probs)
             extra["incremental"]["full_recompute_ms_for_comparison"] = ms
 
-    # refine: init, minmax, band_init, band_pass; fuse: gate_tiles, gate_scan, gate_emit,
-    # tile_cull, pairs, reduce (pipeline: refine + tile_cull + pairs per chunk of views)
-    launches_per_step = (3 + 6 * len(chunks) + 1) if pipeline else (4 + 6)
+    # refine: init (keys + band entries), minmax, band_pass; fuse: gate_tiles, gate_scan,
+    # gate_emit, tile_cull, pairs, reduce (pipeline: refine + tile_cull + pairs per chunk)
+    launches_per_step = (3 + 5 * len(chunks) + 1) if pipeline else (3 + 6)
     line = {
         "metric": "voxel-view updates/s", "value": value, "unit": "updates/s",
         "n_gpus": world, "steps": K, "warmup": max(args.warmup, 3), "ms_per_step": ms,
