@@ -144,3 +144,21 @@ def test_staged_api_uploads_match_device_inputs():
                                        t(vg.d_max), t(vg.n_samples), 0.97)
     want = want.cpu().numpy().astype(bool)
     assert np.array_equal(got, want) and got.any() and not got.all()
+
+
+def test_gather_empty_jobs_are_noops():
+    """No jobs, zero rows or zero width: nothing launched, success."""
+    import torch
+    from paper_2601_04860_b200 import _native
+    lib = _native.lib()
+    s = _native.stream_handle()
+    assert lib.divas_gather2d_h2d(None, 0, s) == 0
+    t = torch.empty(64, dtype=torch.float32, pin_memory=True)
+    d = torch.full((64,), 3.0, dtype=torch.float32, device="cuda")
+    jobs = (_native.Copy2D * 2)(_native.Copy2D(t.data_ptr(), d.data_ptr(), 256, 256, 0, 4),
+                                _native.Copy2D(t.data_ptr(), d.data_ptr(), 256, 256, 64, 0))
+    assert lib.divas_gather2d_h2d(jobs, 2, s) == 0
+    torch.cuda.synchronize()
+    assert float(d.min()) == 3.0 and float(d.max()) == 3.0
+    bad = (_native.Copy2D * 1)(_native.Copy2D(t.data_ptr(), d.data_ptr(), 16, 16, 64, 1))
+    assert lib.divas_gather2d_h2d(bad, 1, s) == 1            # width beyond the pitches
