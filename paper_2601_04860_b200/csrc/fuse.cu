@@ -1600,12 +1600,18 @@ __device__ __forceinline__ void tile_culled4(const FuseConst &C, const double *_
         // i / ntx as a multiply-high by ceil(2^32 / ntx): exact for i * ntx < 2^32
         // (i < 256, ntx <= 256 here); the divide was a quarter of the kernel
         const unsigned magic = ntx > 1 ? 0xffffffffu / (unsigned)ntx + 1u : 0u;
+        // 32 tiles per round; stop at the first round with a hit (kept tiles,
+        // the common case where the projections are large, need one round)
         bool hit = false;
-        for (int i = lane; i < ntt; i += 32) {
-            const int q = ntx > 1 ? (int)__umulhi((unsigned)i, magic) : i;
-            const int ty = by + q, tx = bx + (i - q * ntx);
-            const double2 b = __ldg(bv + (int64_t)ty * C.ntx + tx);
-            hit |= hi_ >= b.x && lo_ <= b.y;
+        for (int i0 = 0; i0 < ntt; i0 += 32) {
+            const int i = i0 + lane;
+            if (i < ntt) {
+                const int q = ntx > 1 ? (int)__umulhi((unsigned)i, magic) : i;
+                const int ty = by + q, tx = bx + (i - q * ntx);
+                const double2 b = __ldg(bv + (int64_t)ty * C.ntx + tx);
+                hit = hi_ >= b.x && lo_ <= b.y;
+            }
+            if (__any_sync(0xffffffffu, hit)) break;
         }
         cull[s] = !__any_sync(0xffffffffu, hit);
     }
